@@ -1,0 +1,132 @@
+/*
+ * ips4o.h -- C ABI of libips4o.so, a B200-native (sm_100a) in-place samplesort.
+ *
+ * The operation is the paper's problem statement (Axtmann et al., "In-place
+ * Parallel Super Scalar Samplesort (IPS4o)", arXiv 1705.02257; PAPER.md:22,
+ * §1): sort A[1..n] in place under a total order on keys, using only
+ * sublinear extra memory.  The method is the paper's
+ * distribution step -- sampling, branchless classification
+ * with equality buckets, block-buffered local
+ * classification (§4.1), block permutation with atomic
+ * fetch-and-add on per-bucket (w,r) pointers (§4.2), cleanup
+ * (§4.3) -- recursed until subproblems fit a base-case sort
+ * (PAPER.md:147-153, 403).
+ *
+ * Element types (all little-endian, contiguous arrays in device memory):
+ *   IPS4O_U64        8 B unsigned integer, ascending unsigned order.
+ *   IPS4O_F64        8 B IEEE double, ascending '<'.  Inputs must contain no NaN and
+ *                    no -0.0 (the order is then total); behaviour is unspecified otherwise.
+ *   IPS4O_PAIR_U64   16 B {uint64 key; uint64 payload}; ordered by key only; unstable:
+ *                    the payload order inside a run of equal keys is unspecified.
+ *   IPS4O_REC100_K10 100 B record; key = bytes [0,10) compared as unsigned bytes
+ *                    (memcmp order); payload = bytes [10,100); unstable.
+ *
+ * Conventions for every entry point:
+ *   - Device pointers are CUDA device memory of the current device; the caller owns it.
+ *   - Work is enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ *     stream).  The call may synchronise `stream` internally between recursion levels
+ *     (it reads back the small per-level task list); it never synchronises other streams.
+ *   - Argument errors return synchronously and leave the data untouched.
+ *   - Device faults surface as IPS4O_ECUDA from this or a later call (CUDA convention).
+ *   - The library owns a lazily grown per-device auxiliary workspace whose size is
+ *     reported by ips4o_aux_bytes(); it is O(k * b * CTAs + tasks), never O(n) beyond that.
+ *   - Calls are serialised by an internal mutex (one sort at a time per process).
+ */
+#ifndef IPS4O_H
+#define IPS4O_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    IPS4O_U64 = 0,
+    IPS4O_F64 = 1,
+    IPS4O_PAIR_U64 = 2,
+    IPS4O_REC100_K10 = 3
+} ips4o_type;
+
+typedef enum {
+    IPS4O_OK = 0,
+    IPS4O_EINVAL = -1,   /* null pointer with n > 0, bad type, n >= 2^40, bad splitters */
+    IPS4O_EALIGN = -2,   /* data pointer not aligned to 8 B (u64/f64), 16 B (pair), 4 B (rec100) */
+    IPS4O_ENOMEM = -3,   /* workspace allocation failed */
+    IPS4O_ECUDA = -4,    /* CUDA launch/runtime error, see ips4o_error_string */
+    IPS4O_EINTERNAL = -5 /* a device-side consistency check failed (conservation, capacity) */
+} ips4o_status;
+
+/* Statistics of the most recent ips4o_sort / ips4o_debug_partition_once call. */
+typedef struct {
+    uint64_t n;                 /* elements sorted */
+    uint32_t elem_type;
+    uint32_t levels;            /* distribution levels executed (multi-CTA tier) */
+    uint64_t distribution_tasks;/* subproblems partitioned by the distribution kernels */
+    uint64_t base_tasks;        /* subproblems finished by the base-case kernel */
+    uint64_t equality_tasks;    /* subproblems partitioned with equality buckets */
+    uint64_t aux_bytes;         /* device workspace bytes reserved for this call */
+    uint64_t kernel_launches;   /* kernels launched by this call */
+    uint64_t host_syncs;        /* stream synchronisations performed (one per level) */
+} ips4o_stats;
+
+/* ---------------------------------------------------------------- sorting */
+
+/* Sort d_data[0..n) ascending, in place.  n = 0 and n = 1 are no-ops.
+ * Returns IPS4O_OK or a negative ips4o_status. */
+int ips4o_sort(void* d_data, uint64_t n, int elem_type, void* stream);
+
+/* Host-buffer convenience entry point (the end-to-end path): copies h_data[0..n) (host
+ * memory; pinned memory gives full PCIe/C2C bandwidth) to a library-owned device buffer,
+ * sorts it there with ips4o_sort, and copies the result back into h_data.  Returns after
+ * the stream has been synchronised.  The device staging buffer is n * elem_size bytes,
+ * reused across calls and released by ips4o_release_workspace(). */
+int ips4o_sort_host(void* h_data, uint64_t n, int elem_type, void* stream);
+
+/* Upper bound, in bytes, of the device workspace ips4o_sort(n, elem_type) uses
+ * (Theorem 2: O(k b t) buffers; here t = stripes/CTAs). */
+size_t ips4o_aux_bytes(uint64_t n, int elem_type);
+
+/* Statistics of the last call (host memory). */
+int ips4o_last_stats(ips4o_stats* out);
+
+const char* ips4o_error_string(int status);
+
+/* Release the workspace of the current device. */
+int ips4o_release_workspace(void);
+
+/* ------------------------------------------------------------- profiling */
+/* When enabled, every kernel launch is bracketed by CUDA events on the launch stream.
+ * ips4o_profile_read() synchronises the recorded events and returns, per kernel kind,
+ * the number of launches and the summed device milliseconds, then clears the record.
+ * Kinds: 0 sample/splitters, 1 classify_flush, 2 prepare, 3 empty-block moves,
+ * 4 block permutation, 5 cleanup, 6 base case, 7 other. */
+#define IPS4O_NUM_KERNEL_KINDS 8
+int ips4o_profile_enable(int on);
+int ips4o_profile_read(uint64_t* launches /*[8]*/, double* ms /*[8]*/);
+const char* ips4o_kernel_kind_name(int kind);
+
+/* ------------------------------------------------------- test-only hooks */
+
+/* Classification of d_in[0..n) with GIVEN splitters:
+ * h_splitters is HOST memory holding nspl strictly increasing keys in the element
+ * type's key format (u64: uint64; f64: double; pair: uint64 key; rec100: 10-byte
+ * keys packed at a 10-byte stride).  eq enables equality buckets.  Writes the bucket
+ * index of every element to d_bucket_out (device, uint32[n]), using the numbering
+ * of SURVEY.md §8(c) O5.  1 <= nspl <= 255 (<= 127 with eq). */
+int ips4o_debug_classify(const void* d_in, uint64_t n, int elem_type, const void* h_splitters,
+                         uint32_t nspl, int eq, uint32_t* d_bucket_out, void* stream);
+
+/* One distribution step (local classification, block permutation, cleanup) over
+ * d_data[0..n) with GIVEN splitters (same format as above), without recursion.
+ * On return (the stream is synchronised) d_data is partitioned and h_bounds_out
+ * (HOST, >= 257 entries) holds the element-exact bucket starts e_0..e_K, *K_out = K.
+ * n >= 64. */
+int ips4o_debug_partition_once(void* d_data, uint64_t n, int elem_type, const void* h_splitters,
+                               uint32_t nspl, int eq, uint64_t* h_bounds_out, uint32_t* K_out,
+                               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,209 @@
+// common.cuh -- element traits, level descriptors and small device helpers shared by
+// the sm_100a kernels of libips4o.so.  (Product code; shares nothing with oracle/.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ips4o {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+constexpr int MAXK = 256;            // buckets per step: k = 256, or 2k'-1 <= 255 with eq
+constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer
+constexpr u32 INV_BUCKET = 0xFFFFu;  // "no element" marker in classification registers
+constexpr int K2_THREADS = 512;      // local classification CTA
+constexpr int K3_THREADS = 256;      // block permutation CTA (one chain per warp)
+constexpr int K4_THREADS = 256;      // cleanup CTA
+constexpr int BLOCK_BYTES = 512;     // block b*s in bytes for the 8/16-byte types
+
+// ----------------------------------------------------------------- element traits
+// key(): order-preserving unsigned 64-bit image of the sort key.
+// less(): the base-case order.  For PAIR it is (key, payload) lexicographic -- a valid
+// unstable order that also makes padding with the all-ones element harmless.
+
+struct TU64 {
+    typedef u64 V;
+    static constexpr int S = 8, B = 64, VEC = 2, E2 = 8, CAP = 16384, TYPE = 0;
+    __device__ __forceinline__ static u64 key(V v) { return v; }
+    __device__ __forceinline__ static bool less(V a, V b) { return a < b; }
+    __host__ __device__ __forceinline__ static V pad() { return ~0ull; }
+};
+
+// IEEE doubles without NaN/-0.0: flip all bits of negatives, set the sign bit of
+// non-negatives -> unsigned order equals '<' (PAPER.md:452 uses 64-bit floats).
+struct TF64 {
+    typedef u64 V;
+    static constexpr int S = 8, B = 64, VEC = 2, E2 = 8, CAP = 16384, TYPE = 1;
+    __host__ __device__ __forceinline__ static u64 key(V v) {
+        return (v >> 63) ? ~v : (v | 0x8000000000000000ull);
+    }
+    __device__ __forceinline__ static bool less(V a, V b) { return key(a) < key(b); }
+    __host__ __device__ __forceinline__ static V pad() { return 0x7FFFFFFFFFFFFFFFull; }  // key = ~0
+};
+
+struct TPair {
+    typedef ulonglong2 V;
+    static constexpr int S = 16, B = 32, VEC = 1, E2 = 4, CAP = 8192, TYPE = 2;
+    __device__ __forceinline__ static u64 key(V v) { return v.x; }
+    __device__ __forceinline__ static bool less(V a, V b) {
+        return a.x < b.x || (a.x == b.x && a.y < b.y);
+    }
+    __host__ __device__ __forceinline__ static V pad() { return make_ulonglong2(~0ull, ~0ull); }
+};
+
+// ------------------------------------------------------------- level descriptors
+
+struct TaskDesc {
+    u64 lo, hi;
+};
+
+// Per task of one distribution level.  Block grid origin g: the first element index
+// >= lo whose address is 16-byte aligned (TMA bulk copies need 16 B); block x covers
+// elements [g + x*B, g + (x+1)*B).  nblocks = ceil((hi-g)/B) (the last block may
+// reach past hi: its writes go to the overflow block).
+struct TaskParam {
+    u64 lo, hi, g;
+    u32 nblocks;
+    u32 kprime, logk, eq, K;      // classifier (written by k_sample or the debug path)
+    u32 stripe_begin, nstripes;   // this task's stripes in the stripe table (contiguous)
+    u32 pad_;
+};
+
+// A stripe: [begin, end) elements of one task.  Its whole blocks [sb, se) (relative to
+// the task's g) receive the flushed blocks at the front.
+struct StripeDesc {
+    u64 begin, end;
+    u32 task, sb, se, first;      // first: 1 if this is the task's first stripe
+};
+
+enum {
+    CTR_STRIPE = 0,   // K2 stripe ticket
+    CTR_NEXT = 1,     // next-level task queue length
+    CTR_BASE = 2,     // base-case task queue length
+    CTR_TICKET = 3,   // cleanup ticket
+    CTR_ERROR = 4,    // error bits
+    CTR_NEXT_OVF = 5, // next-level queue overflow count
+    CTR_EQ = 6,       // tasks partitioned with equality buckets
+    CTR_N = 8
+};
+enum { ERR_SPILL = 1, ERR_CONSERVE = 2, ERR_QUEUE = 4, ERR_CAPACITY = 8 };
+
+struct LevelArgs {
+    void* data;
+    const TaskParam* tp;
+    u32 ntasks;
+    const StripeDesc* sd;
+    const u32* stripe_order;
+    u32 nstripes;
+    u64* tree;        // [T][256] BFS tree a[1..k'-1] (index 0 unused)
+    u64* spl;         // [T][256] sorted padded splitters s[1..k'-1]
+    u32* s_count;     // [S][256] elements per bucket in stripe
+    u32* s_fill;      // [S][256] partial buffer fill at the end of the stripe
+    u32* s_spoff;     // [S][256] offset of the partial buffer in the stripe's spill
+    u64* s_spbase;    // [S] stripe spill base (elements)
+    u32* s_nfull;     // [S] full blocks flushed at the stripe front
+    u32* prefF;       // [S] full blocks in earlier stripes of the same task
+    u32* prefE;       // [S] empty blocks in earlier stripes of the same task
+    void* spill;
+    u64 spill_cap;    // elements
+    u64* bnd;         // [T][257] element-exact bucket starts e_0..e_256
+    u32* dblk;        // [T][257] delimiters d_i (block index, rounded up)
+    u32* nfb;         // [T][256] full blocks of bucket i
+    u32* mov;         // [T][257] prefix of Appendix-A moves over buckets
+    u64* wr;          // [T][256] packed (w:32 | r+RBIAS:32) block pointers
+    u32* readers;     // [T][256]
+    u32* done;        // [T][8]   bucket has no unprocessed block left
+    u32* cflag;       // [T][256] cleanup: overhang saved
+    void* ovf;        // [T][B]   overflow blocks
+    int* ovf_owner;   // [T]
+    TaskDesc* q_next;
+    TaskDesc* q_base;
+    u32 q_cap;
+    u32* ctr;         // [CTR_N]
+    u64* spill_ctr;
+    u32 base_cap;     // tasks with <= base_cap elements go to the base case
+    int emit;         // emit next-level / base tasks (0 for the debug single step)
+    u64 seed;
+};
+
+// ---------------------------------------------------------------- device helpers
+
+__device__ __forceinline__ u32 lanemask_lt() {
+    u32 r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+// TMA bulk copy shared -> global (cp.async.bulk, SASS UBLKCP), bulk-group completion.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, u32 bytes) {
+    u32 s = (u32)__cvta_generic_to_shared(ssrc);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ u32 ld_acquire_u32(const u32* p) {
+    u32 v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(u32* p, u32 v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__host__ __device__ __forceinline__ u64 mix64(u64 z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Branchless descent of the implicit search tree: j <- 2j + [a_j <= e]
+// (ties go right: s_{i-1} <= e < s_i), then with equality buckets one
+// extra comparison against the lower splitter: 2i-1 for {s_i}, 2i else.
+__device__ __forceinline__ u32 classify_key(u64 k, const u64* tree, const u64* spl, u32 logk,
+                                            u32 kprime, u32 eq) {
+    u32 j = 1;
+#pragma unroll
+    for (int l = 0; l < 8; ++l)
+        if ((u32)l < logk) j = 2 * j + (k >= tree[j] ? 1u : 0u);
+    u32 i = j - kprime;
+    if (eq) {
+        u32 ii = i ? i : 1u;
+        u32 isq = (i >= 1u && spl[ii] >= k) ? 1u : 0u;
+        return 2 * i - isq;
+    }
+    return i;
+}
+
+}  // namespace ips4o

@@ -1,0 +1,731 @@
+// ips4o.cu -- libips4o.so: host planner, kernel launch sequence and the C ABI of
+// include/ips4o.h.  The host only plans (stripes per task) and enqueues kernels on the
+// caller's stream; every step of the sort runs in the kernels of k_*.cuh.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/ips4o.h"
+#include "common.cuh"
+#include "k_base.cuh"
+#include "k_classify.cuh"
+#include "k_cleanup.cuh"
+#include "k_permute.cuh"
+#include "k_sample.cuh"
+
+namespace ips4o {
+
+constexpr u32 MAXT = 512;          // tasks per level batch
+constexpr u32 MAXS = 512;          // stripes per level batch
+constexpr u32 QCAP = MAXT * MAXK;  // queue capacity (tasks)
+constexpr u64 MIN_STRIPE = 65536;  // elements
+
+static std::mutex g_mu;
+static char g_errbuf[512];
+static ips4o_stats g_stats;
+
+enum KernelKind { KK_SAMPLE = 0, KK_CLASSIFY, KK_PREPARE, KK_MOVES, KK_PERMUTE, KK_CLEANUP, KK_BASE, KK_OTHER };
+static const char* kKindNames[IPS4O_NUM_KERNEL_KINDS] = {
+    "sample_splitters", "classify_flush", "prepare", "empty_block_moves",
+    "block_permute",    "cleanup",        "base_case", "other"};
+
+struct Prof {
+    bool on = false;
+    struct Rec {
+        int kind;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+} g_prof;
+
+struct Workspace {
+    int device = -1;
+    int num_sms = 0;
+    char* dev = nullptr;
+    size_t dev_bytes = 0;
+    u64 spill_elems = 0;  // capacity in elements (of the current element size)
+    int spill_elem_size = 0;
+    char* host = nullptr;
+    // device carve-up
+    TaskParam* tp;
+    StripeDesc* sd;
+    u32* order;
+    u64 *tree, *spl;
+    u32 *s_count, *s_fill, *s_spoff, *s_nfull, *prefF, *prefE;
+    u64* s_spbase;
+    u64* bnd;
+    u32 *dblk, *nfb, *mov, *readers, *done, *cflag;
+    u64* wr;
+    void* ovf;
+    int* ovf_owner;
+    TaskDesc *q_next, *q_base;
+    u32* ctr;
+    u64* spill_ctr;
+    u64* dsplit;
+    void* spill;
+    // pinned host
+    TaskParam* h_tp;
+    StripeDesc* h_sd;
+    u32* h_order;
+    u32* h_ctr;
+    TaskDesc* h_q;
+    u64* h_bnd;
+    u32 k2_blocks = 0, k3_blocks = 0;
+    int k2_type = -1;
+};
+static Workspace g_ws;
+
+static int set_cuda_error(cudaError_t e, const char* what) {
+    snprintf(g_errbuf, sizeof g_errbuf, "%s: %s", what, cudaGetErrorString(e));
+    return IPS4O_ECUDA;
+}
+#define CK(x)                                                  \
+    do {                                                       \
+        cudaError_t e_ = (x);                                  \
+        if (e_ != cudaSuccess) return set_cuda_error(e_, #x);  \
+    } while (0)
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static size_t fixed_bytes() {
+    size_t s = 0;
+    auto add = [&](size_t b) { s += align_up(b, 256); };
+    add(MAXT * sizeof(TaskParam));
+    add(MAXS * sizeof(StripeDesc));
+    add(MAXS * 4);
+    add((size_t)MAXT * MAXK * 8 * 2);          // tree, spl
+    add((size_t)MAXS * MAXK * 4 * 3);          // s_count, s_fill, s_spoff
+    add(MAXS * 8 + MAXS * 4 * 3);              // s_spbase, s_nfull, prefF, prefE
+    add((size_t)MAXT * (MAXK + 1) * 8);        // bnd
+    add((size_t)MAXT * (MAXK + 1) * 4 * 2);    // dblk, mov
+    add((size_t)MAXT * MAXK * 4 * 3);          // nfb, readers, cflag
+    add((size_t)MAXT * (MAXK / 32) * 4);       // done
+    add((size_t)MAXT * MAXK * 8);              // wr
+    add((size_t)MAXT * BLOCK_BYTES);           // ovf
+    add(MAXT * 4);                             // ovf_owner
+    add((size_t)QCAP * sizeof(TaskDesc) * 2);  // queues
+    add(CTR_N * 4 + 8);                        // ctr + spill ctr
+    add(MAXK * 8);                             // debug splitters
+    return s;
+}
+
+static u64 spill_bound_elems(u64 n, int esize) {
+    // a stripe spills at most 256 partially filled buffers of < b elements (b*s = 512 B)
+    const u64 per_stripe = (u64)MAXK * (BLOCK_BYTES / esize);
+    return std::min<u64>(n + 64, (u64)MAXS * per_stripe);
+}
+
+static int ensure_ws(u64 n, int esize) {
+    int dev;
+    CK(cudaGetDevice(&dev));
+    if (g_ws.device != dev) {
+        if (g_ws.dev) {
+            cudaFree(g_ws.dev);
+            g_ws.dev = nullptr;
+        }
+        g_ws.device = dev;
+        CK(cudaDeviceGetAttribute(&g_ws.num_sms, cudaDevAttrMultiProcessorCount, dev));
+        g_ws.k2_type = -1;
+    }
+    const u64 need_spill = spill_bound_elems(n, esize);
+    const size_t need = fixed_bytes() + align_up(need_spill * esize, 256);
+    if (g_ws.dev && g_ws.dev_bytes >= need) {
+        g_ws.spill_elems = (g_ws.dev_bytes - fixed_bytes()) / esize;
+        g_ws.spill_elem_size = esize;
+        return IPS4O_OK;
+    }
+    if (g_ws.dev) cudaFree(g_ws.dev);
+    g_ws.dev = nullptr;
+    if (cudaMalloc(&g_ws.dev, need) != cudaSuccess) {
+        cudaGetLastError();
+        g_ws.dev_bytes = 0;
+        snprintf(g_errbuf, sizeof g_errbuf, "workspace allocation of %zu bytes failed", need);
+        return IPS4O_ENOMEM;
+    }
+    g_ws.dev_bytes = need;
+    char* p = g_ws.dev;
+    auto take = [&](size_t b) {
+        char* r = p;
+        p += align_up(b, 256);
+        return r;
+    };
+    g_ws.tp = (TaskParam*)take(MAXT * sizeof(TaskParam));
+    g_ws.sd = (StripeDesc*)take(MAXS * sizeof(StripeDesc));
+    g_ws.order = (u32*)take(MAXS * 4);
+    char* tr = take((size_t)MAXT * MAXK * 8 * 2);
+    g_ws.tree = (u64*)tr;
+    g_ws.spl = (u64*)(tr + (size_t)MAXT * MAXK * 8);
+    char* sc = take((size_t)MAXS * MAXK * 4 * 3);
+    g_ws.s_count = (u32*)sc;
+    g_ws.s_fill = g_ws.s_count + (size_t)MAXS * MAXK;
+    g_ws.s_spoff = g_ws.s_fill + (size_t)MAXS * MAXK;
+    char* ss = take(MAXS * 8 + MAXS * 4 * 3);
+    g_ws.s_spbase = (u64*)ss;
+    g_ws.s_nfull = (u32*)(ss + MAXS * 8);
+    g_ws.prefF = g_ws.s_nfull + MAXS;
+    g_ws.prefE = g_ws.prefF + MAXS;
+    g_ws.bnd = (u64*)take((size_t)MAXT * (MAXK + 1) * 8);
+    char* dm = take((size_t)MAXT * (MAXK + 1) * 4 * 2);
+    g_ws.dblk = (u32*)dm;
+    g_ws.mov = g_ws.dblk + (size_t)MAXT * (MAXK + 1);
+    char* nr = take((size_t)MAXT * MAXK * 4 * 3);
+    g_ws.nfb = (u32*)nr;
+    g_ws.readers = g_ws.nfb + (size_t)MAXT * MAXK;
+    g_ws.cflag = g_ws.readers + (size_t)MAXT * MAXK;
+    g_ws.done = (u32*)take((size_t)MAXT * (MAXK / 32) * 4);
+    g_ws.wr = (u64*)take((size_t)MAXT * MAXK * 8);
+    g_ws.ovf = take((size_t)MAXT * BLOCK_BYTES);
+    g_ws.ovf_owner = (int*)take(MAXT * 4);
+    char* q = take((size_t)QCAP * sizeof(TaskDesc) * 2);
+    g_ws.q_next = (TaskDesc*)q;
+    g_ws.q_base = g_ws.q_next + QCAP;
+    char* c = take(CTR_N * 4 + 8);
+    g_ws.ctr = (u32*)c;
+    g_ws.spill_ctr = (u64*)(c + CTR_N * 4);
+    g_ws.dsplit = (u64*)take(MAXK * 8);
+    g_ws.spill = p;
+    g_ws.spill_elems = (g_ws.dev_bytes - fixed_bytes()) / esize;
+    g_ws.spill_elem_size = esize;
+    if (!g_ws.host) {
+        size_t hb = MAXT * sizeof(TaskParam) + MAXS * sizeof(StripeDesc) + MAXS * 4 + CTR_N * 4 +
+                    (size_t)QCAP * sizeof(TaskDesc) + (MAXK + 1) * 8 + 4096;
+        CK(cudaMallocHost(&g_ws.host, hb));
+        char* h = g_ws.host;
+        g_ws.h_tp = (TaskParam*)h;
+        h += MAXT * sizeof(TaskParam);
+        g_ws.h_sd = (StripeDesc*)h;
+        h += MAXS * sizeof(StripeDesc);
+        g_ws.h_order = (u32*)h;
+        h += MAXS * 4;
+        g_ws.h_ctr = (u32*)h;
+        h += CTR_N * 4;
+        g_ws.h_q = (TaskDesc*)h;
+        h += (size_t)QCAP * sizeof(TaskDesc);
+        g_ws.h_bnd = (u64*)h;
+    }
+    return IPS4O_OK;
+}
+
+// ------------------------------------------------------------------ launching
+
+template <class F>
+static int launch(int kind, cudaStream_t st, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (g_prof.on) {
+        a = g_prof.get();
+        b = g_prof.get();
+        cudaEventRecord(a, st);
+    }
+    f();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, kKindNames[kind]);
+    if (g_prof.on) {
+        cudaEventRecord(b, st);
+        g_prof.recs.push_back({kind, a, b});
+    }
+    g_stats.kernel_launches++;
+    return IPS4O_OK;
+}
+#define LAUNCH(kind, ...)                                         \
+    do {                                                          \
+        int rc_ = launch(kind, st, [&]() { __VA_ARGS__; });       \
+        if (rc_) return rc_;                                      \
+    } while (0)
+
+template <class TR>
+static int prepare_kernels(void) {
+    if (g_ws.k2_type == TR::TYPE) return IPS4O_OK;
+    CK(cudaFuncSetAttribute(k_classify<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)K2Smem<TR>::total));
+    CK(cudaFuncSetAttribute(k_basecase<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(TR::CAP * sizeof(typename TR::V))));
+    int occ2 = 0, occ3 = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_classify<TR>, K2_THREADS,
+                                                     K2Smem<TR>::total));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_permute<TR>, K3_THREADS, 0));
+    if (occ2 < 1 || occ3 < 1) {
+        snprintf(g_errbuf, sizeof g_errbuf, "occupancy query returned %d/%d", occ2, occ3);
+        return IPS4O_ECUDA;
+    }
+    g_ws.k2_blocks = (u32)(occ2 * g_ws.num_sms);
+    g_ws.k3_blocks = (u32)(occ3 * g_ws.num_sms);
+    g_ws.k2_type = TR::TYPE;
+    return IPS4O_OK;
+}
+
+template <class TR>
+static LevelArgs level_args(void* data, u32 T, u32 S, int emit, u64 seed) {
+    LevelArgs A;
+    memset(&A, 0, sizeof A);
+    A.data = data;
+    A.tp = g_ws.tp;
+    A.ntasks = T;
+    A.sd = g_ws.sd;
+    A.stripe_order = g_ws.order;
+    A.nstripes = S;
+    A.tree = g_ws.tree;
+    A.spl = g_ws.spl;
+    A.s_count = g_ws.s_count;
+    A.s_fill = g_ws.s_fill;
+    A.s_spoff = g_ws.s_spoff;
+    A.s_spbase = g_ws.s_spbase;
+    A.s_nfull = g_ws.s_nfull;
+    A.prefF = g_ws.prefF;
+    A.prefE = g_ws.prefE;
+    A.spill = g_ws.spill;
+    A.spill_cap = g_ws.spill_elems;
+    A.bnd = g_ws.bnd;
+    A.dblk = g_ws.dblk;
+    A.nfb = g_ws.nfb;
+    A.mov = g_ws.mov;
+    A.wr = g_ws.wr;
+    A.readers = g_ws.readers;
+    A.done = g_ws.done;
+    A.cflag = g_ws.cflag;
+    A.ovf = g_ws.ovf;
+    A.ovf_owner = g_ws.ovf_owner;
+    A.q_next = g_ws.q_next;
+    A.q_base = g_ws.q_base;
+    A.q_cap = QCAP;
+    A.ctr = g_ws.ctr;
+    A.spill_ctr = g_ws.spill_ctr;
+    A.base_cap = TR::CAP;
+    A.emit = emit;
+    A.seed = seed;
+    return A;
+}
+
+// Plan the stripes of a batch of tasks (host) into g_ws.h_tp / h_sd / h_order.
+template <class TR>
+static void plan_batch(const TaskDesc* tasks, u32 T, uintptr_t base_addr, u32* S_out) {
+    constexpr int B = TR::B;
+    u64 N = 0;
+    for (u32 i = 0; i < T; ++i) N += tasks[i].hi - tasks[i].lo;
+    const u64 target = std::max<u64>(1, std::min<u64>(MAXS, 3ull * g_ws.num_sms));
+    u64 L = std::max<u64>((N + target - 1) / target, MIN_STRIPE);
+    L = (L + B - 1) / B * B;
+    u32 S = 0;
+    for (u32 i = 0; i < T; ++i) {
+        const u64 lo = tasks[i].lo, hi = tasks[i].hi;
+        u64 g = lo;
+        while (((base_addr + g * TR::S) & 15u) != 0 && g < hi) ++g;
+        TaskParam& tp = g_ws.h_tp[i];
+        memset(&tp, 0, sizeof tp);
+        tp.lo = lo;
+        tp.hi = hi;
+        tp.g = g;
+        tp.nblocks = (u32)((hi - g + B - 1) / B);
+        const u64 main = hi - g;
+        u64 ns = std::max<u64>(1, (main + L / 2) / L);
+        u64 Lt = ((main + ns - 1) / ns + B - 1) / B * B;
+        ns = std::max<u64>(1, (main + Lt - 1) / Lt);
+        tp.stripe_begin = S;
+        tp.nstripes = (u32)ns;
+        for (u64 j = 0; j < ns; ++j) {
+            StripeDesc& sd = g_ws.h_sd[S];
+            sd.begin = j == 0 ? lo : g + j * Lt;
+            sd.end = j + 1 == ns ? hi : g + (j + 1) * Lt;
+            sd.task = i;
+            const u64 mb = std::max(sd.begin, g);
+            sd.sb = (u32)((mb - g) / B);
+            sd.se = (u32)((sd.end - g + B - 1) / B);
+            sd.first = j == 0;
+            ++S;
+        }
+    }
+    // longest stripes first (LPT) for the persistent K2 CTAs
+    for (u32 j = 0; j < S; ++j) g_ws.h_order[j] = j;
+    std::stable_sort(g_ws.h_order, g_ws.h_order + S, [](u32 a, u32 b) {
+        return (g_ws.h_sd[a].end - g_ws.h_sd[a].begin) > (g_ws.h_sd[b].end - g_ws.h_sd[b].begin);
+    });
+    *S_out = S;
+}
+
+// number of stripes plan_batch will create for a task, for batching decisions
+template <class TR>
+static u32 stripes_for(u64 size, u64 N) {
+    const u64 target = std::max<u64>(1, std::min<u64>(MAXS, 3ull * g_ws.num_sms));
+    u64 L = std::max<u64>((N + target - 1) / target, MIN_STRIPE);
+    L = (L + TR::B - 1) / TR::B * TR::B;
+    return (u32)std::max<u64>(1, (size + L / 2) / L) + 1;
+}
+
+// One distribution level over T <= MAXT tasks (already planned into h_tp/h_sd).
+template <class TR>
+static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitters, u32 nspl,
+                     u32 eq, int emit, u64 seed) {
+    CK(cudaMemcpyAsync(g_ws.tp, g_ws.h_tp, T * sizeof(TaskParam), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(g_ws.sd, g_ws.h_sd, S * sizeof(StripeDesc), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(g_ws.order, g_ws.h_order, S * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(g_ws.ctr, 0, CTR_N * 4 + 8, st));
+    LevelArgs A = level_args<TR>(data, T, S, emit, seed);
+    if (from_splitters) {
+        LAUNCH(KK_SAMPLE, (k_tree_from_splitters<<<1, 256, 0, st>>>(A, g_ws.dsplit, nspl, eq)));
+    } else {
+        LAUNCH(KK_SAMPLE, (k_sample<TR><<<T, K1_THREADS, 0, st>>>(A)));
+    }
+    const u32 g2 = std::min<u32>(S, g_ws.k2_blocks);
+    LAUNCH(KK_CLASSIFY, (k_classify<TR><<<g2, K2_THREADS, K2Smem<TR>::total, st>>>(A)));
+    LAUNCH(KK_PREPARE, (k_prepare<TR><<<T, MAXK, 0, st>>>(A)));
+    const u32 gx = std::max<u32>(1, (2 * g_ws.num_sms + T - 1) / T);
+    LAUNCH(KK_MOVES, (k_moves<TR><<<dim3(gx, T), 256, 0, st>>>(A)));
+    LAUNCH(KK_PERMUTE, (k_permute<TR><<<g_ws.k3_blocks, K3_THREADS, 0, st>>>(A)));
+    LAUNCH(KK_CLEANUP, (k_cleanup<TR><<<T * MAXK, K4_THREADS, 0, st>>>(A)));
+    CK(cudaMemcpyAsync(g_ws.h_ctr, g_ws.ctr, CTR_N * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    g_stats.host_syncs++;
+    if (g_ws.h_ctr[CTR_ERROR]) {
+        snprintf(g_errbuf, sizeof g_errbuf, "device consistency check failed (flags 0x%x)",
+                 g_ws.h_ctr[CTR_ERROR]);
+        return IPS4O_EINTERNAL;
+    }
+    g_stats.equality_tasks += g_ws.h_ctr[CTR_EQ];
+    return IPS4O_OK;
+}
+
+template <class TR>
+static int run_base(void* data, u32 count, TaskDesc* d_tasks, cudaStream_t st) {
+    if (!count) return IPS4O_OK;
+    const u32 grid = std::min<u32>(count, 8u * g_ws.num_sms);
+    const size_t smem = TR::CAP * sizeof(typename TR::V);
+    LAUNCH(KK_BASE, (k_basecase<TR><<<grid, K5_THREADS, smem, st>>>(d_tasks, count, data)));
+    g_stats.base_tasks += count;
+    return IPS4O_OK;
+}
+
+template <class TR>
+static int sort_impl(void* data, u64 n, cudaStream_t st) {
+    int rc = ensure_ws(n, TR::S);
+    if (rc) return rc;
+    rc = prepare_kernels<TR>();
+    if (rc) return rc;
+    g_stats.aux_bytes = g_ws.dev_bytes;
+    if (n <= (u64)TR::CAP) {
+        g_ws.h_q[0] = TaskDesc{0, n};
+        CK(cudaMemcpyAsync(g_ws.q_base, g_ws.h_q, sizeof(TaskDesc), cudaMemcpyHostToDevice, st));
+        return run_base<TR>(data, 1, g_ws.q_base, st);
+    }
+    std::vector<TaskDesc> cur(1, TaskDesc{0, n}), next;
+    u64 seed = 0x1234567ull;
+    while (!cur.empty()) {
+        g_stats.levels++;
+        next.clear();
+        // largest tasks first; batches of <= MAXT tasks and <= MAXS stripes
+        std::sort(cur.begin(), cur.end(),
+                  [](const TaskDesc& a, const TaskDesc& b) { return a.hi - a.lo > b.hi - b.lo; });
+        u64 Ntot = 0;
+        for (auto& t : cur) Ntot += t.hi - t.lo;
+        size_t i0 = 0;
+        while (i0 < cur.size()) {
+            size_t i1 = i0;
+            u32 sacc = 0;
+            while (i1 < cur.size() && i1 - i0 < MAXT) {
+                u32 s = stripes_for<TR>(cur[i1].hi - cur[i1].lo, Ntot);
+                if (sacc + s > MAXS && i1 > i0) break;
+                sacc += s;
+                ++i1;
+            }
+            const u32 T = (u32)(i1 - i0);
+            u32 S = 0;
+            plan_batch<TR>(&cur[i0], T, (uintptr_t)data, &S);
+            if (S > MAXS) {
+                snprintf(g_errbuf, sizeof g_errbuf, "stripe planning overflow");
+                return IPS4O_EINTERNAL;
+            }
+            seed = mix64(seed);
+            rc = run_level<TR>(data, T, S, st, false, 0, 0, 1, seed);
+            if (rc) return rc;
+            g_stats.distribution_tasks += T;
+            const u32 nb = g_ws.h_ctr[CTR_BASE], nn = g_ws.h_ctr[CTR_NEXT];
+            rc = run_base<TR>(data, nb, g_ws.q_base, st);
+            if (rc) return rc;
+            if (nn) {
+                CK(cudaMemcpyAsync(g_ws.h_q, g_ws.q_next, nn * sizeof(TaskDesc), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                next.insert(next.end(), g_ws.h_q, g_ws.h_q + nn);
+            }
+            i0 = i1;
+        }
+        cur.swap(next);
+    }
+    return IPS4O_OK;
+}
+
+static int type_size(int t) {
+    switch (t) {
+        case IPS4O_U64: return 8;
+        case IPS4O_F64: return 8;
+        case IPS4O_PAIR_U64: return 16;
+        case IPS4O_REC100_K10: return 100;
+        default: return 0;
+    }
+}
+
+static int check_args(const void* p, u64 n, int type) {
+    if (type_size(type) == 0) {
+        snprintf(g_errbuf, sizeof g_errbuf, "unknown element type %d", type);
+        return IPS4O_EINVAL;
+    }
+    if (type == IPS4O_REC100_K10) {
+        snprintf(g_errbuf, sizeof g_errbuf, "element type rec100 is not implemented in this build");
+        return IPS4O_EINVAL;
+    }
+    if (n >= (1ull << 40)) {
+        snprintf(g_errbuf, sizeof g_errbuf, "n too large");
+        return IPS4O_EINVAL;
+    }
+    if (n > 0 && !p) {
+        snprintf(g_errbuf, sizeof g_errbuf, "null data pointer");
+        return IPS4O_EINVAL;
+    }
+    const uintptr_t a = (uintptr_t)p;
+    const int need = type == IPS4O_PAIR_U64 ? 16 : 8;
+    if (n > 0 && (a % need)) {
+        snprintf(g_errbuf, sizeof g_errbuf, "data pointer not %d-byte aligned", need);
+        return IPS4O_EALIGN;
+    }
+    return IPS4O_OK;
+}
+
+template <class TR>
+static int splitters_to_keys(const void* h, u32 nspl, std::vector<u64>& out) {
+    out.resize(nspl);
+    if (TR::TYPE == 1) {
+        for (u32 i = 0; i < nspl; ++i) {
+            u64 bits;
+            memcpy(&bits, (const char*)h + 8 * i, 8);
+            out[i] = TF64::key(bits);
+        }
+    } else {
+        memcpy(out.data(), h, 8ull * nspl);
+    }
+    for (u32 i = 1; i < nspl; ++i)
+        if (!(out[i - 1] < out[i])) return IPS4O_EINVAL;
+    return IPS4O_OK;
+}
+
+template <class TR>
+static int debug_classify_impl(const void* d_in, u64 n, const void* h_spl, u32 nspl, int eq,
+                               u32* d_out, cudaStream_t st) {
+    int rc = ensure_ws(n, TR::S);
+    if (rc) return rc;
+    std::vector<u64> keys;
+    if (splitters_to_keys<TR>(h_spl, nspl, keys)) {
+        snprintf(g_errbuf, sizeof g_errbuf, "splitters must be strictly increasing");
+        return IPS4O_EINVAL;
+    }
+    CK(cudaMemcpyAsync(g_ws.dsplit, keys.data(), 8ull * nspl, cudaMemcpyHostToDevice, st));
+    LevelArgs A = level_args<TR>(const_cast<void*>(d_in), 1, 0, 0, 0);
+    LAUNCH(KK_OTHER, (k_tree_from_splitters<<<1, 256, 0, st>>>(A, g_ws.dsplit, nspl, (u32)eq)));
+    if (n) {
+        const u32 grid = (u32)std::min<u64>((n + 255) / 256, 4096);
+        LAUNCH(KK_OTHER, (k_debug_classify<TR><<<grid, 256, 0, st>>>(d_in, n, g_ws.tree, g_ws.spl,
+                                                                      g_ws.tp, d_out)));
+    }
+    return IPS4O_OK;
+}
+
+template <class TR>
+static int debug_partition_impl(void* d, u64 n, const void* h_spl, u32 nspl, int eq, u64* h_bnd,
+                                u32* K_out, cudaStream_t st) {
+    int rc = ensure_ws(n, TR::S);
+    if (rc) return rc;
+    rc = prepare_kernels<TR>();
+    if (rc) return rc;
+    std::vector<u64> keys;
+    if (splitters_to_keys<TR>(h_spl, nspl, keys)) {
+        snprintf(g_errbuf, sizeof g_errbuf, "splitters must be strictly increasing");
+        return IPS4O_EINVAL;
+    }
+    CK(cudaMemcpyAsync(g_ws.dsplit, keys.data(), 8ull * nspl, cudaMemcpyHostToDevice, st));
+    TaskDesc td{0, n};
+    u32 S = 0;
+    plan_batch<TR>(&td, 1, (uintptr_t)d, &S);
+    rc = run_level<TR>(d, 1, S, st, true, nspl, (u32)eq, 0, 1);
+    if (rc) return rc;
+    g_stats.levels = 1;
+    g_stats.distribution_tasks = 1;
+    CK(cudaMemcpyAsync(h_bnd, g_ws.bnd, (MAXK + 1) * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    u32 kp = 2;
+    while (kp < nspl + 1) kp <<= 1;
+    *K_out = eq ? 2 * kp - 1 : kp;
+    return IPS4O_OK;
+}
+
+}  // namespace ips4o
+
+using namespace ips4o;
+
+extern "C" {
+
+int ips4o_sort(void* d_data, uint64_t n, int elem_type, void* stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int rc = check_args(d_data, n, elem_type);
+    if (rc) return rc;
+    memset(&g_stats, 0, sizeof g_stats);
+    g_stats.n = n;
+    g_stats.elem_type = (uint32_t)elem_type;
+    if (n <= 1) return IPS4O_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (elem_type) {
+        case IPS4O_U64: return sort_impl<TU64>(d_data, n, st);
+        case IPS4O_F64: return sort_impl<TF64>(d_data, n, st);
+        case IPS4O_PAIR_U64: return sort_impl<TPair>(d_data, n, st);
+        default: return IPS4O_EINVAL;
+    }
+}
+
+int ips4o_sort_host(void* h_data, uint64_t n, int elem_type, void* stream) {
+    static void* d_stage = nullptr;
+    static size_t stage_bytes = 0;
+    static int stage_dev = -1;
+    const int s = type_size(elem_type);
+    if (!s || (n > 0 && !h_data)) return IPS4O_EINVAL;
+    if (n <= 1) return IPS4O_OK;
+    const size_t bytes = (size_t)n * s;
+    cudaStream_t st = (cudaStream_t)stream;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        if (d_stage && (stage_bytes < bytes || stage_dev != dev)) {
+            cudaFree(d_stage);
+            d_stage = nullptr;
+        }
+        if (!d_stage) {
+            if (cudaMalloc(&d_stage, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                return IPS4O_ENOMEM;
+            }
+            stage_bytes = bytes;
+            stage_dev = dev;
+        }
+        CK(cudaMemcpyAsync(d_stage, h_data, bytes, cudaMemcpyHostToDevice, st));
+    }
+    int rc = ips4o_sort(d_stage, n, elem_type, stream);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h_data, d_stage, bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return IPS4O_OK;
+}
+
+size_t ips4o_aux_bytes(uint64_t n, int elem_type) {
+    const int s = type_size(elem_type);
+    if (!s) return 0;
+    return fixed_bytes() + align_up(spill_bound_elems(n, s) * s, 256);
+}
+
+int ips4o_last_stats(ips4o_stats* out) {
+    if (!out) return IPS4O_EINVAL;
+    *out = g_stats;
+    return IPS4O_OK;
+}
+
+const char* ips4o_error_string(int status) {
+    switch (status) {
+        case IPS4O_OK: return "ok";
+        case IPS4O_EINVAL: return g_errbuf[0] ? g_errbuf : "invalid argument";
+        case IPS4O_EALIGN: return g_errbuf[0] ? g_errbuf : "misaligned pointer";
+        case IPS4O_ENOMEM: return g_errbuf[0] ? g_errbuf : "out of device memory";
+        case IPS4O_ECUDA: return g_errbuf[0] ? g_errbuf : "CUDA error";
+        case IPS4O_EINTERNAL: return g_errbuf[0] ? g_errbuf : "internal consistency check failed";
+        default: return "unknown status";
+    }
+}
+
+int ips4o_release_workspace(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_ws.dev) cudaFree(g_ws.dev);
+    g_ws.dev = nullptr;
+    g_ws.dev_bytes = 0;
+    g_ws.device = -1;
+    return IPS4O_OK;
+}
+
+int ips4o_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_prof.on = on != 0;
+    return IPS4O_OK;
+}
+
+int ips4o_profile_read(uint64_t* launches, double* ms) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (int k = 0; k < IPS4O_NUM_KERNEL_KINDS; ++k) {
+        if (launches) launches[k] = 0;
+        if (ms) ms[k] = 0;
+    }
+    for (auto& r : g_prof.recs) {
+        cudaEventSynchronize(r.b);
+        float t = 0;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        if (launches) launches[r.kind]++;
+        if (ms) ms[r.kind] += t;
+        g_prof.pool.push_back(r.a);
+        g_prof.pool.push_back(r.b);
+    }
+    g_prof.recs.clear();
+    return IPS4O_OK;
+}
+
+const char* ips4o_kernel_kind_name(int kind) {
+    if (kind < 0 || kind >= IPS4O_NUM_KERNEL_KINDS) return "unknown";
+    return kKindNames[kind];
+}
+
+int ips4o_debug_classify(const void* d_in, uint64_t n, int elem_type, const void* h_splitters,
+                         uint32_t nspl, int eq, uint32_t* d_bucket_out, void* stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int rc = check_args(d_in, n, elem_type);
+    if (rc) return rc;
+    if (!h_splitters || nspl < 1 || nspl > 255 || (eq && nspl > 127) || (n && !d_bucket_out))
+        return IPS4O_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (elem_type) {
+        case IPS4O_U64: return debug_classify_impl<TU64>(d_in, n, h_splitters, nspl, eq, d_bucket_out, st);
+        case IPS4O_F64: return debug_classify_impl<TF64>(d_in, n, h_splitters, nspl, eq, d_bucket_out, st);
+        case IPS4O_PAIR_U64:
+            return debug_classify_impl<TPair>(d_in, n, h_splitters, nspl, eq, d_bucket_out, st);
+        default: return IPS4O_EINVAL;
+    }
+}
+
+int ips4o_debug_partition_once(void* d_data, uint64_t n, int elem_type, const void* h_splitters,
+                               uint32_t nspl, int eq, uint64_t* h_bounds_out, uint32_t* K_out,
+                               void* stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int rc = check_args(d_data, n, elem_type);
+    if (rc) return rc;
+    if (!h_splitters || nspl < 1 || nspl > 255 || (eq && nspl > 127) || n < 64 || !h_bounds_out ||
+        !K_out)
+        return IPS4O_EINVAL;
+    memset(&g_stats, 0, sizeof g_stats);
+    g_stats.n = n;
+    g_stats.elem_type = (uint32_t)elem_type;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (elem_type) {
+        case IPS4O_U64:
+            return debug_partition_impl<TU64>(d_data, n, h_splitters, nspl, eq, (u64*)h_bounds_out, K_out, st);
+        case IPS4O_F64:
+            return debug_partition_impl<TF64>(d_data, n, h_splitters, nspl, eq, (u64*)h_bounds_out, K_out, st);
+        case IPS4O_PAIR_U64:
+            return debug_partition_impl<TPair>(d_data, n, h_splitters, nspl, eq, (u64*)h_bounds_out, K_out, st);
+        default: return IPS4O_EINVAL;
+    }
+}
+
+}  // extern "C"

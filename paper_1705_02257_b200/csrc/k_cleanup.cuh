@@ -1,0 +1,143 @@
+// k_cleanup.cuh -- K4: cleanup of partial blocks (§4.3) and task emission.
+//
+// One CTA per (task, bucket), taken in order through an atomic ticket so that a bucket's
+// predecessor is always already running.  For bucket i:
+//   empty slots  = its head [e_i, min(d_i, e_{i+1})) and [min(w_i, e_{i+1}), e_{i+1});
+//   sources      = the overhang of its last written block into the next bucket's head
+//                  [e_{i+1}, w_i), every stripe's partially filled buffer for
+//                  i, and the overflow block if it belongs to i.
+// The overhang is read into shared memory first and published with a flag; a bucket
+// writes its head only after the bucket owning the block under that head has
+// published (the paper's "reads the head of the first bucket of the next thread into one
+// of its swap buffers").  Then the bucket is emitted to the next
+// level, to the base case, or dropped (equality buckets; size <= 1).
+#pragma once
+#include "common.cuh"
+
+namespace ips4o {
+
+constexpr int K4_MAXSTRIPES = 1024;
+
+template <class TR>
+__global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
+    typedef typename TR::V V;
+    constexpr int B = TR::B;
+    __shared__ V s_ovh[B];
+    __shared__ u32 s_pref[K4_MAXSTRIPES + 1];
+    __shared__ u32 s_wsum[K4_THREADS / 32];
+    __shared__ u32 s_ticket;
+    const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) s_ticket = atomicAdd(&A.ctr[CTR_TICKET], 1u);
+    __syncthreads();
+    const u32 ticket = s_ticket;
+    const u32 t = ticket / MAXK, b = ticket % MAXK;
+    const TaskParam tp = A.tp[t];
+    u32* flag = A.cflag + (u64)t * MAXK;
+    if (b >= tp.K) {
+        if (tid == 0) st_release_u32(flag + b, 1u);
+        return;
+    }
+    V* data = reinterpret_cast<V*>(A.data);
+    const u64* bnd = A.bnd + (u64)t * (MAXK + 1);
+    const u32* dbl = A.dblk + (u64)t * (MAXK + 1);
+    const u64 e0 = bnd[b], e1 = bnd[b + 1];
+    const u32 d = dbl[b];
+    const u32 wfin = (u32)(A.wr[(u64)t * MAXK + b] >> 32);
+    const bool own_ovf = A.ovf_owner[t] == (int)b;
+    const u64 db_el = tp.g + (u64)d * B;
+    const u64 in_end = own_ovf ? tp.g + (u64)(tp.nblocks - 1) * B : tp.g + (u64)wfin * B;
+    const u32 ovl = (in_end > db_el && in_end > e1) ? (u32)(in_end - e1) : 0u;
+    for (u32 k = tid; k < ovl; k += blockDim.x) s_ovh[k] = data[e1 + k];
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        st_release_u32(flag + b, 1u);
+    }
+    // spilled partial buffers of every stripe of this task for bucket b
+    const u32 S0 = tp.stripe_begin, NS = tp.nstripes;
+    u32 sp_total = 0;
+    for (u32 base = 0; base < NS; base += K4_THREADS) {
+        const u32 j = base + tid;
+        const u32 len = j < NS ? A.s_fill[(u64)(S0 + j) * MAXK + b] : 0u;
+        u32 incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (u32)o) incl += y;
+        }
+        if (lane == 31) s_wsum[w] = incl;
+        __syncthreads();
+        u32 woff = 0, tot = 0;
+        for (u32 ww = 0; ww < K4_THREADS / 32; ++ww) {
+            if (ww < w) woff += s_wsum[ww];
+            tot += s_wsum[ww];
+        }
+        if (j < NS) s_pref[j] = sp_total + woff + incl - len;
+        sp_total += tot;
+        __syncthreads();
+    }
+    if (tid == 0) s_pref[NS] = sp_total;
+    const u32 nsrc = ovl + sp_total + (own_ovf ? (u32)B : 0u);
+    const u64 hend = db_el < e1 ? db_el : e1;
+    const u64 ts = db_el < e1 ? (in_end < e1 ? in_end : e1) : e1;
+    const u64 hl = hend - e0;
+    const u64 nslots = hl + (e1 - ts);
+    if ((u64)nsrc != nslots) {
+        if (tid == 0) atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_CONSERVE);
+        return;
+    }
+    // wait until the bucket owning block d-1 (which holds our head) saved its overhang
+    if (tid == 0 && hl > 0 && d >= 1) {
+        const u32 x = d - 1;
+        u32 lo = 0, hi = b;  // largest o < b with dbl[o] <= x
+        while (hi - lo > 1) {
+            u32 mid = (lo + hi) >> 1;
+            if (dbl[mid] <= x) lo = mid;
+            else hi = mid;
+        }
+        if (lo < b) {
+            while (ld_acquire_u32(flag + lo) == 0u) __nanosleep(100);
+        }
+    }
+    __syncthreads();
+    const V* spill = reinterpret_cast<const V*>(A.spill);
+    const V* ovf = reinterpret_cast<const V*>(A.ovf) + (u64)t * B;
+    for (u32 k = tid; k < nsrc; k += blockDim.x) {
+        V val;
+        if (k < ovl) {
+            val = s_ovh[k];
+        } else if (k - ovl < sp_total) {
+            const u32 kk = k - ovl;
+            u32 lo = 0, hi = NS;  // last j with s_pref[j] <= kk
+            while (hi - lo > 1) {
+                u32 mid = (lo + hi) >> 1;
+                if (s_pref[mid] <= kk) lo = mid;
+                else hi = mid;
+            }
+            const u64 at = A.s_spbase[S0 + lo] + A.s_spoff[(u64)(S0 + lo) * MAXK + b] + (kk - s_pref[lo]);
+            val = spill[at];
+        } else {
+            val = ovf[k - ovl - sp_total];
+        }
+        const u64 dst = (u64)k < hl ? e0 + k : ts + (k - hl);
+        data[dst] = val;
+    }
+    // emit the bucket (equality buckets are never recursed into)
+    if (tid == 0 && A.emit) {
+        const u64 sz = e1 - e0;
+        const bool eqb = tp.eq && (b & 1u);
+        if (sz > 1 && !eqb) {
+            if (sz <= A.base_cap) {
+                u32 i = atomicAdd(&A.ctr[CTR_BASE], 1u);
+                if (i < A.q_cap) A.q_base[i] = TaskDesc{e0, e1};
+                else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
+            } else {
+                u32 i = atomicAdd(&A.ctr[CTR_NEXT], 1u);
+                if (i < A.q_cap) A.q_next[i] = TaskDesc{e0, e1};
+                else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
+            }
+        }
+    }
+}
+
+}  // namespace ips4o

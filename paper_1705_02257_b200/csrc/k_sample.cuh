@@ -1,0 +1,135 @@
+// k_sample.cuh -- K1: oversampled splitter selection and the implicit search tree.
+//
+// One CTA per task.  PAPER.md:134-141 (§3): sort alpha*k-1 sampled elements, pick k-1
+// equidistant splitters, store them as a complete binary search tree a_1 = s_{k/2},
+// a_2 = s_{k/4}, a_3 = s_{3k/4}, ...  PAPER.md:399-401 (§4.7): remove duplicate
+// splitters; equality buckets only if duplicates were found.  alpha = 0.2 log n
+// (PAPER.md:414).  The sample lives in shared memory instead of being swapped to the
+// front of the array: same splitters, no writes to the input.
+#pragma once
+#include "common.cuh"
+
+namespace ips4o {
+
+constexpr int K1_THREADS = 1024;
+constexpr int K1_SAMPLE = 2048;  // >= alpha*k - 1 for n < 2^42
+
+// Builds the padded splitter array spl[1..k'-1] and the BFS tree from nd distinct sorted
+// splitters held in s_dist[0..nd).  k' = next power of two >= nd+1; padding repeats the
+// largest splitter.  Writes the task's classifier fields.
+__device__ void build_tree_block(const u64* s_dist, u32 nd, u32 eq, u64* g_tree, u64* g_spl,
+                                 TaskParam* tp) {
+    u32 kp = 2;
+    while (kp < nd + 1) kp <<= 1;
+    u32 logk = 0;
+    while ((1u << logk) < kp) ++logk;
+    for (u32 i = threadIdx.x; i < (u32)MAXK; i += blockDim.x) {
+        u64 s = 0;
+        if (i >= 1 && i < kp) s = s_dist[(i <= nd ? i : nd) - 1];
+        g_spl[i] = s;
+    }
+    for (u32 j = threadIdx.x; j < (u32)MAXK; j += blockDim.x) {
+        u64 v = 0;
+        if (j >= 1 && j < kp) {
+            u32 l = 31 - __clz(j);
+            u32 pos = j - (1u << l);
+            u32 idx = (2 * pos + 1) * (kp >> (l + 1));  // 1-based splitter index
+            v = s_dist[(idx <= nd ? idx : nd) - 1];
+        }
+        g_tree[j] = v;
+    }
+    if (threadIdx.x == 0) {
+        tp->kprime = kp;
+        tp->logk = logk;
+        tp->eq = eq;
+        tp->K = eq ? 2 * kp - 1 : kp;
+    }
+}
+
+template <class TR>
+__global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
+    typedef typename TR::V V;
+    __shared__ u64 keys[K1_SAMPLE];
+    __shared__ u64 dist[MAXK];
+    __shared__ u32 s_flag, s_nd;
+    const u32 t = blockIdx.x;
+    TaskParam* tp = const_cast<TaskParam*>(A.tp) + t;
+    const u64 lo = tp->lo, hi = tp->hi, n = hi - lo;
+    const V* data = reinterpret_cast<const V*>(A.data);
+
+    // k = min(256, max(4, pow2_floor(n/16))) and alpha = max(1, round(0.2 log2 n))
+    u64 q = n / 16;
+    u32 k = 4;
+    while ((u64)k * 2 <= q && k < (u32)MAXK) k *= 2;
+    u32 alpha = (u32)llround(0.2 * log2((double)n));
+    if (alpha < 1) alpha = 1;
+    u32 m = alpha * k - 1;
+    if (m > K1_SAMPLE) m = K1_SAMPLE - 1;
+    if ((u64)m > n) m = (u32)n;
+
+    // stratified random sample without replacement: one element per stratum
+    for (u32 j = threadIdx.x; j < (u32)K1_SAMPLE; j += blockDim.x) {
+        u64 key = ~0ull;
+        if (j < m) {
+            u64 a = lo + (u64)((unsigned __int128)n * j / m);
+            u64 b = lo + (u64)((unsigned __int128)n * (j + 1) / m);
+            u64 r = mix64(A.seed ^ mix64(lo * 0x9E3779B97F4A7C15ull + j));
+            key = TR::key(data[a + r % (b - a)]);
+        }
+        keys[j] = key;
+    }
+    __syncthreads();
+    // bitonic sort of the 2048 sampled keys in shared memory
+    for (u32 kk = 2; kk <= (u32)K1_SAMPLE; kk <<= 1) {
+        for (u32 jj = kk >> 1; jj > 0; jj >>= 1) {
+            for (u32 p = threadIdx.x; p < (u32)K1_SAMPLE / 2; p += blockDim.x) {
+                u32 i = 2 * p - (p & (jj - 1));
+                u32 x = i + jj;
+                bool up = (i & kk) == 0;
+                u64 a = keys[i], b = keys[x];
+                if ((a > b) == up) {
+                    keys[i] = b;
+                    keys[x] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // equidistant picks s_i = S[i*alpha - 1]; duplicates?
+    if (threadIdx.x == 0) s_flag = 0;
+    __syncthreads();
+    for (u32 i = 1 + threadIdx.x; i + 1 < k; i += blockDim.x)
+        if (keys[i * alpha - 1] == keys[(i + 1) * alpha - 1]) s_flag = 1;
+    __syncthreads();
+    u32 eq = s_flag;
+    if (!eq) {
+        for (u32 i = threadIdx.x; i + 1 < k; i += blockDim.x) dist[i] = keys[(i + 1) * alpha - 1];
+        if (threadIdx.x == 0) s_nd = k - 1;
+    } else {
+        // Equality buckets.  Take k/2-1 equidistant picks so
+        // that 2k'-1 <= 255 buckets fit the shared-memory budget, then keep
+        // one copy of each distinct value.
+        const u32 k2 = k / 2, a2 = 2 * alpha;
+        if (threadIdx.x == 0) {
+            u32 nd = 0;
+            for (u32 i = 1; i < k2; ++i) {
+                u64 v = keys[i * a2 - 1];
+                if (nd == 0 || dist[nd - 1] != v) dist[nd++] = v;
+            }
+            s_nd = nd;
+        }
+    }
+    __syncthreads();
+    build_tree_block(dist, s_nd, eq, A.tree + (u64)t * MAXK, A.spl + (u64)t * MAXK, tp);
+    if (threadIdx.x == 0 && eq) atomicAdd(&A.ctr[CTR_EQ], 1u);
+}
+
+// Debug path: classifier from splitters given by the caller (already key-transformed).
+__global__ void k_tree_from_splitters(LevelArgs A, const u64* splitters, u32 nspl, u32 eq) {
+    __shared__ u64 dist[MAXK];
+    for (u32 i = threadIdx.x; i < nspl; i += blockDim.x) dist[i] = splitters[i];
+    __syncthreads();
+    build_tree_block(dist, nspl, eq, A.tree, A.spl, const_cast<TaskParam*>(A.tp));
+}
+
+}  // namespace ips4o

@@ -1,0 +1,62 @@
+"""The C-ABI library builds, loads without a GPU and exports every symbol include/ips4o.h
+declares; host-only entry points behave (-m "not gpu")."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1705_02257_b200 as ips4o
+from paper_1705_02257_b200 import builder as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return ips4o.lib()
+
+
+def _declared():
+    txt = open(os.path.join(ROOT, "include", "ips4o.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(ips4o_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_header_declares_binding_exports():
+    assert sorted(ips4o.EXPORTS) == _declared()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    raw = ctypes.CDLL(ips4o.LIB_PATH)
+    for name in _declared():
+        assert hasattr(raw, name), name
+
+
+def test_host_only_calls(lib):
+    # n <= 1 and argument errors return without touching a device
+    assert lib.ips4o_sort(None, 0, 0, None) == 0
+    assert lib.ips4o_sort(None, 5, 0, None) == -1          # null pointer, n > 0
+    assert lib.ips4o_sort(ctypes.c_void_p(8), 5, 9, None) == -1   # bad type
+    assert lib.ips4o_sort(ctypes.c_void_p(12), 5, 0, None) == -2  # misaligned u64
+    assert lib.ips4o_sort(ctypes.c_void_p(8), 5, 2, None) == -2   # pair needs 16 B
+    assert b"aligned" in lib.ips4o_error_string(-2)
+    assert lib.ips4o_kernel_kind_name(1) == b"classify_flush"
+
+
+def test_aux_bytes_sublinear(lib):
+    """Theorem 2: O(k b t) -- bounded independently of n for large n."""
+    a24 = ips4o.ips4o_aux_bytes(1 << 24, 0)
+    a28 = ips4o.ips4o_aux_bytes(1 << 28, 0)
+    a32 = ips4o.ips4o_aux_bytes(1 << 32, 0)
+    assert a28 == a32                      # independent of n beyond the k*b*stripes term
+    assert a28 < 0.05 * (8 << 28)          # < 5 % of the 2 GiB input at the headline size
+    assert a24 <= a28
+
+
+def test_no_cpu_fallback_in_product():
+    """The product package never imports the oracle or a CPU sort."""
+    src = open(os.path.join(ROOT, "paper_1705_02257_b200", "__init__.py")).read()
+    assert "oracle" not in src.replace("oracle/", "")
+    assert "np.sort" not in src and "torch.sort" not in src

@@ -1,0 +1,271 @@
+"""CUDA path vs the oracle (-m gpu).  Everything calls through the C ABI of libips4o.so.
+
+Layers (SURVEY.md §4 "build test layers"):
+  (ii)  classification (T1) vs oracle.classify, exhaustive small domains + random k=256;
+  (iii) one distribution step (T2) vs oracle.partition_with: identical e_i, per-bucket
+        multisets, every element of [e_i, e_{i+1}) in bucket i;
+  (iv)  whole sorts bit-exact vs oracle.sort on every distribution and type, sizes that
+        span several tiles / stripes / levels with ragged tails, degenerate inputs;
+  (v)   full BASELINE sizes in the bench launch configuration: non-decreasing keys and an
+        equal multiset digest (properties that hold at any size), plus exact oracle
+        parity where the oracle finishes in seconds (config 1).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import paper_1705_02257_b200 as ips4o  # noqa: E402
+import workloads as W  # noqa: E402
+from tests.gpu_util import (check_equal_to_oracle, digest, keys_nondecreasing, to_dev,  # noqa: E402
+                            to_host)
+
+TYPES = [W.ELEM_U64, W.ELEM_F64, W.ELEM_PAIR]
+CAP = {W.ELEM_U64: 16384, W.ELEM_F64: 16384, W.ELEM_PAIR: 8192}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    ips4o.lib()
+    torch.cuda.set_device(0)
+
+
+def _gen(et, n, seed, kind="uniform"):
+    rng = np.random.default_rng(seed)
+    if et == W.ELEM_U64:
+        if kind == "uniform":
+            return W.u64_uniform(n, seed)
+        if kind == "few":
+            return rng.integers(0, 7, size=n).astype(np.uint64)
+        if kind == "max":
+            return np.where(rng.random(n) < 0.5, np.uint64(2**64 - 1), np.uint64(0)).astype(np.uint64)
+    if et == W.ELEM_F64:
+        if kind == "uniform":
+            return W.f64_exponential(n, seed)
+        if kind == "few":
+            return rng.integers(0, 7, size=n).astype(np.float64) - 3.0
+        if kind == "max":
+            x = rng.standard_normal(n) * 1e300
+            x[x == 0] = 1.0
+            return x
+    if et == W.ELEM_PAIR:
+        a = W.pair16(n, seed)
+        if kind == "few":
+            a[:, 0] = rng.integers(0, 7, size=n).astype(np.uint64)
+        if kind == "max":
+            a[:, 0] = np.where(rng.random(n) < 0.5, np.uint64(2**64 - 1), np.uint64(0))
+        return a
+    raise ValueError
+
+
+def _sort_gpu(a, et):
+    t = to_dev(a, et)
+    ips4o.sort_(t)
+    torch.cuda.synchronize()
+    return to_host(t, et)
+
+
+# ------------------------------------------------------------- (ii) classification
+
+def _spl_keys(spl, et):
+    return spl.astype(np.float64) if et == W.ELEM_F64 else spl.astype(np.uint64)
+
+
+@pytest.mark.parametrize("et", TYPES)
+@pytest.mark.parametrize("eq", [False, True])
+def test_classify_vs_oracle(et, eq):
+    rng = np.random.default_rng(100 + et)
+    for trial in range(20):
+        nspl = int(rng.integers(1, 128 if eq else 256)) if trial % 3 else int(rng.integers(1, 8))
+        if et == W.ELEM_F64:
+            spl = np.unique(rng.standard_normal(nspl * 2))[:nspl]
+            x = np.concatenate([rng.standard_normal(5000), spl, -spl])
+            x[x == 0] = 0.5
+            elems = x
+        elif trial % 3 == 0:
+            spl = np.unique(rng.choice(64, size=nspl, replace=False)).astype(np.uint64)
+            elems = np.arange(64, dtype=np.uint64)
+        else:
+            spl = np.unique(rng.integers(0, 1 << 40, size=nspl * 2, dtype=np.uint64))[:nspl]
+            elems = np.concatenate([rng.integers(0, 1 << 40, size=5000, dtype=np.uint64), spl])
+        if et == W.ELEM_PAIR:
+            el = np.stack([elems.astype(np.uint64), np.arange(elems.shape[0], dtype=np.uint64)], axis=1)
+        else:
+            el = elems
+        exp = oracle.classify(spl, eq, el)
+        d_in = to_dev(el, et)
+        out = torch.empty(el.shape[0], dtype=torch.int32, device="cuda")
+        buf, ptr, ns = ips4o.splitters_buffer(_spl_keys(spl, et), et)
+        ips4o.ips4o_debug_classify(d_in.data_ptr(), el.shape[0], et, ptr, ns, eq, out.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, exp), (et, eq, trial)
+
+
+# ------------------------------------------------------------ (iii) one step
+
+def _partition_case(et, n, nspl, eq, seed, offset=0, kind="uniform"):
+    rng = np.random.default_rng(seed)
+    a = _gen(et, n + offset, seed, kind)
+    keys = a[:, 0] if et == W.ELEM_PAIR else a
+    pool = np.unique(keys[offset:])
+    nspl = min(nspl, pool.shape[0])
+    spl = np.sort(rng.choice(pool, size=nspl, replace=False))
+    # oracle on the sub-array [offset, offset+n)
+    sub = np.ascontiguousarray(a[offset:])
+    o_out, o_bounds = oracle.partition_with(sub, spl, eq, 16)
+    d = to_dev(a, et)
+    esz = 16 if et == W.ELEM_PAIR else 8
+    buf, ptr, ns = ips4o.splitters_buffer(_spl_keys(spl, et), et)
+    bounds, K = ips4o.ips4o_debug_partition_once(d.data_ptr() + offset * esz, n, et, ptr, ns, eq,
+                                                 torch.cuda.current_stream().cuda_stream)
+    got = to_host(d, et)
+    assert np.array_equal(np.array(bounds), o_bounds), "bucket bounds e_i differ from the oracle"
+    assert (got[:offset] == a[:offset]).all()       # nothing outside the range was touched
+    g = got[offset:]
+    cls = oracle.classify(spl, eq, g)
+    for i in range(K):
+        seg = cls[bounds[i]:bounds[i + 1]]
+        assert (seg == i).all(), f"bucket {i} holds foreign elements"
+    # per-bucket multisets equal to the oracle's
+    for i in range(K):
+        gs, os_ = g[bounds[i]:bounds[i + 1]], o_out[bounds[i]:bounds[i + 1]]
+        if et == W.ELEM_PAIR:
+            gs = np.sort(gs.view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k", "v"])
+            os_ = np.sort(os_.view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k", "v"])
+        else:
+            gs, os_ = np.sort(gs), np.sort(os_)
+        assert np.array_equal(gs, os_)
+
+
+@pytest.mark.parametrize("et", TYPES)
+def test_partition_once_vs_oracle(et):
+    cases = [(64, 3, False), (1000, 7, False), (4099, 255, False), (100_003, 255, False),
+             (300_001, 100, True), (2_000_003, 255, False), (1_500_017, 127, True)]
+    for i, (n, nspl, eq) in enumerate(cases):
+        _partition_case(et, n, nspl, eq, seed=7 + i)
+
+
+@pytest.mark.parametrize("et", [W.ELEM_U64, W.ELEM_F64])
+def test_partition_once_misaligned_start(et):
+    """Data starting at an 8-byte (not 16-byte) boundary: head element + shifted block grid."""
+    for i, n in enumerate([777, 65_537, 1_000_001]):
+        _partition_case(et, n, 255, False, seed=50 + i, offset=1)
+        _partition_case(et, n, 63, True, seed=60 + i, offset=1, kind="few")
+
+
+def test_partition_once_duplicates_and_skew():
+    _partition_case(W.ELEM_U64, 500_000, 3, True, seed=3, kind="few")
+    _partition_case(W.ELEM_U64, 500_000, 1, False, seed=4, kind="few")
+    _partition_case(W.ELEM_U64, 200_000, 1, True, seed=5, kind="max")
+
+
+# ------------------------------------------------------------ (iv) whole sorts
+
+SIZES = [0, 1, 2, 3, 17, 1000, 16383, 16384, 16385, 40_000, 131_073, 1_000_003, 3_000_017]
+
+
+@pytest.mark.parametrize("et", TYPES)
+def test_sort_sizes_vs_oracle(et):
+    for i, n in enumerate(SIZES):
+        a = _gen(et, n, 1000 + i)
+        got = _sort_gpu(a, et)
+        exp = oracle.sort(a)
+        check_equal_to_oracle(et, a, got, exp)
+
+
+@pytest.mark.parametrize("et", TYPES)
+@pytest.mark.parametrize("kind", ["few", "max"])
+def test_sort_duplicates_vs_oracle(et, kind):
+    for n in (5000, 70_001, 2_000_000):
+        a = _gen(et, n, 77, kind)
+        check_equal_to_oracle(et, a, _sort_gpu(a, et), oracle.sort(a))
+
+
+@pytest.mark.parametrize("dist", ["rootdup", "twodup", "eightdup", "almostsorted", "reversesorted",
+                                  "sorted", "zeros", "ones", "uniform", "f64_uniform", "f64_exponential",
+                                  "pair16"])
+def test_distributions_vs_oracle(dist):
+    for seed in (1, 2, 3):
+        et, a = W.make(dist, 1 << 21, seed)
+        check_equal_to_oracle(et, a, _sort_gpu(a, et), oracle.sort(a))
+
+
+def test_config1_full_size_vs_oracle():
+    """BASELINE config 1 (2^20 uniform u64) at full size, seeds 1-3."""
+    for seed in (1, 2, 3):
+        a = W.u64_uniform(1 << 20, seed)
+        got = _sort_gpu(a, W.ELEM_U64)
+        assert np.array_equal(got, oracle.sort(a))
+
+
+def test_misaligned_whole_sort():
+    a = W.u64_uniform((1 << 20) + 3, 9)
+    t = to_dev(a, W.ELEM_U64)
+    sub = t[1:]
+    ips4o.ips4o_sort(sub.data_ptr(), sub.shape[0], W.ELEM_U64, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    got = to_host(t, W.ELEM_U64)
+    assert got[0] == a[0]
+    assert np.array_equal(got[1:], oracle.sort(a[1:]))
+
+
+def test_equality_buckets_all_zero_one_step():
+    """All-equal input is an easy instance: one distribution step."""
+    a = np.zeros(1 << 22, dtype=np.uint64)
+    got = _sort_gpu(a, W.ELEM_U64)
+    assert (got == 0).all()
+    st = ips4o.ips4o_last_stats()
+    assert st["distribution_tasks"] == 1 and st["equality_tasks"] == 1 and st["base_tasks"] == 0
+
+
+def test_stats_and_aux_bytes():
+    n = 1 << 24
+    a = W.u64_uniform(n, 4)
+    _sort_gpu(a, W.ELEM_U64)
+    st = ips4o.ips4o_last_stats()
+    assert st["aux_bytes"] <= ips4o.ips4o_aux_bytes(n, W.ELEM_U64)
+    assert st["aux_bytes"] < 0.1 * n * 8
+    assert st["levels"] == 2
+
+
+def test_sort_host_entry_point():
+    a = W.u64_uniform(1 << 20, 11)
+    h = a.copy()
+    ips4o.ips4o_sort_host(h.ctypes.data, h.shape[0], W.ELEM_U64, 0)
+    assert np.array_equal(h, oracle.sort(a))
+
+
+def test_type_switching_and_reuse():
+    for et in (W.ELEM_PAIR, W.ELEM_U64, W.ELEM_F64, W.ELEM_PAIR):
+        a = _gen(et, 200_001, 5)
+        check_equal_to_oracle(et, a, _sort_gpu(a, et), oracle.sort(a))
+
+
+# ------------------------------------------------------ (v) full BASELINE sizes
+
+FULL = [("uniform", 28), ("f64_uniform", 28), ("f64_exponential", 28), ("rootdup", 27),
+        ("twodup", 27), ("eightdup", 27), ("almostsorted", 27), ("reversesorted", 27),
+        ("zeros", 27), ("pair16", 27)]
+
+
+@pytest.mark.parametrize("dist,e", FULL)
+def test_full_size_properties(dist, e):
+    et, a = W.make(dist, 1 << e, 1)
+    t = to_dev(a, et)
+    del a
+    before = digest(t)
+    ips4o.sort_(t)
+    torch.cuda.synchronize()
+    assert keys_nondecreasing(t, et)
+    assert digest(t) == before
+    if et == W.ELEM_PAIR:
+        # payload = original index: a permutation of 0..n-1 travelling with its key
+        pay = t.view(torch.int64)[:, 1]
+        assert int(pay.sum().item()) == (1 << e) * ((1 << e) - 1) // 2
