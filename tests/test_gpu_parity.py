@@ -22,7 +22,7 @@ torch = pytest.importorskip("torch")
 import oracle  # noqa: E402
 import paper_1705_02257_b200 as ips4o  # noqa: E402
 import workloads as W  # noqa: E402
-from tests.gpu_util import (check_equal_to_oracle, digest, keys_nondecreasing, to_dev,  # noqa: E402
+from gpu_util import (check_equal_to_oracle, digest, keys_nondecreasing, to_dev,  # noqa: E402
                             to_host)
 
 TYPES = [W.ELEM_U64, W.ELEM_F64, W.ELEM_PAIR]
