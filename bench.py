@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the IPS4o hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config H|C1|C2a|C2b|C3_*|C4] [--impl ours|reference]
+
+One step = one in-place ips4o_sort of the whole synthetic workload (all distribution levels
+and the base case), inputs resident in HBM.  The input is larger than L2 and is restored
+from a pristine device copy before every step, outside the timed region (an in-place sort
+destroys its input); each step is bracketed by CUDA events on the sorting stream.
+
+Multi-GPU: the north star is one GPU; N > 1 runs independent replicas (one process per GPU,
+each sorting its own copy), value = total elements / max-over-ranks time ("weak" scaling).
+
+--impl reference times the CPU oracle (oracle/, the paper's sequential IS4o written from the
+paper) on a bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "Gelem/s sorted in-place on 1 B200 (2^28 u64) and % of HBM-pass roofline"
+
+# name -> (distribution, log2 n, description)
+CONFIGS = {
+    "H": ("uniform", 28, "H: 2^28 u64 keys i.i.d. uniform over [0,2^64), seed 1 (headline)"),
+    "C1": ("uniform", 20, "C1: 2^20 u64 uniform, seed 1 (L2-resident)"),
+    "C2a": ("f64_uniform", 28, "C2a: 2^28 f64 uniform [0,1), seed 1"),
+    "C2b": ("f64_exponential", 28, "C2b: 2^28 f64 exponential(1), seed 1"),
+    "C3_rootdup": ("rootdup", 27, "C3: 2^27 u64 RootDup"),
+    "C3_twodup": ("twodup", 27, "C3: 2^27 u64 TwoDup"),
+    "C3_eightdup": ("eightdup", 27, "C3: 2^27 u64 EightDup"),
+    "C3_almostsorted": ("almostsorted", 27, "C3: 2^27 u64 AlmostSorted"),
+    "C3_reversesorted": ("reversesorted", 27, "C3: 2^27 u64 ReverseSorted"),
+    "C3_zeros": ("zeros", 27, "C3: 2^27 u64 all-zero"),
+    "C4": ("pair16", 27, "C4: 2^27 Pair16 (u64 key uniform [0,2^32), payload = index)"),
+    "C5": ("rec100", 24, "C5: 2^24 100-byte records (10-byte key)"),
+}
+DTYPE = {W.ELEM_U64: "u64", W.ELEM_F64: "f64", W.ELEM_PAIR: "u64x2", W.ELEM_REC100: "u8x100"}
+BW_NOMINAL = 8000.0  # GB/s, the north star's "roughly 8 TB/s"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", d
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)", {}
+
+
+def levels_for(n: int, esize: int) -> int:
+    """L = ceil(log_256(n / n_base)), n_base = 4096 (2048 for 100-byte records)."""
+    nb = 2048 if esize == 100 else 4096
+    if n <= nb:
+        return 1
+    return max(1, math.ceil(math.log(n / nb, 256) - 1e-12))
+
+
+# ------------------------------------------------------------------ clocks sampler
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.out = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thr = threading.Thread(target=self._read, daemon=True)
+            self.thr.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.out.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thr.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_input(cfg: str, n_override: int | None = None):
+    dist, e, desc = CONFIGS[cfg]
+    n = n_override or (1 << e)
+    et, a = W.make(dist, n, 1)
+    return et, a, desc
+
+
+def host_to_device(a: np.ndarray, et: int):
+    import torch
+    if et == W.ELEM_F64:
+        return torch.from_numpy(a).cuda()
+    if et in (W.ELEM_U64, W.ELEM_PAIR):
+        return torch.from_numpy(a.view(np.int64)).cuda().view(torch.uint64)
+    return torch.from_numpy(a).cuda()
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args):
+    """The oracle as it stands on the host cores, on bounded samples of the workload."""
+    import oracle
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    dist, e, desc = CONFIGS[args.config]
+    n_full = 1 << e
+    sample = min(n_full, 1 << args.ref_log2)
+    et, a = W.make(dist, sample, 1)
+    esize = W.ELEM_SIZE[et]
+    for _ in range(args.warmup):
+        oracle.sort(a[: min(sample, 1 << 16)])
+    times = []
+    for _ in range(args.steps):
+        b = a.copy()
+        t0 = time.perf_counter()
+        oracle.sort_inplace(b)
+        times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    val = sample / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "Gelem/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE[et],
+        "data": "synthetic",
+        "config": {"workload": desc, "n": n_full, "elem_bytes": esize, "sample_n": sample},
+        "cpu_baseline": {"value": val, "unit": "Gelem/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{dist} n=2^{int(math.log2(sample))} (seed 1) per step, "
+                                   f"oracle/ sequential IS4o, 1 thread"},
+        "e2e": {"value": val, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(dist: str, log2: int, secs_target: float = 15.0):
+    """Oracle on a bounded sample (rank 0, N=1 only)."""
+    import oracle
+    n = 1 << log2
+    et, a = W.make(dist, n, 1)
+    b = a.copy()
+    t0 = time.perf_counter()
+    oracle.sort_inplace(b)
+    t = time.perf_counter() - t0
+    reps = 1
+    return {"value": n / t / 1e9, "unit": "Gelem/s", "cores": 1, "kind": "oracle",
+            "sample": f"{dist} n=2^{log2} (seed 1), {reps} run, {t:.1f} s; oracle/ sequential IS4o "
+                      f"(PAPER.md:419), 1 thread"}
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args):
+    import torch
+    import paper_1705_02257_b200 as ips4o
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ips4o.lib()
+    et, a, desc = make_input(args.config, args.n)
+    n = a.shape[0]
+    esize = W.ELEM_SIZE[et]
+    pristine = host_to_device(a, et)
+    work = pristine.clone()
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    def one_sort():
+        ips4o.ips4o_sort(work.data_ptr(), n, et, sptr)
+
+    for _ in range(max(args.warmup, 0)):
+        work.copy_(pristine)
+        one_sort()
+    torch.cuda.synchronize()
+
+    # timed region: K steps, per-step events around the sort only
+    ips4o.ips4o_profile_enable(True)
+    ips4o.ips4o_profile_read()  # clear
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    launches = 0
+    stats = None
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            work.copy_(pristine)
+            evs[i][0].record(stream)
+            one_sort()
+            evs[i][1].record(stream)
+            stats = ips4o.ips4o_last_stats()
+            launches += stats["kernel_launches"]
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in evs]
+    prof = ips4o.ips4o_profile_read()
+    ips4o.ips4o_profile_enable(False)
+    mean_ms = statistics.mean(step_ms)
+    tot_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([tot_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        mean_ms = tot_ms / args.steps
+    # verify the last output (never report an unverified run)
+    ok = verify(work, et, pristine)
+
+    # end-to-end: host (pinned) buffer -> device -> sort -> host, through the C ABI
+    e2e = None
+    if rank == 0 and args.e2e_steps > 0:
+        h = torch.empty(tuple(work.shape), dtype=work.dtype, pin_memory=True)
+        hsrc = pristine.cpu().pin_memory()
+        e2e_t = []
+        for i in range(args.e2e_steps + 1):
+            h.copy_(hsrc)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ips4o.ips4o_sort_host(h.data_ptr(), n, et, sptr)
+            dt = time.perf_counter() - t0
+            if i > 0:
+                e2e_t.append(dt)
+        e2e = {"value": n / statistics.mean(e2e_t) / 1e9, "unit": "Gelem/s",
+               "h2d_bytes_per_step": n * esize, "d2h_bytes_per_step": n * esize,
+               "ms_per_step": statistics.mean(e2e_t) * 1e3, "path": "ips4o_sort_host (pinned host buffer)"}
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+
+    peak, peak_src, peaks = measured_peaks()
+    # dominant kernel and its roofline (algorithmic bytes / live event-timed duration)
+    kinds = {k: v for k, v in prof.items() if v[0] > 0}
+    dom = max(kinds, key=lambda k: kinds[k][1])
+    nl, msk = kinds[dom]
+    dist_el = stats["distributed_elements"]
+    base_el = stats["base_elements"]
+    per_step_bytes = {
+        "classify_flush": 2 * dist_el * esize,   # read every element + flush write
+        "block_permute": 2 * dist_el * esize,    # read + write of every block
+        "base_case": 2 * base_el * esize,        # read + write once
+    }
+    launches_per_step = nl / args.steps
+    roof = None
+    if dom in per_step_bytes:
+        bytes_per_launch = per_step_bytes[dom] / launches_per_step
+        avg_ms = msk / nl
+        achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9
+        traffic = load_traffic(args.config, dom)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+                "share_of_step": msk / sum(v[1] for v in kinds.values())}
+    L = levels_for(n, esize)
+    t_roof_nom = 4 * n * esize * L / (BW_NOMINAL * 1e9)
+    t_roof_meas = 4 * n * esize * L / (peak * 1e9)
+    per_gpu_s = mean_ms * 1e-3
+    value = ws * n / per_gpu_s / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": DTYPE[et], "data": "synthetic",
+        "config": {"workload": desc, "n": n, "elem_bytes": esize,
+                   "parallelism": "replicas" if ws > 1 else "single-gpu",
+                   "l2": "input larger than L2 (126 MB) except C1; restored from a pristine device "
+                         "copy before every step, outside the events"},
+        "roofline": roof,
+        "step_roofline": {"levels": L, "bytes": 4 * n * esize * L,
+                          "frac_at_8TBs": t_roof_nom / per_gpu_s, "frac_at_measured": t_roof_meas / per_gpu_s},
+        "kernels_ms_per_step": {k: v[1] / args.steps for k, v in kinds.items()},
+        "gpu_launches": launches,
+        "verified": ok,
+        "aux_bytes": stats["aux_bytes"], "aux_frac_of_input": stats["aux_bytes"] / (n * esize),
+        "sort_stats": stats,
+        "clocks": clk.summary(),
+        "ms_per_step_min": min(step_ms), "ms_per_step_median": statistics.median(step_ms),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if ws == 1 and not args.no_cpu_baseline:
+        dist_name = CONFIGS[args.config][0]
+        line["cpu_baseline"] = cpu_baseline(dist_name, min(CONFIGS[args.config][1], args.cpu_log2))
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0 if ok else 1
+
+
+def load_traffic(cfg: str, kernel: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    v = d.get(cfg, {}).get(kernel)
+    return v
+
+
+def verify(work, et, pristine) -> bool:
+    """Keys non-decreasing and equal multiset digest (properties that hold at any size)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from gpu_util import digest, keys_nondecreasing
+    return keys_nondecreasing(work, et) and digest(work) == digest(pristine)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="H", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="override n (debug)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-log2", type=int, default=25)
+    ap.add_argument("--ref-log2", type=int, default=23)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -68,6 +68,8 @@ typedef struct {
     uint64_t aux_bytes;         /* device workspace bytes reserved for this call */
     uint64_t kernel_launches;   /* kernels launched by this call */
     uint64_t host_syncs;        /* stream synchronisations performed (one per level) */
+    uint64_t distributed_elements; /* sum over distribution steps of the subproblem sizes */
+    uint64_t base_elements;     /* sum of the base-case subproblem sizes */
 } ips4o_stats;
 
 /* ---------------------------------------------------------------- sorting */

@@ -36,7 +36,8 @@ class Stats(ctypes.Structure):
     _fields_ = [("n", ctypes.c_uint64), ("elem_type", ctypes.c_uint32), ("levels", ctypes.c_uint32),
                 ("distribution_tasks", ctypes.c_uint64), ("base_tasks", ctypes.c_uint64),
                 ("equality_tasks", ctypes.c_uint64), ("aux_bytes", ctypes.c_uint64),
-                ("kernel_launches", ctypes.c_uint64), ("host_syncs", ctypes.c_uint64)]
+                ("kernel_launches", ctypes.c_uint64), ("host_syncs", ctypes.c_uint64),
+                ("distributed_elements", ctypes.c_uint64), ("base_elements", ctypes.c_uint64)]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

@@ -122,6 +122,7 @@ struct LevelArgs {
     u32 q_cap;
     u32* ctr;         // [CTR_N]
     u64* spill_ctr;
+    u64* base_elems;  // sum of sizes of emitted base-case tasks
     u32 base_cap;     // tasks with <= base_cap elements go to the base case
     int emit;         // emit next-level / base tasks (0 for the debug single step)
     u64 seed;

@@ -118,7 +118,7 @@ static size_t fixed_bytes() {
     add((size_t)MAXT * BLOCK_BYTES);           // ovf
     add(MAXT * 4);                             // ovf_owner
     add((size_t)QCAP * sizeof(TaskDesc) * 2);  // queues
-    add(CTR_N * 4 + 8);                        // ctr + spill ctr
+    add(CTR_N * 4 + 16);                       // ctr + spill ctr + base-element ctr
     add(MAXK * 8);                             // debug splitters
     return s;
 }
@@ -193,7 +193,7 @@ static int ensure_ws(u64 n, int esize) {
     char* q = take((size_t)QCAP * sizeof(TaskDesc) * 2);
     g_ws.q_next = (TaskDesc*)q;
     g_ws.q_base = g_ws.q_next + QCAP;
-    char* c = take(CTR_N * 4 + 8);
+    char* c = take(CTR_N * 4 + 16);
     g_ws.ctr = (u32*)c;
     g_ws.spill_ctr = (u64*)(c + CTR_N * 4);
     g_ws.dsplit = (u64*)take(MAXK * 8);
@@ -201,7 +201,7 @@ static int ensure_ws(u64 n, int esize) {
     g_ws.spill_elems = (g_ws.dev_bytes - fixed_bytes()) / esize;
     g_ws.spill_elem_size = esize;
     if (!g_ws.host) {
-        size_t hb = MAXT * sizeof(TaskParam) + MAXS * sizeof(StripeDesc) + MAXS * 4 + CTR_N * 4 +
+        size_t hb = MAXT * sizeof(TaskParam) + MAXS * sizeof(StripeDesc) + MAXS * 4 + CTR_N * 4 + 64 +
                     (size_t)QCAP * sizeof(TaskDesc) + (MAXK + 1) * 8 + 4096;
         CK(cudaMallocHost(&g_ws.host, hb));
         char* h = g_ws.host;
@@ -212,7 +212,7 @@ static int ensure_ws(u64 n, int esize) {
         g_ws.h_order = (u32*)h;
         h += MAXS * 4;
         g_ws.h_ctr = (u32*)h;
-        h += CTR_N * 4;
+        h += CTR_N * 4 + 64;
         g_ws.h_q = (TaskDesc*)h;
         h += (size_t)QCAP * sizeof(TaskDesc);
         g_ws.h_bnd = (u64*)h;
@@ -303,6 +303,7 @@ static LevelArgs level_args(void* data, u32 T, u32 S, int emit, u64 seed) {
     A.q_cap = QCAP;
     A.ctr = g_ws.ctr;
     A.spill_ctr = g_ws.spill_ctr;
+    A.base_elems = g_ws.spill_ctr + 1;
     A.base_cap = TR::CAP;
     A.emit = emit;
     A.seed = seed;
@@ -371,7 +372,7 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
     CK(cudaMemcpyAsync(g_ws.tp, g_ws.h_tp, T * sizeof(TaskParam), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(g_ws.sd, g_ws.h_sd, S * sizeof(StripeDesc), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(g_ws.order, g_ws.h_order, S * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(g_ws.ctr, 0, CTR_N * 4 + 8, st));
+    CK(cudaMemsetAsync(g_ws.ctr, 0, CTR_N * 4 + 16, st));
     LevelArgs A = level_args<TR>(data, T, S, emit, seed);
     if (from_splitters) {
         LAUNCH(KK_SAMPLE, (k_tree_from_splitters<<<1, 256, 0, st>>>(A, g_ws.dsplit, nspl, eq)));
@@ -385,7 +386,7 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
     LAUNCH(KK_MOVES, (k_moves<TR><<<dim3(gx, T), 256, 0, st>>>(A)));
     LAUNCH(KK_PERMUTE, (k_permute<TR><<<g_ws.k3_blocks, K3_THREADS, 0, st>>>(A)));
     LAUNCH(KK_CLEANUP, (k_cleanup<TR><<<T * MAXK, K4_THREADS, 0, st>>>(A)));
-    CK(cudaMemcpyAsync(g_ws.h_ctr, g_ws.ctr, CTR_N * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(g_ws.h_ctr, g_ws.ctr, CTR_N * 4 + 16, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     g_stats.host_syncs++;
     if (g_ws.h_ctr[CTR_ERROR]) {
@@ -394,6 +395,11 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
         return IPS4O_EINTERNAL;
     }
     g_stats.equality_tasks += g_ws.h_ctr[CTR_EQ];
+    {
+        u64 be;
+        memcpy(&be, (const char*)g_ws.h_ctr + CTR_N * 4 + 8, 8);
+        g_stats.base_elements += be;
+    }
     return IPS4O_OK;
 }
 
@@ -413,8 +419,9 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
     if (rc) return rc;
     rc = prepare_kernels<TR>();
     if (rc) return rc;
-    g_stats.aux_bytes = g_ws.dev_bytes;
+    g_stats.aux_bytes = fixed_bytes() + align_up(spill_bound_elems(n, TR::S) * TR::S, 256);
     if (n <= (u64)TR::CAP) {
+        g_stats.base_elements += n;
         g_ws.h_q[0] = TaskDesc{0, n};
         CK(cudaMemcpyAsync(g_ws.q_base, g_ws.h_q, sizeof(TaskDesc), cudaMemcpyHostToDevice, st));
         return run_base<TR>(data, 1, g_ws.q_base, st);
@@ -450,6 +457,7 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
             rc = run_level<TR>(data, T, S, st, false, 0, 0, 1, seed);
             if (rc) return rc;
             g_stats.distribution_tasks += T;
+            for (u32 q = 0; q < T; ++q) g_stats.distributed_elements += cur[i0 + q].hi - cur[i0 + q].lo;
             const u32 nb = g_ws.h_ctr[CTR_BASE], nn = g_ws.h_ctr[CTR_NEXT];
             rc = run_base<TR>(data, nb, g_ws.q_base, st);
             if (rc) return rc;

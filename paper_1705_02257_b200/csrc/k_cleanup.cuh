@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
         const bool eqb = tp.eq && (b & 1u);
         if (sz > 1 && !eqb) {
             if (sz <= A.base_cap) {
+                atomicAdd((unsigned long long*)A.base_elems, (unsigned long long)sz);
                 u32 i = atomicAdd(&A.ctr[CTR_BASE], 1u);
                 if (i < A.q_cap) A.q_base[i] = TaskDesc{e0, e1};
                 else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
