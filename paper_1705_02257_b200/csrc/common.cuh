@@ -12,7 +12,6 @@ typedef unsigned int u32;
 constexpr int MAXK = 256;            // buckets per step: k = 256, or 2k'-1 <= 255 with eq
 constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer
 constexpr u32 INV_BUCKET = 0xFFFFu;  // "no element" marker in classification registers
-constexpr int K2_THREADS = 512;      // local classification CTA
 constexpr int K3_THREADS = 256;      // block permutation CTA (one chain per warp)
 constexpr int K4_THREADS = 256;      // cleanup CTA
 constexpr int BLOCK_BYTES = 512;     // block b*s in bytes for the 8/16-byte types
@@ -24,7 +23,7 @@ constexpr int BLOCK_BYTES = 512;     // block b*s in bytes for the 8/16-byte typ
 
 struct TU64 {
     typedef u64 V;
-    static constexpr int S = 8, B = 64, VEC = 2, E2 = 8, CAP = 16384, TYPE = 0;
+    static constexpr int S = 8, B = 64, VEC = 2, CAP = 16384, TYPE = 0;
     __device__ __forceinline__ static u64 key(V v) { return v; }
     __device__ __forceinline__ static bool less(V a, V b) { return a < b; }
     __host__ __device__ __forceinline__ static V pad() { return ~0ull; }
@@ -34,7 +33,7 @@ struct TU64 {
 // non-negatives -> unsigned order equals '<' (PAPER.md:452 uses 64-bit floats).
 struct TF64 {
     typedef u64 V;
-    static constexpr int S = 8, B = 64, VEC = 2, E2 = 8, CAP = 16384, TYPE = 1;
+    static constexpr int S = 8, B = 64, VEC = 2, CAP = 16384, TYPE = 1;
     __host__ __device__ __forceinline__ static u64 key(V v) {
         return (v >> 63) ? ~v : (v | 0x8000000000000000ull);
     }
@@ -44,7 +43,7 @@ struct TF64 {
 
 struct TPair {
     typedef ulonglong2 V;
-    static constexpr int S = 16, B = 32, VEC = 1, E2 = 4, CAP = 8192, TYPE = 2;
+    static constexpr int S = 16, B = 32, VEC = 1, CAP = 8192, TYPE = 2;
     __device__ __forceinline__ static u64 key(V v) { return v.x; }
     __device__ __forceinline__ static bool less(V a, V b) {
         return a.x < b.x || (a.x == b.x && a.y < b.y);
@@ -80,13 +79,17 @@ struct StripeDesc {
 enum {
     CTR_STRIPE = 0,   // K2 stripe ticket
     CTR_NEXT = 1,     // next-level task queue length
-    CTR_BASE = 2,     // base-case task queue length
-    CTR_TICKET = 3,   // cleanup ticket
-    CTR_ERROR = 4,    // error bits
-    CTR_NEXT_OVF = 5, // next-level queue overflow count
-    CTR_EQ = 6,       // tasks partitioned with equality buckets
-    CTR_N = 8
+    CTR_TICKET = 2,   // cleanup ticket
+    CTR_ERROR = 3,    // error bits
+    CTR_EQ = 4,       // tasks partitioned with equality buckets
+    CTR_BASE0 = 8,    // base-case queue lengths, one per size class (4)
+    CTR_N = 16
 };
+constexpr int NUM_BASE_CLASSES = 4;
+// base-case size classes: <= 2048, <= 4096, <= 8192, <= 16384 elements
+__host__ __device__ __forceinline__ u32 base_class(u64 n) {
+    return n <= 2048 ? 0u : n <= 4096 ? 1u : n <= 8192 ? 2u : 3u;
+}
 enum { ERR_SPILL = 1, ERR_CONSERVE = 2, ERR_QUEUE = 4, ERR_CAPACITY = 8 };
 
 struct LevelArgs {
@@ -114,6 +117,7 @@ struct LevelArgs {
     u64* wr;          // [T][256] packed (w:32 | r+RBIAS:32) block pointers
     u32* readers;     // [T][256]
     u32* done;        // [T][8]   bucket has no unprocessed block left
+    u32* tdone;       // [T/32]   task has no unprocessed block left
     u32* cflag;       // [T][256] cleanup: overhang saved
     void* ovf;        // [T][B]   overflow blocks
     int* ovf_owner;   // [T]

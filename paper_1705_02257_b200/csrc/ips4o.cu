@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -68,7 +69,7 @@ struct Workspace {
     u32 *s_count, *s_fill, *s_spoff, *s_nfull, *prefF, *prefE;
     u64* s_spbase;
     u64* bnd;
-    u32 *dblk, *nfb, *mov, *readers, *done, *cflag;
+    u32 *dblk, *nfb, *mov, *readers, *done, *cflag, *tdone;
     u64* wr;
     void* ovf;
     int* ovf_owner;
@@ -84,6 +85,7 @@ struct Workspace {
     u32* h_ctr;
     TaskDesc* h_q;
     u64* h_bnd;
+    u32* h_tdone;
     u32 k2_blocks = 0, k3_blocks = 0;
     int k2_type = -1;
 };
@@ -114,10 +116,11 @@ static size_t fixed_bytes() {
     add((size_t)MAXT * (MAXK + 1) * 4 * 2);    // dblk, mov
     add((size_t)MAXT * MAXK * 4 * 3);          // nfb, readers, cflag
     add((size_t)MAXT * (MAXK / 32) * 4);       // done
+    add(MAXT / 32 * 4);                        // tdone
     add((size_t)MAXT * MAXK * 8);              // wr
     add((size_t)MAXT * BLOCK_BYTES);           // ovf
     add(MAXT * 4);                             // ovf_owner
-    add((size_t)QCAP * sizeof(TaskDesc) * 2);  // queues
+    add((size_t)QCAP * sizeof(TaskDesc) * (1 + NUM_BASE_CLASSES));  // queues
     add(CTR_N * 4 + 16);                       // ctr + spill ctr + base-element ctr
     add(MAXK * 8);                             // debug splitters
     return s;
@@ -187,10 +190,11 @@ static int ensure_ws(u64 n, int esize) {
     g_ws.readers = g_ws.nfb + (size_t)MAXT * MAXK;
     g_ws.cflag = g_ws.readers + (size_t)MAXT * MAXK;
     g_ws.done = (u32*)take((size_t)MAXT * (MAXK / 32) * 4);
+    g_ws.tdone = (u32*)take(MAXT / 32 * 4);
     g_ws.wr = (u64*)take((size_t)MAXT * MAXK * 8);
     g_ws.ovf = take((size_t)MAXT * BLOCK_BYTES);
     g_ws.ovf_owner = (int*)take(MAXT * 4);
-    char* q = take((size_t)QCAP * sizeof(TaskDesc) * 2);
+    char* q = take((size_t)QCAP * sizeof(TaskDesc) * (1 + NUM_BASE_CLASSES));
     g_ws.q_next = (TaskDesc*)q;
     g_ws.q_base = g_ws.q_next + QCAP;
     char* c = take(CTR_N * 4 + 16);
@@ -202,7 +206,7 @@ static int ensure_ws(u64 n, int esize) {
     g_ws.spill_elem_size = esize;
     if (!g_ws.host) {
         size_t hb = MAXT * sizeof(TaskParam) + MAXS * sizeof(StripeDesc) + MAXS * 4 + CTR_N * 4 + 64 +
-                    (size_t)QCAP * sizeof(TaskDesc) + (MAXK + 1) * 8 + 4096;
+                    (size_t)QCAP * sizeof(TaskDesc) + (MAXK + 1) * 8 + MAXT / 32 * 4 + 4096;
         CK(cudaMallocHost(&g_ws.host, hb));
         char* h = g_ws.host;
         g_ws.h_tp = (TaskParam*)h;
@@ -216,6 +220,8 @@ static int ensure_ws(u64 n, int esize) {
         g_ws.h_q = (TaskDesc*)h;
         h += (size_t)QCAP * sizeof(TaskDesc);
         g_ws.h_bnd = (u64*)h;
+        h += (MAXK + 1) * 8;
+        g_ws.h_tdone = (u32*)h;
     }
     return IPS4O_OK;
 }
@@ -246,16 +252,51 @@ static int launch(int kind, cudaStream_t st, F&& f) {
         if (rc_) return rc_;                                      \
     } while (0)
 
+template <class TR, int TH>
+static cudaError_t set_base_attr1() {
+    return cudaFuncSetAttribute(k_base_merge<TR, TH, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)BaseClass<TR, TH, 16>::smem);
+}
+template <class TR>
+static cudaError_t set_base_attrs() {
+    cudaError_t e = set_base_attr1<TR, 128>();
+    if (e == cudaSuccess) e = set_base_attr1<TR, 256>();
+    if (e == cudaSuccess) e = set_base_attr1<TR, 512>();
+    if (e == cudaSuccess && TR::CAP >= 16384) e = set_base_attr1<TR, (TR::CAP >= 16384 ? 1024 : 512)>();
+    return e;
+}
+
+// K2 configurations: (threads, elements per thread).  IPS4O_K2_VARIANT=1 selects the
+// 1024-thread configuration (tuning experiments); the default is variant 0.
+template <class TR> struct K2Cfg0 { static constexpr int NT = 512, E = 16 / TR::S * 4; };
+template <class TR> struct K2Cfg1 { static constexpr int NT = 1024, E = 16 / TR::S * 2; };
+static int k2_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("IPS4O_K2_VARIANT");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v;
+}
+template <class TR, class C>
+static cudaError_t k2_setup(int* occ) {
+    cudaError_t e = cudaFuncSetAttribute(k_classify<TR, C::NT, C::E>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)K2Smem<TR, C::NT>::total);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_classify<TR, C::NT, C::E>, C::NT,
+                                                         K2Smem<TR, C::NT>::total);
+}
+
 template <class TR>
 static int prepare_kernels(void) {
     if (g_ws.k2_type == TR::TYPE) return IPS4O_OK;
-    CK(cudaFuncSetAttribute(k_classify<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)K2Smem<TR>::total));
-    CK(cudaFuncSetAttribute(k_basecase<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(TR::CAP * sizeof(typename TR::V))));
+    CK(set_base_attrs<TR>());
+    CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            K1_SAMPLE_BIG * 8));
     int occ2 = 0, occ3 = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_classify<TR>, K2_THREADS,
-                                                     K2Smem<TR>::total));
+    if (k2_variant() == 1) CK((k2_setup<TR, K2Cfg1<TR>>(&occ2)));
+    else CK((k2_setup<TR, K2Cfg0<TR>>(&occ2)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_permute<TR>, K3_THREADS, 0));
     if (occ2 < 1 || occ3 < 1) {
         snprintf(g_errbuf, sizeof g_errbuf, "occupancy query returned %d/%d", occ2, occ3);
@@ -295,6 +336,7 @@ static LevelArgs level_args(void* data, u32 T, u32 S, int emit, u64 seed) {
     A.wr = g_ws.wr;
     A.readers = g_ws.readers;
     A.done = g_ws.done;
+    A.tdone = g_ws.tdone;
     A.cflag = g_ws.cflag;
     A.ovf = g_ws.ovf;
     A.ovf_owner = g_ws.ovf_owner;
@@ -377,13 +419,34 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
     if (from_splitters) {
         LAUNCH(KK_SAMPLE, (k_tree_from_splitters<<<1, 256, 0, st>>>(A, g_ws.dsplit, nspl, eq)));
     } else {
-        LAUNCH(KK_SAMPLE, (k_sample<TR><<<T, K1_THREADS, 0, st>>>(A)));
+        u64 maxn = 0;
+        for (u32 i = 0; i < T; ++i) maxn = std::max<u64>(maxn, g_ws.h_tp[i].hi - g_ws.h_tp[i].lo);
+        if (maxn >= K1_BIG_TASK)
+            LAUNCH(KK_SAMPLE, (k_sample<TR, K1_SAMPLE_BIG><<<T, K1_THREADS, K1_SAMPLE_BIG * 8, st>>>(A)));
+        else
+            LAUNCH(KK_SAMPLE, (k_sample<TR, K1_SAMPLE><<<T, K1_THREADS, K1_SAMPLE * 8, st>>>(A)));
     }
     const u32 g2 = std::min<u32>(S, g_ws.k2_blocks);
-    LAUNCH(KK_CLASSIFY, (k_classify<TR><<<g2, K2_THREADS, K2Smem<TR>::total, st>>>(A)));
+    if (k2_variant() == 1) {
+        typedef K2Cfg1<TR> C;
+        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E><<<g2, C::NT, K2Smem<TR, C::NT>::total, st>>>(A)));
+    } else {
+        typedef K2Cfg0<TR> C;
+        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E><<<g2, C::NT, K2Smem<TR, C::NT>::total, st>>>(A)));
+    }
     LAUNCH(KK_PREPARE, (k_prepare<TR><<<T, MAXK, 0, st>>>(A)));
     const u32 gx = std::max<u32>(1, (2 * g_ws.num_sms + T - 1) / T);
     LAUNCH(KK_MOVES, (k_moves<TR><<<dim3(gx, T), 256, 0, st>>>(A)));
+    {
+        u32 tw[MAXT / 32];
+        const u32 nwd = (T + 31) / 32;
+        for (u32 i = 0; i < nwd; ++i) {
+            const u32 lo = i * 32;
+            tw[i] = (T >= lo + 32) ? 0u : ~((1u << (T - lo)) - 1u);  // bits of absent tasks set
+        }
+        memcpy(g_ws.h_tdone, tw, nwd * 4);
+        CK(cudaMemcpyAsync(g_ws.tdone, g_ws.h_tdone, nwd * 4, cudaMemcpyHostToDevice, st));
+    }
     LAUNCH(KK_PERMUTE, (k_permute<TR><<<g_ws.k3_blocks, K3_THREADS, 0, st>>>(A)));
     LAUNCH(KK_CLEANUP, (k_cleanup<TR><<<T * MAXK, K4_THREADS, 0, st>>>(A)));
     CK(cudaMemcpyAsync(g_ws.h_ctr, g_ws.ctr, CTR_N * 4 + 16, cudaMemcpyDeviceToHost, st));
@@ -403,14 +466,30 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
     return IPS4O_OK;
 }
 
-template <class TR>
-static int run_base(void* data, u32 count, TaskDesc* d_tasks, cudaStream_t st) {
+template <class TR, int TH>
+static int run_base_class(void* data, u32 count, TaskDesc* d_tasks, cudaStream_t st) {
     if (!count) return IPS4O_OK;
-    const u32 grid = std::min<u32>(count, 8u * g_ws.num_sms);
-    const size_t smem = TR::CAP * sizeof(typename TR::V);
-    LAUNCH(KK_BASE, (k_basecase<TR><<<grid, K5_THREADS, smem, st>>>(d_tasks, count, data)));
+    typedef BaseClass<TR, TH, 16> BC;
+    const u32 grid = std::min<u32>(count, 16u * g_ws.num_sms);
+    LAUNCH(KK_BASE, (k_base_merge<TR, TH, 16><<<grid, TH, BC::smem, st>>>(d_tasks, count, data)));
     g_stats.base_tasks += count;
     return IPS4O_OK;
+}
+
+// counts[c] tasks of size class c at d_queues + c*QCAP
+template <class TR>
+static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStream_t st) {
+    int rc = run_base_class<TR, 128>(data, counts[0], d_queues, st);
+    if (!rc) rc = run_base_class<TR, 256>(data, counts[1], d_queues + QCAP, st);
+    if (!rc) rc = run_base_class<TR, 512>(data, counts[2], d_queues + 2 * QCAP, st);
+    if (!rc && counts[3]) {
+        if (TR::CAP < 16384) {
+            snprintf(g_errbuf, sizeof g_errbuf, "base task above the type's capacity");
+            return IPS4O_EINTERNAL;
+        }
+        rc = run_base_class<TR, (TR::CAP >= 16384 ? 1024 : 512)>(data, counts[3], d_queues + 3 * QCAP, st);
+    }
+    return rc;
 }
 
 template <class TR>
@@ -422,9 +501,13 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
     g_stats.aux_bytes = fixed_bytes() + align_up(spill_bound_elems(n, TR::S) * TR::S, 256);
     if (n <= (u64)TR::CAP) {
         g_stats.base_elements += n;
+        const u32 c = base_class(n);
         g_ws.h_q[0] = TaskDesc{0, n};
-        CK(cudaMemcpyAsync(g_ws.q_base, g_ws.h_q, sizeof(TaskDesc), cudaMemcpyHostToDevice, st));
-        return run_base<TR>(data, 1, g_ws.q_base, st);
+        CK(cudaMemcpyAsync(g_ws.q_base + (size_t)c * QCAP, g_ws.h_q, sizeof(TaskDesc),
+                           cudaMemcpyHostToDevice, st));
+        u32 counts[NUM_BASE_CLASSES] = {0, 0, 0, 0};
+        counts[c] = 1;
+        return run_base<TR>(data, counts, g_ws.q_base, st);
     }
     std::vector<TaskDesc> cur(1, TaskDesc{0, n}), next;
     u64 seed = 0x1234567ull;
@@ -458,8 +541,8 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
             if (rc) return rc;
             g_stats.distribution_tasks += T;
             for (u32 q = 0; q < T; ++q) g_stats.distributed_elements += cur[i0 + q].hi - cur[i0 + q].lo;
-            const u32 nb = g_ws.h_ctr[CTR_BASE], nn = g_ws.h_ctr[CTR_NEXT];
-            rc = run_base<TR>(data, nb, g_ws.q_base, st);
+            const u32 nn = g_ws.h_ctr[CTR_NEXT];
+            rc = run_base<TR>(data, g_ws.h_ctr + CTR_BASE0, g_ws.q_base, st);
             if (rc) return rc;
             if (nn) {
                 CK(cudaMemcpyAsync(g_ws.h_q, g_ws.q_next, nn * sizeof(TaskDesc), cudaMemcpyDeviceToHost, st));

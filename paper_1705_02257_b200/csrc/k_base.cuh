@@ -1,49 +1,125 @@
-// k_base.cuh -- K5: base-case sort of small subproblems in shared memory, and the T1
-// classification debug kernel.
+// k_base.cuh -- K5: base-case sort of small subproblems, and the T1 classification debug kernel.
 //
-// The paper stops the recursion below n0 = 16 elements and uses insertion sort
-// (PAPER.md:403, 416).  On the GPU the leaves are whole shared-memory tiles: a task of at
-// most CAP elements is loaded into shared memory, padded to a power of two with the
-// all-ones element, sorted by a bitonic network, and written back.
+// The paper stops the recursion below n0 = 16 elements and finishes with insertion sort
+// (PAPER.md:403, 416).  On the GPU a leaf is a whole shared-memory tile: one CTA loads a
+// subproblem of at most THREADS*ITEMS elements, pads it with the all-ones element (which
+// is >= every key and, for records, identical to any equal real element, so the first n
+// outputs are exactly the sorted input), and sorts it:
+//   1. every thread sorts ITEMS consecutive elements in registers with a bitonic network
+//      (compile-time indices, no branches: the GPU counterpart of the paper's
+//      branch-free base case);
+//   2. log2(TILE/ITEMS) merge passes: each thread locates its output window in the pair
+//      of runs by a merge-path binary search and merges ITEMS elements serially from
+//      shared memory into registers;
+//   3. coalesced write-back of the first n elements.
+// Shared memory is padded by one element per 16 so that the blocked (thread-contiguous)
+// accesses of 64-bit elements are free of bank conflicts beyond the 2-wavefront minimum.
+// Subproblems are binned by size class (2K/4K/8K/16K elements) by the cleanup kernel so
+// that each launch uses a CTA sized to its tasks.
 #pragma once
 #include "common.cuh"
 
 namespace ips4o {
 
-constexpr int K5_THREADS = 1024;
+__host__ __device__ constexpr u32 padidx(u32 i) { return i + (i >> 4); }
 
 template <class TR>
-__global__ void __launch_bounds__(K5_THREADS) k_basecase(TaskDesc* tasks, u32 ntasks, void* vdata) {
+__device__ __forceinline__ void ce(typename TR::V& a, typename TR::V& b, bool up) {
+    const bool sw = TR::less(b, a) == up;
+    const typename TR::V x = a, y = b;
+    a = sw ? y : x;
+    b = sw ? x : y;
+}
+
+template <class TR, int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS) k_base_merge(const TaskDesc* tasks, u32 ntasks, void* vdata) {
     typedef typename TR::V V;
+    constexpr u32 TILE = THREADS * ITEMS;
     extern __shared__ __align__(16) unsigned char smem5[];
     V* s = reinterpret_cast<V*>(smem5);
     V* data = reinterpret_cast<V*>(vdata);
+    const u32 tid = threadIdx.x;
     for (u32 ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
         const TaskDesc td = tasks[ti];
         const u32 n = (u32)(td.hi - td.lo);
-        u32 P = 1;
-        while (P < n) P <<= 1;
-        for (u32 i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < n ? data[td.lo + i] : TR::pad();
+        V* g = data + td.lo;
+        // coalesced load + padding
+        for (u32 i = tid; i < TILE; i += THREADS) s[padidx(i)] = i < n ? g[i] : TR::pad();
         __syncthreads();
-        for (u32 kk = 2; kk <= P; kk <<= 1) {
-            for (u32 jj = kk >> 1; jj > 0; jj >>= 1) {
-                for (u32 p = threadIdx.x; p < P / 2; p += blockDim.x) {
-                    const u32 i = 2 * p - (p & (jj - 1));
-                    const u32 x = i + jj;
-                    const bool up = (i & kk) == 0;
-                    const V a = s[i], c = s[x];
-                    if (TR::less(c, a) == up) {
-                        s[i] = c;
-                        s[x] = a;
-                    }
+        V v[ITEMS];
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) v[k] = s[padidx(tid * ITEMS + k)];
+        // 1. bitonic network over the thread's ITEMS registers (ascending); threads whose
+        //    items are all padding have nothing to do
+        if (tid * ITEMS < n)
+#pragma unroll
+        for (int kk = 2; kk <= ITEMS; kk <<= 1) {
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const int l = i ^ jj;
+                    if (l > i) ce<TR>(v[i], v[l], (i & kk) == 0);
                 }
-                __syncthreads();
             }
         }
-        for (u32 i = threadIdx.x; i < n; i += blockDim.x) data[td.lo + i] = s[i];
+        // 2. merge passes
+#pragma unroll 1
+        for (u32 w = ITEMS; w < TILE; w <<= 1) {
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) s[padidx(tid * ITEMS + k)] = v[k];
+            __syncthreads();
+            const u32 out0 = tid * ITEMS;
+            const u32 ps = out0 & ~(2 * w - 1);  // start of the run pair
+            const u32 diag = out0 - ps;
+            const u32 A0 = ps, B0 = ps + w;
+            // real (non-padding) elements of the two runs: windows past them output padding
+            const u32 ra = n > A0 ? (n - A0 < w ? n - A0 : w) : 0u;
+            const u32 rb = n > B0 ? (n - B0 < w ? n - B0 : w) : 0u;
+            if (diag >= ra + rb) {
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) v[k] = TR::pad();
+                continue;
+            }
+            // merge path: number of A elements among the first diag outputs
+            u32 lo = diag > w ? diag - w : 0u, hi = diag < w ? diag : w;
+            while (lo < hi) {
+                const u32 mid = (lo + hi) >> 1;
+                if (TR::less(s[padidx(B0 + diag - 1 - mid)], s[padidx(A0 + mid)])) hi = mid;
+                else lo = mid + 1;
+            }
+            u32 ai = A0 + lo, bi = B0 + (diag - lo);
+            const u32 ae = A0 + w, be = B0 + w;
+            V av = s[padidx(ai < ae ? ai : ae - 1)];
+            V bv = s[padidx(bi < be ? bi : be - 1)];
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) {
+                const bool takeA = ai < ae && (bi >= be || !TR::less(bv, av));
+                v[k] = takeA ? av : bv;
+                if (takeA) {
+                    ++ai;
+                    av = s[padidx(ai < ae ? ai : ae - 1)];
+                } else {
+                    ++bi;
+                    bv = s[padidx(bi < be ? bi : be - 1)];
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) s[padidx(tid * ITEMS + k)] = v[k];
+        __syncthreads();
+        for (u32 i = tid; i < n; i += THREADS) g[i] = s[padidx(i)];
         __syncthreads();
     }
 }
+
+template <class TR, int THREADS, int ITEMS>
+struct BaseClass {
+    static constexpr u32 TILE = THREADS * ITEMS;
+    static constexpr size_t smem = (size_t)padidx(TILE) * sizeof(typename TR::V) + 16;
+};
 
 template <class TR>
 __global__ void k_debug_classify(const void* vin, u64 n, const u64* tree_g, const u64* spl_g,

@@ -19,11 +19,11 @@
 
 namespace ips4o {
 
-template <class TR>
+template <class TR, int NT>
 struct K2Smem {
     typedef typename TR::V V;
     static constexpr int B = TR::B;
-    static constexpr int NW = K2_THREADS / 32;
+    static constexpr int NW = NT / 32;
     static constexpr size_t buf_bytes = (size_t)MAXK * B * sizeof(V);
     static constexpr size_t wcnt_bytes = (size_t)NW * MAXK * 2;
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
@@ -31,46 +31,95 @@ struct K2Smem {
     static constexpr size_t total = buf_bytes + wcnt_bytes + tree_bytes + arr_bytes;
 };
 
-template <class TR>
-__device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, u64 tb, u32 len,
-                                        bool final_tile, u64 mb, u32 cap,
-                                        typename TR::V* buf, unsigned short* wcnt,
-                                        const u64* tree, const u64* spl, u32* fill, u32* cnt,
-                                        u32* slotb, u32* nfl, u32* s_nflushed, u32 logk,
-                                        u32 kprime, u32 eq) {
+// Loads one tile (<= 512*E elements from tb, len valid) into registers; bit e of the
+// returned mask is set for valid elements.  128-bit coalesced loads (read-only path:
+// every element is read before anything is written to its address in this kernel).
+template <class TR, int NT, int E>
+__device__ __forceinline__ u32 k2_load(const typename TR::V* __restrict__ data, u64 tb, u32 len,
+                                       typename TR::V (&v)[E]) {
     typedef typename TR::V V;
-    constexpr int B = TR::B, E = TR::E2, VEC = TR::VEC, NV = E / VEC;
-    const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-
-    V v[E];
-    u32 bk[E];
-    u32 pos[E];
-    // 1. load + classify
+    constexpr int VEC = TR::VEC, NV = E / VEC;
+    const u32 tid = threadIdx.x;
+    u32 valid = 0;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-        const u32 e0 = (u32)(i * K2_THREADS + tid) * VEC;
+        const u32 e0 = (u32)(i * NT + tid) * VEC;
         if (e0 + VEC <= len) {
             uint4 x = ld_nc_v4(data + tb + e0);
             V tmp[VEC];
             memcpy(tmp, &x, 16);
 #pragma unroll
             for (int q = 0; q < VEC; ++q) v[i * VEC + q] = tmp[q];
-#pragma unroll
-            for (int q = 0; q < VEC; ++q)
-                bk[i * VEC + q] = classify_key(TR::key(v[i * VEC + q]), tree, spl, logk, kprime, eq);
+            valid |= ((1u << VEC) - 1u) << (i * VEC);
         } else {
 #pragma unroll
             for (int q = 0; q < VEC; ++q) {
                 if (e0 + q < len) {
                     v[i * VEC + q] = data[tb + e0 + q];
-                    bk[i * VEC + q] = classify_key(TR::key(v[i * VEC + q]), tree, spl, logk, kprime, eq);
+                    valid |= 1u << (i * VEC + q);
                 } else {
                     v[i * VEC + q] = TR::pad();
-                    bk[i * VEC + q] = INV_BUCKET;
                 }
             }
         }
     }
+    return valid;
+}
+
+// Branchless descent for all E elements of the thread, level by level so that the E
+// independent shared-memory lookups of a level are in flight together.  LOGK = 8 is the
+// k' = 256 case of the big levels; LOGK = 0 takes the depth at run time.
+template <class TR, int E, int LOGK>
+__device__ __forceinline__ void k2_classify(const typename TR::V (&v)[E], u32 valid,
+                                            const u64* tree, const u64* spl, u32 logk, u32 kprime,
+                                            u32 eq, u32 (&bk)[E]) {
+    u64 key[E];
+    u32 a[E];  // byte offset 8*j of the current tree node
+    const u64 root = tree[1];
+    const char* tb = reinterpret_cast<const char*>(tree);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        key[e] = TR::key(v[e]);
+        a[e] = key[e] >= root ? 24u : 16u;  // level 0 from a register: j = 2 + [root <= e]
+    }
+    if (LOGK == 8) {
+#pragma unroll
+        for (int l = 1; l < 8; ++l)
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                a[e] = (a[e] << 1) + (key[e] >= *reinterpret_cast<const u64*>(tb + a[e]) ? 8u : 0u);
+    } else {
+        for (u32 l = 1; l < logk; ++l)
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                a[e] = (a[e] << 1) + (key[e] >= *reinterpret_cast<const u64*>(tb + a[e]) ? 8u : 0u);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        u32 i = (a[e] >> 3) - kprime;
+        if (eq) {
+            const u32 ii = i ? i : 1u;
+            const u32 isq = (i >= 1u && spl[ii] >= key[e]) ? 1u : 0u;
+            i = 2 * i - isq;
+        }
+        bk[e] = (valid >> e) & 1u ? i : INV_BUCKET;
+    }
+}
+
+template <class TR, int NT, int E, int LOGK>
+__device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const typename TR::V (&v)[E],
+                                        u32 valid, bool final_tile, u64 mb, u32 cap,
+                                        typename TR::V* buf, unsigned short* wcnt,
+                                        const u64* tree, const u64* spl, u32* fill, u32* cnt,
+                                        u32* slotb, u32* nfl, u32* s_nflushed, u32 logk,
+                                        u32 kprime, u32 eq) {
+    typedef typename TR::V V;
+    constexpr int B = TR::B;
+    const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    u32 bk[E];
+    u32 pos[E];
+    // 1. classify
+    k2_classify<TR, E, LOGK>(v, valid, tree, spl, logk, kprime, eq, bk);
     // 2. warp-aggregated ranking
     const u32 lt = lanemask_lt();
 #pragma unroll
@@ -94,7 +143,7 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, u64 t
         const u32 f = fill[b];
         u32 run = f;
 #pragma unroll
-        for (int ww = 0; ww < K2_THREADS / 32; ++ww) {
+        for (int ww = 0; ww < NT / 32; ++ww) {
             u32 c = wcnt[ww * MAXK + b];
             wcnt[ww * MAXK + b] = (unsigned short)run;
             run += c;
@@ -152,17 +201,17 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, u64 t
         if (defer & (1u << j)) buf[bk[j] * B + pos[j]] = v[j];
     if (tid < (u32)MAXK) {
 #pragma unroll
-        for (int ww = 0; ww < K2_THREADS / 32; ++ww) wcnt[ww * MAXK + tid] = 0;
+        for (int ww = 0; ww < NT / 32; ++ww) wcnt[ww * MAXK + tid] = 0;
     }
     __syncthreads();
 }
 
-template <class TR>
-__global__ void __launch_bounds__(K2_THREADS, 1) k_classify(LevelArgs A) {
+template <class TR, int NT, int E>
+__global__ void __launch_bounds__(NT, 1) k_classify(LevelArgs A) {
     typedef typename TR::V V;
-    typedef K2Smem<TR> SM;
-    constexpr int B = TR::B, E = TR::E2;
-    constexpr u32 TILE = K2_THREADS * E;
+    typedef K2Smem<TR, NT> SM;
+    constexpr int B = TR::B;
+    constexpr u32 TILE = NT * E;
     extern __shared__ __align__(128) unsigned char smem[];
     V* buf = reinterpret_cast<V*>(smem);
     unsigned short* wcnt = reinterpret_cast<unsigned short*>(smem + SM::buf_bytes);
@@ -172,7 +221,7 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k_classify(LevelArgs A) {
     u32* cnt = fill + MAXK;
     u32* slotb = cnt + MAXK;
     u32* nfl = slotb + MAXK;
-    __shared__ u32 s_stripe, s_nflushed, s_wsum[K2_THREADS / 32];
+    __shared__ u32 s_stripe, s_nflushed, s_wsum[NT / 32];
     __shared__ u64 s_spbase;
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     V* data = reinterpret_cast<V*>(A.data);
@@ -193,24 +242,40 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k_classify(LevelArgs A) {
             fill[tid] = 0;
             cnt[tid] = 0;
 #pragma unroll
-            for (int ww = 0; ww < K2_THREADS / 32; ++ww) wcnt[ww * MAXK + tid] = 0;
+            for (int ww = 0; ww < NT / 32; ++ww) wcnt[ww * MAXK + tid] = 0;
         }
         if (tid == 0) s_nflushed = 0;
         __syncthreads();
         const u64 mb = sd.begin > tp.g ? sd.begin : tp.g;  // stripe main region start (block aligned)
         const u64 me = sd.end;
         const u32 cap = me > mb ? (u32)((me - mb) / B) : 0u;
-        for (u64 tb = mb; tb < me; tb += TILE) {
-            const u32 len = (u32)((me - tb) < TILE ? (me - tb) : TILE);
-            k2_tile<TR>(data, tb, len, false, mb, cap, buf, wcnt, tree, spl, fill, cnt, slotb, nfl,
-                        &s_nflushed, tp.logk, tp.kprime, tp.eq);
+        if (mb < me) {
+            V cur[E], nxt[E];
+            u32 vcur = k2_load<TR, NT, E>(data, mb, (u32)((me - mb) < TILE ? (me - mb) : TILE), cur);
+            for (u64 tb = mb; tb < me; tb += TILE) {
+                // prefetch the next tile into registers while this one is processed
+                const u64 tn = tb + TILE;
+                u32 vnxt = 0;
+                if (tn < me) vnxt = k2_load<TR, NT, E>(data, tn, (u32)((me - tn) < TILE ? (me - tn) : TILE), nxt);
+                if (tp.logk == 8)
+                    k2_tile<TR, NT, E, 8>(data, cur, vcur, false, mb, cap, buf, wcnt, tree, spl, fill, cnt,
+                                   slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
+                else
+                    k2_tile<TR, NT, E, 0>(data, cur, vcur, false, mb, cap, buf, wcnt, tree, spl, fill, cnt,
+                                   slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
+#pragma unroll
+                for (int e = 0; e < E; ++e) cur[e] = nxt[e];
+                vcur = vnxt;
+            }
         }
         if (sd.first && tp.lo < tp.g) {
             // head elements [lo, g) of the task, processed last so that every write stays
             // behind the read frontier (their block grid starts at g)
             const u64 hend = tp.g < tp.hi ? tp.g : tp.hi;
-            k2_tile<TR>(data, tp.lo, (u32)(hend - tp.lo), true, mb, cap, buf, wcnt, tree, spl,
-                        fill, cnt, slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
+            V hv[E];
+            const u32 hval = k2_load<TR, NT, E>(data, tp.lo, (u32)(hend - tp.lo), hv);
+            k2_tile<TR, NT, E, 0>(data, hv, hval, true, mb, cap, buf, wcnt, tree, spl, fill, cnt, slotb, nfl,
+                           &s_nflushed, tp.logk, tp.kprime, tp.eq);
         }
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area
         u32 f = tid < (u32)MAXK ? fill[tid] : 0u;
@@ -244,7 +309,7 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k_classify(LevelArgs A) {
         __syncthreads();
         if (s_spbase + total <= A.spill_cap) {
             V* sp = reinterpret_cast<V*>(A.spill) + s_spbase;
-            for (u32 b = w; b < (u32)MAXK; b += K2_THREADS / 32) {
+            for (u32 b = w; b < (u32)MAXK; b += NT / 32) {
                 const u32 fb = fill[b], ob = slotb[b];
                 for (u32 j = lane; j < fb; j += 32) sp[ob + j] = buf[b * B + j];
             }

@@ -129,8 +129,9 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
         if (sz > 1 && !eqb) {
             if (sz <= A.base_cap) {
                 atomicAdd((unsigned long long*)A.base_elems, (unsigned long long)sz);
-                u32 i = atomicAdd(&A.ctr[CTR_BASE], 1u);
-                if (i < A.q_cap) A.q_base[i] = TaskDesc{e0, e1};
+                const u32 c = base_class(sz);
+                u32 i = atomicAdd(&A.ctr[CTR_BASE0 + c], 1u);
+                if (i < A.q_cap) A.q_base[(u64)c * A.q_cap + i] = TaskDesc{e0, e1};
                 else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
             } else {
                 u32 i = atomicAdd(&A.ctr[CTR_NEXT], 1u);

@@ -164,25 +164,16 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
 // ------------------------------------------------------------------ permutation
 
 template <class TR>
-__device__ __forceinline__ u32 block_dest(const uint4& first_lane0, u32 t, const LevelArgs& A,
-                                          const TaskParam& tp) {
+__device__ __forceinline__ u32 block_dest(const uint4& first_lane0, const u64* tree, const u64* spl,
+                                          u32 logk, u32 kprime, u32 eq) {
     typename TR::V v;
     memcpy(&v, &first_lane0, sizeof(v) < 16 ? sizeof(v) : 16);
-    const u64 k = TR::key(v);
-    const u64* tree = A.tree + (u64)t * MAXK;
-    const u64* spl = A.spl + (u64)t * MAXK;
-    u32 j = 1;
-    for (u32 l = 0; l < tp.logk; ++l) j = 2 * j + (k >= __ldg(tree + j) ? 1u : 0u);
-    const u32 i = j - tp.kprime;
-    if (tp.eq) {
-        const u32 isq = (i >= 1u && __ldg(spl + i) >= k) ? 1u : 0u;
-        return 2 * i - isq;
-    }
-    return i;
+    return classify_key(TR::key(v), tree, spl, logk, kprime, eq);
 }
 
-// next bucket (cyclic, starting at gb inclusive) whose "done" bit is clear; ~0u if none.
-__device__ __forceinline__ u32 next_open_bucket(const u32* done, u32 nwords, u32 gb, u32 lane) {
+// next bucket (cyclic over nwords*32 buckets, starting at gb inclusive) whose bit in
+// `bits` is clear; ~0u if none.  Warp-cooperative: 32 words per probe.
+__device__ __forceinline__ u32 next_clear_bit(const u32* bits, u32 nwords, u32 gb, u32 lane) {
     const u32 w0 = gb >> 5;
     for (u32 base = 0; base <= nwords; base += 32) {
         const u32 off = base + lane;
@@ -190,10 +181,9 @@ __device__ __forceinline__ u32 next_open_bucket(const u32* done, u32 nwords, u32
         u32 widx = 0;
         if (off <= nwords) {
             widx = (w0 + off) % nwords;
-            word = *(volatile const u32*)(done + widx);
-            if (off == 0) word |= (1u << (gb & 31)) - 1u;             // first pass: bits >= gb
-            if (off == nwords) word |= ~((1u << (gb & 31)) - 1u);     // wrap: bits < gb
-            if (off == nwords && (gb & 31) == 0) word = 0xFFFFFFFFu;
+            word = *(volatile const u32*)(bits + widx);
+            if (off == 0) word |= (1u << (gb & 31)) - 1u;          // first pass: bits >= gb
+            if (off == nwords) word |= ~((1u << (gb & 31)) - 1u);  // wrap-around: bits < gb
         }
         const u32 bal = __ballot_sync(0xffffffffu, word != 0xFFFFFFFFu);
         if (bal) {
@@ -206,86 +196,111 @@ __device__ __forceinline__ u32 next_open_bucket(const u32* done, u32 nwords, u32
     return 0xFFFFFFFFu;
 }
 
+// Block permutation.  Each CTA works on one task at a time (its classifier in shared
+// memory), starting from a task chosen by its index so that CTAs spread over the tasks;
+// when the task has no unprocessed block left it moves to the next unfinished task.
 template <class TR>
 __global__ void __launch_bounds__(K3_THREADS) k_permute(LevelArgs A) {
     constexpr int B = TR::B;
     constexpr u32 BB = B * TR::S;  // block bytes (512)
-    const u32 lane = threadIdx.x & 31;
-    const u32 nchains = gridDim.x * (blockDim.x >> 5);
-    const u32 chain = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const u32 TB = A.ntasks * MAXK;
-    const u32 nwords = TB / 32;
-    u32 gb = (u32)((u64)chain * TB / nchains);
+    __shared__ u64 s_tree[MAXK], s_spl[MAXK];
+    const u32 tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
+    const u32 nw = blockDim.x >> 5;
+    const u32 T = A.ntasks;
     char* const data = reinterpret_cast<char*>(A.data);
+    u32 t = (u32)((u64)blockIdx.x * T / gridDim.x);
+    const u32 tnwords = (T + 31) / 32;
 
     for (;;) {
-        // ---- take an unprocessed block from the primary bucket (r <- r-1)
-        gb = next_open_bucket(A.done, nwords, gb, lane);
-        if (gb == 0xFFFFFFFFu) return;
-        u32 t = gb / MAXK;
-        int blk = 0;
-        int ok = 0;
-        if (lane == 0) {
-            atomicAdd(&A.readers[gb], 1u);
-            __threadfence();
-            const u64 old = atomicAdd((unsigned long long*)&A.wr[gb], ~0ull);  // r -= 1
-            const int ow = (int)(u32)(old >> 32);
-            const int orr = (int)((u32)old - RBIAS);
-            if (orr < ow) {
-                atomicSub(&A.readers[gb], 1u);
-                atomicOr(&A.done[gb >> 5], 1u << (gb & 31));
-            } else {
-                ok = 1;
-                blk = orr;
-            }
+        // next unfinished task (cyclic from t); exit when every task is finished
+        if (tid < 32) {
+            const u32 nt = next_clear_bit(A.tdone, tnwords, t, lane);
+            if (lane == 0) s_tree[0] = nt;  // slot 0 of the tree is unused: borrow it
         }
-        ok = __shfl_sync(0xffffffffu, ok, 0);
-        if (!ok) continue;
-        blk = __shfl_sync(0xffffffffu, blk, 0);
+        __syncthreads();
+        const u32 nt = (u32)s_tree[0];
+        __syncthreads();
+        if (nt == 0xFFFFFFFFu || nt >= T) return;
+        t = nt;
+        if (tid < (u32)MAXK) {
+            s_tree[tid] = A.tree[(u64)t * MAXK + tid];
+            s_spl[tid] = A.spl[(u64)t * MAXK + tid];
+        }
+        __syncthreads();
         const TaskParam tp = A.tp[t];
+        const u32* done = A.done + (u64)t * (MAXK / 32);
         char* tbase = data + tp.g * TR::S;
-        uint4 cur = ld_v4(tbase + (u64)blk * BB + lane * 16);
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicSub(&A.readers[gb], 1u);
-        // ---- chain: place the block, swapping with unprocessed blocks on the way
+        // primary buckets spread over the task's buckets
+        u32 b = (u32)(((u64)blockIdx.x * nw + wi) * 97u % tp.K);
+
         for (;;) {
-            u32 dest = 0;
-            if (lane == 0) dest = block_dest<TR>(cur, t, A, tp);
-            dest = __shfl_sync(0xffffffffu, dest, 0);
-            const u32 gbd = t * MAXK + dest;
-            u64 old = 0;
-            if (lane == 0) old = atomicAdd((unsigned long long*)&A.wr[gbd], 1ull << 32);  // w += 1
-            old = __shfl_sync(0xffffffffu, old, 0);
-            const int ow = (int)(u32)(old >> 32);
-            const int orr = (int)((u32)old - RBIAS);
-            if (ow <= orr) {
-                // case 1: w_dest points to an unprocessed block -> swap
-                const uint4 oth = ld_v4(tbase + (u64)ow * BB + lane * 16);
-                u32 od = 0;
-                if (lane == 0) od = block_dest<TR>(oth, t, A, tp);
-                od = __shfl_sync(0xffffffffu, od, 0);
-                if (od == dest) continue;  // already in place: skip it
-                st_v4(tbase + (u64)ow * BB + lane * 16, cur);
-                cur = oth;
-            } else {
-                // case 2: w_dest points to an empty block -> wait for readers, write, refill
-                if (lane == 0) {
-                    while (*(volatile u32*)&A.readers[gbd] != 0u) __nanosleep(64);
-                    __threadfence();
-                }
-                __syncwarp();
-                if (tp.g + (u64)(ow + 1) * B > tp.hi) {
-                    // the block would reach past the task end: overflow block
-                    char* ob = reinterpret_cast<char*>(A.ovf) + (u64)t * BB;
-                    st_v4(ob + lane * 16, cur);
-                    if (lane == 0) A.ovf_owner[t] = (int)dest;
+            // ---- take an unprocessed block from the primary bucket (r <- r-1)
+            b = next_clear_bit(done, MAXK / 32, b, lane);
+            if (b == 0xFFFFFFFFu) break;
+            const u32 gb = t * MAXK + b;
+            int blk = 0, ok = 0;
+            if (lane == 0) {
+                atomicAdd(&A.readers[gb], 1u);
+                __threadfence();
+                const u64 old = atomicAdd((unsigned long long*)&A.wr[gb], ~0ull);  // r -= 1
+                const int ow = (int)(u32)(old >> 32);
+                const int orr = (int)((u32)old - RBIAS);
+                if (orr < ow) {
+                    atomicSub(&A.readers[gb], 1u);
+                    atomicOr(&A.done[(u64)t * (MAXK / 32) + (b >> 5)], 1u << (b & 31));
                 } else {
-                    st_v4(tbase + (u64)ow * BB + lane * 16, cur);
+                    ok = 1;
+                    blk = orr;
                 }
-                break;
+            }
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            if (!ok) continue;
+            blk = __shfl_sync(0xffffffffu, blk, 0);
+            uint4 cur = ld_v4(tbase + (u64)blk * BB + lane * 16);
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicSub(&A.readers[gb], 1u);
+            // ---- chain: place the block, swapping with unprocessed blocks on the way
+            for (;;) {
+                u32 dest = 0;
+                if (lane == 0) dest = block_dest<TR>(cur, s_tree, s_spl, tp.logk, tp.kprime, tp.eq);
+                dest = __shfl_sync(0xffffffffu, dest, 0);
+                const u32 gbd = t * MAXK + dest;
+                u64 old = 0;
+                if (lane == 0) old = atomicAdd((unsigned long long*)&A.wr[gbd], 1ull << 32);  // w += 1
+                old = __shfl_sync(0xffffffffu, old, 0);
+                const int ow = (int)(u32)(old >> 32);
+                const int orr = (int)((u32)old - RBIAS);
+                if (ow <= orr) {
+                    // case 1: w_dest points to an unprocessed block -> swap
+                    const uint4 oth = ld_v4(tbase + (u64)ow * BB + lane * 16);
+                    u32 od = 0;
+                    if (lane == 0) od = block_dest<TR>(oth, s_tree, s_spl, tp.logk, tp.kprime, tp.eq);
+                    od = __shfl_sync(0xffffffffu, od, 0);
+                    if (od == dest) continue;  // already in place: skip it
+                    st_v4(tbase + (u64)ow * BB + lane * 16, cur);
+                    cur = oth;
+                } else {
+                    // case 2: w_dest points to an empty block -> wait for readers, write, refill
+                    if (lane == 0) {
+                        while (*(volatile u32*)&A.readers[gbd] != 0u) __nanosleep(64);
+                        __threadfence();
+                    }
+                    __syncwarp();
+                    if (tp.g + (u64)(ow + 1) * B > tp.hi) {
+                        // the block would reach past the task end: overflow block
+                        char* ob = reinterpret_cast<char*>(A.ovf) + (u64)t * BB;
+                        st_v4(ob + lane * 16, cur);
+                        if (lane == 0) A.ovf_owner[t] = (int)dest;
+                    } else {
+                        st_v4(tbase + (u64)ow * BB + lane * 16, cur);
+                    }
+                    break;
+                }
             }
         }
+        __syncthreads();
+        if (tid == 0) atomicOr(&A.tdone[t >> 5], 1u << (t & 31));
     }
 }
 

@@ -12,7 +12,9 @@
 namespace ips4o {
 
 constexpr int K1_THREADS = 1024;
-constexpr int K1_SAMPLE = 2048;  // >= alpha*k - 1 for n < 2^42
+constexpr int K1_SAMPLE = 2048;        // sample capacity for ordinary tasks (static smem)
+constexpr int K1_SAMPLE_BIG = 16384;   // for tasks of >= 2^22 elements (dynamic smem, 128 KB)
+constexpr u64 K1_BIG_TASK = 1ull << 22;
 
 // Builds the padded splitter array spl[1..k'-1] and the BFS tree from nd distinct sorted
 // splitters held in s_dist[0..nd).  k' = next power of two >= nd+1; padding repeats the
@@ -46,10 +48,11 @@ __device__ void build_tree_block(const u64* s_dist, u32 nd, u32 eq, u64* g_tree,
     }
 }
 
-template <class TR>
+template <class TR, int SAMPLE>
 __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
     typedef typename TR::V V;
-    __shared__ u64 keys[K1_SAMPLE];
+    extern __shared__ __align__(16) unsigned char smem1[];
+    u64* keys = reinterpret_cast<u64*>(smem1);
     __shared__ u64 dist[MAXK];
     __shared__ u32 s_flag, s_nd;
     const u32 t = blockIdx.x;
@@ -57,18 +60,23 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
     const u64 lo = tp->lo, hi = tp->hi, n = hi - lo;
     const V* data = reinterpret_cast<const V*>(A.data);
 
-    // k = min(256, max(4, pow2_floor(n/16))) and alpha = max(1, round(0.2 log2 n))
-    u64 q = n / 16;
+    // Bucket count: the last levels use an adaptive k aimed at
+    // base-case tiles of ~4096 elements: k = min(256, max(4, pow2_ceil(n/4096))).
+    // Oversampling: the paper's alpha = 0.2 log n is a CPU-cache choice;
+    // sorting the sample costs the same ~10 us here for any alpha <= 2048/k, so the GPU
+    // takes alpha = max(0.2 log2 n, 2048/k - 1 rounded down), which keeps subproblems
+    // close to their expected size (fewer extra levels).  Any alpha gives the same output.
     u32 k = 4;
-    while ((u64)k * 2 <= q && k < (u32)MAXK) k *= 2;
+    while ((u64)k * 4096 < n && k < (u32)MAXK) k *= 2;
     u32 alpha = (u32)llround(0.2 * log2((double)n));
     if (alpha < 1) alpha = 1;
+    const u32 amax = (SAMPLE - 1) / k;
+    if (alpha < amax) alpha = amax;
     u32 m = alpha * k - 1;
-    if (m > K1_SAMPLE) m = K1_SAMPLE - 1;
+    if (m > SAMPLE - 1) m = SAMPLE - 1;
     if ((u64)m > n) m = (u32)n;
-
     // stratified random sample without replacement: one element per stratum
-    for (u32 j = threadIdx.x; j < (u32)K1_SAMPLE; j += blockDim.x) {
+    for (u32 j = threadIdx.x; j < (u32)SAMPLE; j += blockDim.x) {
         u64 key = ~0ull;
         if (j < m) {
             u64 a = lo + (u64)((unsigned __int128)n * j / m);
@@ -79,10 +87,10 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
         keys[j] = key;
     }
     __syncthreads();
-    // bitonic sort of the 2048 sampled keys in shared memory
-    for (u32 kk = 2; kk <= (u32)K1_SAMPLE; kk <<= 1) {
+    // bitonic sort of the sampled keys in shared memory
+    for (u32 kk = 2; kk <= (u32)SAMPLE; kk <<= 1) {
         for (u32 jj = kk >> 1; jj > 0; jj >>= 1) {
-            for (u32 p = threadIdx.x; p < (u32)K1_SAMPLE / 2; p += blockDim.x) {
+            for (u32 p = threadIdx.x; p < (u32)SAMPLE / 2; p += blockDim.x) {
                 u32 i = 2 * p - (p & (jj - 1));
                 u32 x = i + jj;
                 bool up = (i & kk) == 0;

@@ -32,13 +32,17 @@ def words_i64(t: torch.Tensor) -> torch.Tensor:
     return t.view(torch.int64).reshape(t.shape[0], -1)
 
 
+def _i64(x: int) -> int:
+    return ((x + (1 << 63)) % (1 << 64)) - (1 << 63)
+
+
 def digest(t: torch.Tensor):
     """Order-independent multiset digest: (sum of h(row), sum of h(row)^2) mod 2^64 with a
     row hash built from wrapping int64 arithmetic."""
     w = words_i64(t)
     h = torch.zeros(w.shape[0], dtype=torch.int64, device=t.device)
     for c in range(w.shape[1]):
-        x = w[:, c] + (c + 1) * -7046029254386353131   # + c * golden
+        x = w[:, c] + _i64((c + 1) * 0x9E3779B97F4A7C15)
         x = x ^ (x >> 31)
         x = x * -4658895280553007687
         x = x ^ (x >> 29)
