@@ -14,7 +14,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libips4o.so")
+# IPS4O_LIB may name an alternative build (tuning experiments, e.g. libips4o_bb256.so)
+LIB_PATH = os.environ.get("IPS4O_LIB") or os.path.join(_HERE, "libips4o.so")
 
 IPS4O_U64, IPS4O_F64, IPS4O_PAIR_U64, IPS4O_REC100_K10 = 0, 1, 2, 3
 ELEM_SIZE = {0: 8, 1: 8, 2: 16, 3: 100}

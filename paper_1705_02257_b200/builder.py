@@ -10,6 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libips4o.so")
+# experimental build variants (tuning only): name -> extra nvcc flags
+VARIANTS = {"bb256": ["-DIPS4O_BLOCK_BYTES=256"]}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [
@@ -26,25 +28,35 @@ def sources():
                   [os.path.join(ROOT, "include", "ips4o.h")])
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def lib_path(variant: str | None = None) -> str:
+    return LIB if not variant else os.path.join(HERE, f"libips4o_{variant}.so")
+
+
+def needs_build(variant: str | None = None) -> bool:
+    p = lib_path(variant)
+    if not os.path.exists(p):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(p)
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not needs_build():
-        return LIB
-    cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"),
-           "-o", LIB, os.path.join(CSRC, "ips4o.cu")]
+def build(force: bool = False, verbose: bool = False, extra=(), variant: str | None = None) -> str:
+    out = lib_path(variant)
+    if not force and not needs_build(variant):
+        return out
+    flags = list(extra) + (VARIANTS[variant] if variant else [])
+    cmd = [NVCC, *NVCC_FLAGS, *flags, "-I", os.path.join(ROOT, "include"),
+           "-o", out, os.path.join(CSRC, "ips4o.cu")]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
     v = "-v" in sys.argv
     extra = ["-Xptxas", "-v"] if "--ptxas-v" in sys.argv else []
     print(build(force=True, verbose=v, extra=extra))
+    if "--variants" in sys.argv:
+        for name in VARIANTS:
+            print(build(force=True, verbose=v, extra=extra, variant=name))

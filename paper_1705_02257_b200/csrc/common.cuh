@@ -14,7 +14,10 @@ constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer (SURVEY 
 constexpr u32 INV_BUCKET = 0xFFFFu;  // "no element" marker in classification registers
 constexpr int K3_THREADS = 256;      // block permutation CTA (one chain per warp)
 constexpr int K4_THREADS = 256;      // cleanup CTA
-constexpr int BLOCK_BYTES = 512;     // block b*s in bytes for the 8/16-byte types
+#ifndef IPS4O_BLOCK_BYTES
+#define IPS4O_BLOCK_BYTES 512
+#endif
+constexpr int BLOCK_BYTES = IPS4O_BLOCK_BYTES;  // block b*s in bytes for the 8/16-byte types
 
 // ----------------------------------------------------------------- element traits
 // key(): order-preserving unsigned 64-bit image of the sort key.
@@ -23,7 +26,7 @@ constexpr int BLOCK_BYTES = 512;     // block b*s in bytes for the 8/16-byte typ
 
 struct TU64 {
     typedef u64 V;
-    static constexpr int S = 8, B = 64, VEC = 2, CAP = 16384, TYPE = 0;
+    static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 0;
     __device__ __forceinline__ static u64 key(V v) { return v; }
     __device__ __forceinline__ static bool less(V a, V b) { return a < b; }
     __host__ __device__ __forceinline__ static V pad() { return ~0ull; }
@@ -33,7 +36,7 @@ struct TU64 {
 // non-negatives -> unsigned order equals '<' (PAPER.md:452 uses 64-bit floats).
 struct TF64 {
     typedef u64 V;
-    static constexpr int S = 8, B = 64, VEC = 2, CAP = 16384, TYPE = 1;
+    static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 1;
     __host__ __device__ __forceinline__ static u64 key(V v) {
         return (v >> 63) ? ~v : (v | 0x8000000000000000ull);
     }
@@ -43,7 +46,7 @@ struct TF64 {
 
 struct TPair {
     typedef ulonglong2 V;
-    static constexpr int S = 16, B = 32, VEC = 1, CAP = 8192, TYPE = 2;
+    static constexpr int S = 16, B = BLOCK_BYTES / 16, VEC = 1, CAP = 8192, TYPE = 2;
     __device__ __forceinline__ static u64 key(V v) { return v.x; }
     __device__ __forceinline__ static bool less(V a, V b) {
         return a.x < b.x || (a.x == b.x && a.y < b.y);
@@ -155,6 +158,38 @@ __device__ __forceinline__ uint4 ld_v4(const void* p) {
                  : "memory");
     return r;
 }
+// A block held by one warp: BLOCK_BYTES / 32 bytes per lane (16 B for 512-B blocks, 8 B
+// for 256-B blocks).
+#if IPS4O_BLOCK_BYTES == 512
+typedef uint4 BlockLane;
+__device__ __forceinline__ BlockLane ld_blk(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_blk(void* p, BlockLane v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+#elif IPS4O_BLOCK_BYTES == 256
+typedef uint2 BlockLane;
+__device__ __forceinline__ BlockLane ld_blk(const void* p) {
+    uint2 r;
+    asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_blk(void* p, BlockLane v) {
+    asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+#else
+#error "IPS4O_BLOCK_BYTES must be 256 or 512"
+#endif
+constexpr int LANE_BYTES = BLOCK_BYTES / 32;
+
 __device__ __forceinline__ void st_v4(void* p, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                  "r"(v.w)

@@ -268,8 +268,15 @@ static cudaError_t set_base_attrs() {
 
 // K2 configurations: (threads, elements per thread).  IPS4O_K2_VARIANT=1 selects the
 // 1024-thread configuration (tuning experiments); the default is variant 0.
-template <class TR> struct K2Cfg0 { static constexpr int NT = 512, E = 16 / TR::S * 4; };
-template <class TR> struct K2Cfg1 { static constexpr int NT = 1024, E = 16 / TR::S * 2; };
+#if IPS4O_BLOCK_BYTES == 512
+// 256 buffers of 512 B = 128 KB of shared memory: one CTA per SM
+template <class TR> struct K2Cfg0 { static constexpr int NT = 512, E = 16 / TR::S * 4, MINB = 1; };
+template <class TR> struct K2Cfg1 { static constexpr int NT = 1024, E = 16 / TR::S * 2, MINB = 1; };
+#else
+// 256 buffers of 256 B = 64 KB: two CTAs per SM
+template <class TR> struct K2Cfg0 { static constexpr int NT = 256, E = 16 / TR::S * 4, MINB = 2; };
+template <class TR> struct K2Cfg1 { static constexpr int NT = 512, E = 16 / TR::S * 2, MINB = 2; };
+#endif
 static int k2_variant() {
     static int v = -1;
     if (v < 0) {
@@ -280,11 +287,11 @@ static int k2_variant() {
 }
 template <class TR, class C>
 static cudaError_t k2_setup(int* occ) {
-    cudaError_t e = cudaFuncSetAttribute(k_classify<TR, C::NT, C::E>,
+    cudaError_t e = cudaFuncSetAttribute(k_classify<TR, C::NT, C::E, C::MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)K2Smem<TR, C::NT>::total);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_classify<TR, C::NT, C::E>, C::NT,
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_classify<TR, C::NT, C::E, C::MINB>, C::NT,
                                                          K2Smem<TR, C::NT>::total);
 }
 
@@ -294,6 +301,8 @@ static int prepare_kernels(void) {
     CK(set_base_attrs<TR>());
     CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             K1_SAMPLE_BIG * 8));
+    CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            K1_SAMPLE * 8));
     int occ2 = 0, occ3 = 0;
     if (k2_variant() == 1) CK((k2_setup<TR, K2Cfg1<TR>>(&occ2)));
     else CK((k2_setup<TR, K2Cfg0<TR>>(&occ2)));
@@ -429,10 +438,10 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
     const u32 g2 = std::min<u32>(S, g_ws.k2_blocks);
     if (k2_variant() == 1) {
         typedef K2Cfg1<TR> C;
-        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E><<<g2, C::NT, K2Smem<TR, C::NT>::total, st>>>(A)));
+        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E, C::MINB><<<g2, C::NT, K2Smem<TR, C::NT>::total, st>>>(A)));
     } else {
         typedef K2Cfg0<TR> C;
-        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E><<<g2, C::NT, K2Smem<TR, C::NT>::total, st>>>(A)));
+        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E, C::MINB><<<g2, C::NT, K2Smem<TR, C::NT>::total, st>>>(A)));
     }
     LAUNCH(KK_PREPARE, (k_prepare<TR><<<T, MAXK, 0, st>>>(A)));
     const u32 gx = std::max<u32>(1, (2 * g_ws.num_sms + T - 1) / T);

@@ -42,73 +42,77 @@ __global__ void __launch_bounds__(THREADS) k_base_merge(const TaskDesc* tasks, u
     for (u32 ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
         const TaskDesc td = tasks[ti];
         const u32 n = (u32)(td.hi - td.lo);
+        const u32 n16 = (n + ITEMS - 1) / ITEMS * ITEMS;  // only these positions are touched
         V* g = data + td.lo;
-        // coalesced load + padding
-        for (u32 i = tid; i < TILE; i += THREADS) s[padidx(i)] = i < n ? g[i] : TR::pad();
+        // coalesced load; the last thread's items past n are padding
+        for (u32 i = tid; i < n16; i += THREADS) s[padidx(i)] = i < n ? g[i] : TR::pad();
         __syncthreads();
+        const bool active = tid * ITEMS < n;
         V v[ITEMS];
+        if (active) {
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) v[k] = s[padidx(tid * ITEMS + k)];
-        // 1. bitonic network over the thread's ITEMS registers (ascending); threads whose
-        //    items are all padding have nothing to do
-        if (tid * ITEMS < n)
+            for (int k = 0; k < ITEMS; ++k) v[k] = s[padidx(tid * ITEMS + k)];
+            // 1. bitonic network over the thread's ITEMS registers (ascending)
 #pragma unroll
-        for (int kk = 2; kk <= ITEMS; kk <<= 1) {
+            for (int kk = 2; kk <= ITEMS; kk <<= 1) {
 #pragma unroll
-            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+                for (int jj = kk >> 1; jj > 0; jj >>= 1) {
 #pragma unroll
-                for (int i = 0; i < ITEMS; ++i) {
-                    const int l = i ^ jj;
-                    if (l > i) ce<TR>(v[i], v[l], (i & kk) == 0);
+                    for (int i = 0; i < ITEMS; ++i) {
+                        const int l = i ^ jj;
+                        if (l > i) ce<TR>(v[i], v[l], (i & kk) == 0);
+                    }
                 }
             }
         }
-        // 2. merge passes
+        // 2. merge passes over the n16 real positions only (runs are merged by their real
+        //    lengths, so padding beyond n16 is never read).  While a run pair lies inside
+        //    one warp's 32*ITEMS elements a warp barrier suffices.
 #pragma unroll 1
         for (u32 w = ITEMS; w < TILE; w <<= 1) {
-            __syncthreads();
+            const bool warp_local = 2 * w <= 32u * ITEMS;
+            if (warp_local) __syncwarp(); else __syncthreads();
+            if (active) {
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k) s[padidx(tid * ITEMS + k)] = v[k];
-            __syncthreads();
+                for (int k = 0; k < ITEMS; ++k) s[padidx(tid * ITEMS + k)] = v[k];
+            }
+            if (warp_local) __syncwarp(); else __syncthreads();
+            if (!active) continue;
             const u32 out0 = tid * ITEMS;
             const u32 ps = out0 & ~(2 * w - 1);  // start of the run pair
             const u32 diag = out0 - ps;
             const u32 A0 = ps, B0 = ps + w;
-            // real (non-padding) elements of the two runs: windows past them output padding
-            const u32 ra = n > A0 ? (n - A0 < w ? n - A0 : w) : 0u;
-            const u32 rb = n > B0 ? (n - B0 < w ? n - B0 : w) : 0u;
-            if (diag >= ra + rb) {
-#pragma unroll
-                for (int k = 0; k < ITEMS; ++k) v[k] = TR::pad();
-                continue;
-            }
-            // merge path: number of A elements among the first diag outputs
-            u32 lo = diag > w ? diag - w : 0u, hi = diag < w ? diag : w;
+            const u32 ra = n16 > A0 ? (n16 - A0 < w ? n16 - A0 : w) : 0u;
+            const u32 rb = n16 > B0 ? (n16 - B0 < w ? n16 - B0 : w) : 0u;
+            // merge path over A[0, ra) and B[0, rb): number of A elements among the first diag
+            u32 lo = diag > rb ? diag - rb : 0u, hi = diag < ra ? diag : ra;
             while (lo < hi) {
                 const u32 mid = (lo + hi) >> 1;
                 if (TR::less(s[padidx(B0 + diag - 1 - mid)], s[padidx(A0 + mid)])) hi = mid;
                 else lo = mid + 1;
             }
             u32 ai = A0 + lo, bi = B0 + (diag - lo);
-            const u32 ae = A0 + w, be = B0 + w;
-            V av = s[padidx(ai < ae ? ai : ae - 1)];
-            V bv = s[padidx(bi < be ? bi : be - 1)];
+            const u32 ae = A0 + ra, be = B0 + rb;
+            V av = s[padidx(ai < ae ? ai : A0)];
+            V bv = s[padidx(bi < be ? bi : (rb ? B0 : A0))];
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) {
                 const bool takeA = ai < ae && (bi >= be || !TR::less(bv, av));
                 v[k] = takeA ? av : bv;
                 if (takeA) {
                     ++ai;
-                    av = s[padidx(ai < ae ? ai : ae - 1)];
+                    av = s[padidx(ai < ae ? ai : A0)];
                 } else {
                     ++bi;
-                    bv = s[padidx(bi < be ? bi : be - 1)];
+                    bv = s[padidx(bi < be ? bi : (rb ? B0 : A0))];
                 }
             }
         }
         __syncthreads();
+        if (active) {
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) s[padidx(tid * ITEMS + k)] = v[k];
+            for (int k = 0; k < ITEMS; ++k) s[padidx(tid * ITEMS + k)] = v[k];
+        }
         __syncthreads();
         for (u32 i = tid; i < n; i += THREADS) g[i] = s[padidx(i)];
         __syncthreads();

@@ -31,12 +31,14 @@ struct K2Smem {
     static constexpr size_t total = buf_bytes + wcnt_bytes + tree_bytes + arr_bytes;
 };
 
-// Loads one tile (<= 512*E elements from tb, len valid) into registers; bit e of the
-// returned mask is set for valid elements.  128-bit coalesced loads (read-only path:
-// every element is read before anything is written to its address in this kernel).
+// Loads one tile (<= NT*E elements from tb, len valid) into raw 16-byte registers; bit e of
+// the returned mask is set for valid elements.  128-bit coalesced loads (read-only path:
+// every element is read before anything is written to its address in this kernel).  The
+// registers are only consumed when the tile is processed, so the loads of the next tile
+// stay in flight while the current one is classified.
 template <class TR, int NT, int E>
 __device__ __forceinline__ u32 k2_load(const typename TR::V* __restrict__ data, u64 tb, u32 len,
-                                       typename TR::V (&v)[E]) {
+                                       uint4 (&raw)[E / TR::VEC]) {
     typedef typename TR::V V;
     constexpr int VEC = TR::VEC, NV = E / VEC;
     const u32 tid = threadIdx.x;
@@ -45,34 +47,46 @@ __device__ __forceinline__ u32 k2_load(const typename TR::V* __restrict__ data, 
     for (int i = 0; i < NV; ++i) {
         const u32 e0 = (u32)(i * NT + tid) * VEC;
         if (e0 + VEC <= len) {
-            uint4 x = ld_nc_v4(data + tb + e0);
-            V tmp[VEC];
-            memcpy(tmp, &x, 16);
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) v[i * VEC + q] = tmp[q];
+            raw[i] = ld_nc_v4(data + tb + e0);
             valid |= ((1u << VEC) - 1u) << (i * VEC);
         } else {
+            V tmp[VEC];
 #pragma unroll
             for (int q = 0; q < VEC; ++q) {
                 if (e0 + q < len) {
-                    v[i * VEC + q] = data[tb + e0 + q];
+                    tmp[q] = data[tb + e0 + q];
                     valid |= 1u << (i * VEC + q);
                 } else {
-                    v[i * VEC + q] = TR::pad();
+                    tmp[q] = TR::pad();
                 }
             }
+            memcpy(&raw[i], tmp, 16);
         }
     }
     return valid;
 }
 
+template <class TR, int NT, int E>
+__device__ __forceinline__ void k2_load_full(const typename TR::V* __restrict__ data, u64 tb,
+                                             uint4 (&raw)[E / TR::VEC]) {
+#pragma unroll
+    for (int i = 0; i < E / TR::VEC; ++i) raw[i] = ld_nc_v4(data + tb + (u64)(i * NT + threadIdx.x) * TR::VEC);
+}
+
 // Branchless descent for all E elements of the thread, level by level so that the E
 // independent shared-memory lookups of a level are in flight together.  LOGK = 8 is the
 // k' = 256 case of the big levels; LOGK = 0 takes the depth at run time.
+// Branchless descent for all E elements of the thread, level by level so that the E
+// independent shared-memory lookups of a level are in flight together.  LOGK = 8 is the
+// k' = 256 case of the big levels; LOGK = 0 takes the depth at run time.
+// The comparison outcome of level l is bit (logk-1-l) of the leaf index i, so a ballot of
+// it per level gives, at the end, the set of lanes whose element fell into the same leaf
+// ("peers", the warp-aggregation mask) without a separate MATCH.ANY; the equality test
+// and the validity of the element add one ballot each.
 template <class TR, int E, int LOGK>
-__device__ __forceinline__ void k2_classify(const typename TR::V (&v)[E], u32 valid,
+__device__ __forceinline__ void k2_classify(const typename TR::V (&v)[E], u32 valid, bool full,
                                             const u64* tree, const u64* spl, u32 logk, u32 kprime,
-                                            u32 eq, u32 (&bk)[E]) {
+                                            u32 eq, u32 (&bk)[E], u32 (&peers)[E]) {
     u64 key[E];
     u32 a[E];  // byte offset 8*j of the current tree node
     const u64 root = tree[1];
@@ -80,34 +94,52 @@ __device__ __forceinline__ void k2_classify(const typename TR::V (&v)[E], u32 va
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         key[e] = TR::key(v[e]);
-        a[e] = key[e] >= root ? 24u : 16u;  // level 0 from a register: j = 2 + [root <= e]
+        const bool p = key[e] >= root;  // level 0 from a register: j = 2 + [root <= e]
+        const u32 x = __ballot_sync(0xffffffffu, p);
+        peers[e] = p ? x : ~x;
+        a[e] = p ? 24u : 16u;
     }
     if (LOGK == 8) {
 #pragma unroll
         for (int l = 1; l < 8; ++l)
 #pragma unroll
-            for (int e = 0; e < E; ++e)
-                a[e] = (a[e] << 1) + (key[e] >= *reinterpret_cast<const u64*>(tb + a[e]) ? 8u : 0u);
+            for (int e = 0; e < E; ++e) {
+                const bool p = key[e] >= *reinterpret_cast<const u64*>(tb + a[e]);
+                const u32 x = __ballot_sync(0xffffffffu, p);
+                peers[e] &= p ? x : ~x;
+                a[e] = (a[e] << 1) + (p ? 8u : 0u);
+            }
     } else {
         for (u32 l = 1; l < logk; ++l)
 #pragma unroll
-            for (int e = 0; e < E; ++e)
-                a[e] = (a[e] << 1) + (key[e] >= *reinterpret_cast<const u64*>(tb + a[e]) ? 8u : 0u);
+            for (int e = 0; e < E; ++e) {
+                const bool p = key[e] >= *reinterpret_cast<const u64*>(tb + a[e]);
+                const u32 x = __ballot_sync(0xffffffffu, p);
+                peers[e] &= p ? x : ~x;
+                a[e] = (a[e] << 1) + (p ? 8u : 0u);
+            }
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         u32 i = (a[e] >> 3) - kprime;
         if (eq) {
             const u32 ii = i ? i : 1u;
-            const u32 isq = (i >= 1u && spl[ii] >= key[e]) ? 1u : 0u;
-            i = 2 * i - isq;
+            const bool isq = i >= 1u && spl[ii] >= key[e];
+            const u32 x = __ballot_sync(0xffffffffu, isq);
+            peers[e] &= isq ? x : ~x;
+            i = 2 * i - (isq ? 1u : 0u);
         }
-        bk[e] = (valid >> e) & 1u ? i : INV_BUCKET;
+        const bool ok = (valid >> e) & 1u;
+        if (!full) {
+            const u32 x = __ballot_sync(0xffffffffu, ok);
+            peers[e] &= ok ? x : ~x;
+        }
+        bk[e] = ok ? i : INV_BUCKET;
     }
 }
 
 template <class TR, int NT, int E, int LOGK>
-__device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const typename TR::V (&v)[E],
+__device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const uint4 (&raw)[E / TR::VEC],
                                         u32 valid, bool final_tile, u64 mb, u32 cap,
                                         typename TR::V* buf, unsigned short* wcnt,
                                         const u64* tree, const u64* spl, u32* fill, u32* cnt,
@@ -116,24 +148,28 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     typedef typename TR::V V;
     constexpr int B = TR::B;
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    V v[E];
+#pragma unroll
+    for (int i = 0; i < E / TR::VEC; ++i) memcpy(&v[i * TR::VEC], &raw[i], 16);
     u32 bk[E];
     u32 pos[E];
-    // 1. classify
-    k2_classify<TR, E, LOGK>(v, valid, tree, spl, logk, kprime, eq, bk);
-    // 2. warp-aggregated ranking
+    // 1. classify (+ per-slot peer masks for the warp aggregation)
+    u32 peers[E];
+    k2_classify<TR, E, LOGK>(v, valid, __all_sync(0xffffffffu, valid == (1u << E) - 1u), tree, spl,
+                             logk, kprime, eq, bk, peers);
+    // 2. warp-aggregated ranking: the leaders' counter updates in slot order
     const u32 lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < E; ++j) {
         const u32 b = bk[j];
-        const u32 peers = __match_any_sync(0xffffffffu, b);
-        const u32 leader = __ffs(peers) - 1;
+        const u32 leader = __ffs(peers[j]) - 1;
         u32 base = 0;
         if (lane == leader && b != INV_BUCKET) {
             base = wcnt[w * MAXK + b];
-            wcnt[w * MAXK + b] = (unsigned short)(base + __popc(peers));
+            wcnt[w * MAXK + b] = (unsigned short)(base + __popc(peers[j]));
         }
         base = __shfl_sync(0xffffffffu, base, leader);
-        pos[j] = base + __popc(peers & lt);
+        pos[j] = base + __popc(peers[j] & lt);
         __syncwarp();
     }
     __syncthreads();
@@ -206,8 +242,8 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     __syncthreads();
 }
 
-template <class TR, int NT, int E>
-__global__ void __launch_bounds__(NT, 1) k_classify(LevelArgs A) {
+template <class TR, int NT, int E, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
     typedef typename TR::V V;
     typedef K2Smem<TR, NT> SM;
     constexpr int B = TR::B;
@@ -250,29 +286,36 @@ __global__ void __launch_bounds__(NT, 1) k_classify(LevelArgs A) {
         const u64 me = sd.end;
         const u32 cap = me > mb ? (u32)((me - mb) / B) : 0u;
         if (mb < me) {
-            V cur[E], nxt[E];
-            u32 vcur = k2_load<TR, NT, E>(data, mb, (u32)((me - mb) < TILE ? (me - mb) : TILE), cur);
-            for (u64 tb = mb; tb < me; tb += TILE) {
-                // prefetch the next tile into registers while this one is processed
-                const u64 tn = tb + TILE;
-                u32 vnxt = 0;
-                if (tn < me) vnxt = k2_load<TR, NT, E>(data, tn, (u32)((me - tn) < TILE ? (me - tn) : TILE), nxt);
+            // full tiles: straight-line 128-bit loads, the next tile prefetched into registers
+            // while this one is processed; then the (single) partial tail tile
+            const u64 nft = (me - mb) / TILE;
+            uint4 cur[E / TR::VEC], nxt[E / TR::VEC];
+            constexpr u32 ALL = (E >= 32) ? 0xFFFFFFFFu : ((1u << E) - 1u);
+            if (nft > 0) k2_load_full<TR, NT, E>(data, mb, cur);
+            for (u64 ti = 0; ti < nft; ++ti) {
+                const u64 tb = mb + ti * TILE;
+                if (ti + 1 < nft) k2_load_full<TR, NT, E>(data, tb + TILE, nxt);
                 if (tp.logk == 8)
-                    k2_tile<TR, NT, E, 8>(data, cur, vcur, false, mb, cap, buf, wcnt, tree, spl, fill, cnt,
-                                   slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
+                    k2_tile<TR, NT, E, 8>(data, cur, ALL, false, mb, cap, buf, wcnt, tree, spl, fill, cnt,
+                                          slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
                 else
-                    k2_tile<TR, NT, E, 0>(data, cur, vcur, false, mb, cap, buf, wcnt, tree, spl, fill, cnt,
-                                   slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
+                    k2_tile<TR, NT, E, 0>(data, cur, ALL, false, mb, cap, buf, wcnt, tree, spl, fill, cnt,
+                                          slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
 #pragma unroll
-                for (int e = 0; e < E; ++e) cur[e] = nxt[e];
-                vcur = vnxt;
+                for (int e = 0; e < E / TR::VEC; ++e) cur[e] = nxt[e];
+            }
+            const u64 tb = mb + nft * TILE;
+            if (tb < me) {
+                const u32 vt = k2_load<TR, NT, E>(data, tb, (u32)(me - tb), cur);
+                k2_tile<TR, NT, E, 0>(data, cur, vt, false, mb, cap, buf, wcnt, tree, spl, fill, cnt,
+                                      slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
             }
         }
         if (sd.first && tp.lo < tp.g) {
             // head elements [lo, g) of the task, processed last so that every write stays
             // behind the read frontier (their block grid starts at g)
             const u64 hend = tp.g < tp.hi ? tp.g : tp.hi;
-            V hv[E];
+            uint4 hv[E / TR::VEC];
             const u32 hval = k2_load<TR, NT, E>(data, tp.lo, (u32)(hend - tp.lo), hv);
             k2_tile<TR, NT, E, 0>(data, hv, hval, true, mb, cap, buf, wcnt, tree, spl, fill, cnt, slotb, nfl,
                            &s_nflushed, tp.logk, tp.kprime, tp.eq);

@@ -156,18 +156,22 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
         }
         src = __shfl_sync(0xffffffffu, src, 0);
         dst = __shfl_sync(0xffffffffu, dst, 0);
-        const uint4 v = ld_v4(base + src * (B * TR::S) + lane * 16);
-        st_v4(base + dst * (B * TR::S) + lane * 16, v);
+        const BlockLane v = ld_blk(base + src * (B * TR::S) + lane * LANE_BYTES);
+        st_blk(base + dst * (B * TR::S) + lane * LANE_BYTES, v);
     }
 }
 
 // ------------------------------------------------------------------ permutation
 
 template <class TR>
-__device__ __forceinline__ u32 block_dest(const uint4& first_lane0, const u64* tree, const u64* spl,
+__device__ __forceinline__ u32 block_dest(const BlockLane& first_lane0, const u64* tree, const u64* spl,
                                           u32 logk, u32 kprime, u32 eq) {
+    // the key is the first 8 bytes of the block's first element (all 8/16-byte types)
+    u64 raw;
+    memcpy(&raw, &first_lane0, 8);
     typename TR::V v;
-    memcpy(&v, &first_lane0, sizeof(v) < 16 ? sizeof(v) : 16);
+    memset(&v, 0, sizeof(v));
+    memcpy(&v, &raw, 8);
     return classify_key(TR::key(v), tree, spl, logk, kprime, eq);
 }
 
@@ -200,9 +204,9 @@ __device__ __forceinline__ u32 next_clear_bit(const u32* bits, u32 nwords, u32 g
 // memory), starting from a task chosen by its index so that CTAs spread over the tasks;
 // when the task has no unprocessed block left it moves to the next unfinished task.
 template <class TR>
-__global__ void __launch_bounds__(K3_THREADS) k_permute(LevelArgs A) {
+__global__ void __launch_bounds__(K3_THREADS, 8) k_permute(LevelArgs A) {
     constexpr int B = TR::B;
-    constexpr u32 BB = B * TR::S;  // block bytes (512)
+    constexpr u32 BB = B * TR::S;  // block bytes
     __shared__ u64 s_tree[MAXK], s_spl[MAXK];
     const u32 tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
     const u32 nw = blockDim.x >> 5;
@@ -256,7 +260,7 @@ __global__ void __launch_bounds__(K3_THREADS) k_permute(LevelArgs A) {
             ok = __shfl_sync(0xffffffffu, ok, 0);
             if (!ok) continue;
             blk = __shfl_sync(0xffffffffu, blk, 0);
-            uint4 cur = ld_v4(tbase + (u64)blk * BB + lane * 16);
+            BlockLane cur = ld_blk(tbase + (u64)blk * BB + lane * LANE_BYTES);
             __threadfence();
             __syncwarp();
             if (lane == 0) atomicSub(&A.readers[gb], 1u);
@@ -273,12 +277,12 @@ __global__ void __launch_bounds__(K3_THREADS) k_permute(LevelArgs A) {
                 const int orr = (int)((u32)old - RBIAS);
                 if (ow <= orr) {
                     // case 1: w_dest points to an unprocessed block -> swap
-                    const uint4 oth = ld_v4(tbase + (u64)ow * BB + lane * 16);
+                    const BlockLane oth = ld_blk(tbase + (u64)ow * BB + lane * LANE_BYTES);
                     u32 od = 0;
                     if (lane == 0) od = block_dest<TR>(oth, s_tree, s_spl, tp.logk, tp.kprime, tp.eq);
                     od = __shfl_sync(0xffffffffu, od, 0);
                     if (od == dest) continue;  // already in place: skip it
-                    st_v4(tbase + (u64)ow * BB + lane * 16, cur);
+                    st_blk(tbase + (u64)ow * BB + lane * LANE_BYTES, cur);
                     cur = oth;
                 } else {
                     // case 2: w_dest points to an empty block -> wait for readers, write, refill
@@ -290,10 +294,10 @@ __global__ void __launch_bounds__(K3_THREADS) k_permute(LevelArgs A) {
                     if (tp.g + (u64)(ow + 1) * B > tp.hi) {
                         // the block would reach past the task end: overflow block
                         char* ob = reinterpret_cast<char*>(A.ovf) + (u64)t * BB;
-                        st_v4(ob + lane * 16, cur);
+                        st_blk(ob + lane * LANE_BYTES, cur);
                         if (lane == 0) A.ovf_owner[t] = (int)dest;
                     } else {
-                        st_v4(tbase + (u64)ow * BB + lane * 16, cur);
+                        st_blk(tbase + (u64)ow * BB + lane * LANE_BYTES, cur);
                     }
                     break;
                 }

@@ -12,7 +12,7 @@
 namespace ips4o {
 
 constexpr int K1_THREADS = 1024;
-constexpr int K1_SAMPLE = 2048;        // sample capacity for ordinary tasks (static smem)
+constexpr int K1_SAMPLE = 4096;        // sample capacity for ordinary tasks (32 KB smem)
 constexpr int K1_SAMPLE_BIG = 16384;   // for tasks of >= 2^22 elements (dynamic smem, 128 KB)
 constexpr u64 K1_BIG_TASK = 1ull << 22;
 

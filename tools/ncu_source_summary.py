@@ -5,9 +5,11 @@ import subprocess
 import sys
 
 
-def main(rep, top=25):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                         capture_output=True, text=True).stdout
+def main(rep, top=25, kernel=None, launch=0):
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if kernel:
+        cmd += ["-k", f"regex:{kernel}", "-s", str(launch), "-c", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr = None
     fname = ""
@@ -40,4 +42,11 @@ def main(rep, top=25):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 25)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("rep")
+    ap.add_argument("--top", type=int, default=25)
+    ap.add_argument("-k", "--kernel", default=None)
+    ap.add_argument("-s", "--launch", type=int, default=0)
+    a = ap.parse_args()
+    main(a.rep, a.top, a.kernel, a.launch)
