@@ -14,10 +14,7 @@ constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer (SURVEY 
 constexpr u32 INV_BUCKET = 0xFFFFu;  // "no element" marker in classification registers
 constexpr int K3_THREADS = 256;      // block permutation CTA (one chain per warp)
 constexpr int K4_THREADS = 256;      // cleanup CTA
-#ifndef IPS4O_BLOCK_BYTES
-#define IPS4O_BLOCK_BYTES 512
-#endif
-constexpr int BLOCK_BYTES = IPS4O_BLOCK_BYTES;  // block b*s in bytes for the 8/16-byte types
+constexpr int BLOCK_BYTES = 512;  // block b*s in bytes for the 8/16-byte types (records: 400)
 
 // ----------------------------------------------------------------- element traits
 // key(): order-preserving unsigned 64-bit image of the sort key.
@@ -26,8 +23,9 @@ constexpr int BLOCK_BYTES = IPS4O_BLOCK_BYTES;  // block b*s in bytes for the 8/
 
 struct TU64 {
     typedef u64 V;
-    static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 0;
-    __device__ __forceinline__ static u64 key(V v) { return v; }
+    static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 0, PARTS = 1;
+    static constexpr u32 LEAF = 4096;  // target base-case size of the adaptive k
+    __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v; }
     __device__ __forceinline__ static bool less(V a, V b) { return a < b; }
     __host__ __device__ __forceinline__ static V pad() { return ~0ull; }
 };
@@ -36,8 +34,9 @@ struct TU64 {
 // non-negatives -> unsigned order equals '<' (PAPER.md:452 uses 64-bit floats).
 struct TF64 {
     typedef u64 V;
-    static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 1;
-    __host__ __device__ __forceinline__ static u64 key(V v) {
+    static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 1, PARTS = 1;
+    static constexpr u32 LEAF = 4096;
+    __host__ __device__ __forceinline__ static u64 key(V v, u32 = 0) {
         return (v >> 63) ? ~v : (v | 0x8000000000000000ull);
     }
     __device__ __forceinline__ static bool less(V a, V b) { return key(a) < key(b); }
@@ -46,18 +45,40 @@ struct TF64 {
 
 struct TPair {
     typedef ulonglong2 V;
-    static constexpr int S = 16, B = BLOCK_BYTES / 16, VEC = 1, CAP = 8192, TYPE = 2;
-    __device__ __forceinline__ static u64 key(V v) { return v.x; }
+    static constexpr int S = 16, B = BLOCK_BYTES / 16, VEC = 1, CAP = 8192, TYPE = 2, PARTS = 1;
+    static constexpr u32 LEAF = 4096;
+    __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v.x; }
     __device__ __forceinline__ static bool less(V a, V b) {
         return a.x < b.x || (a.x == b.x && a.y < b.y);
     }
     __host__ __device__ __forceinline__ static V pad() { return make_ulonglong2(~0ull, ~0ull); }
 };
 
+// 100-byte record, 4-byte aligned; key = bytes [0,10) in memcmp order.  The key is
+// compared in two 64-bit parts: part 0 = big-endian bytes 0..7, part 1 = big-endian bytes
+// 8..9.  A distribution step classifies on one part; an equality bucket of part 0 (equal
+// first 8 bytes) is re-partitioned on part 1, and the base case compares both.
+struct Rec100 {
+    u32 w[25];
+};
+struct TRec {
+    typedef Rec100 V;
+    static constexpr int S = 100, B = 4, VEC = 0, CAP = 1024, TYPE = 3, PARTS = 2;
+    static constexpr u32 LEAF = 512;
+    __device__ __forceinline__ static u64 hi_of(u32 w0, u32 w1) {
+        return ((u64)__byte_perm(w0, 0, 0x0123) << 32) | (u64)__byte_perm(w1, 0, 0x0123);
+    }
+    __device__ __forceinline__ static u64 lo_of(u32 w2) { return (u64)__byte_perm(w2, 0, 0x4401); }
+    __device__ __forceinline__ static u64 key(const V& v, u32 part) {
+        return part ? lo_of(v.w[2]) : hi_of(v.w[0], v.w[1]);
+    }
+};
+
 // ------------------------------------------------------------- level descriptors
 
 struct TaskDesc {
     u64 lo, hi;
+    u32 part, pad_;   // key part the next distribution step classifies on (records only)
 };
 
 // Per task of one distribution level.  Block grid origin g: the first element index
@@ -69,7 +90,7 @@ struct TaskParam {
     u32 nblocks;
     u32 kprime, logk, eq, K;      // classifier (written by k_sample or the debug path)
     u32 stripe_begin, nstripes;   // this task's stripes in the stripe table (contiguous)
-    u32 pad_;
+    u32 part;                     // key part (TRec); 0 otherwise
 };
 
 // A stripe: [begin, end) elements of one task.  Its whole blocks [sb, se) (relative to
@@ -158,37 +179,62 @@ __device__ __forceinline__ uint4 ld_v4(const void* p) {
                  : "memory");
     return r;
 }
-// A block held by one warp: BLOCK_BYTES / 32 bytes per lane (16 B for 512-B blocks, 8 B
-// for 256-B blocks).
-#if IPS4O_BLOCK_BYTES == 512
-typedef uint4 BlockLane;
-__device__ __forceinline__ BlockLane ld_blk(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p)
-                 : "memory");
-    return r;
-}
-__device__ __forceinline__ void st_blk(void* p, BlockLane v) {
-    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-                 "r"(v.w)
-                 : "memory");
-}
-#elif IPS4O_BLOCK_BYTES == 256
-typedef uint2 BlockLane;
-__device__ __forceinline__ BlockLane ld_blk(const void* p) {
-    uint2 r;
-    asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
-    return r;
-}
-__device__ __forceinline__ void st_blk(void* p, BlockLane v) {
-    asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
-}
-#else
-#error "IPS4O_BLOCK_BYTES must be 256 or 512"
-#endif
-constexpr int LANE_BYTES = BLOCK_BYTES / 32;
+// A block held by one warp in registers (K3 swap buffers, Appendix-A moves): 4 words per
+// lane.  8/16-byte types: 512-byte blocks, one 16-byte vector per lane.  Records: 400-byte
+// blocks (4 records, 4-byte aligned), lane l holds words l, l+32, l+64, l+96.
+struct BlockRegs {
+    u32 w[4];
+};
+template <class TR>
+struct BlockIO {
+    static constexpr u32 BB = TR::B * TR::S;  // block bytes
+    __device__ __forceinline__ static BlockRegs load(const char* blk, u32 lane) {
+        BlockRegs r;
+        if constexpr (TR::S == 100) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const u32 idx = lane + 32 * i;
+                r.w[i] = idx < BB / 4 ? *(volatile const u32*)(blk + 4 * idx) : 0u;
+            }
+        } else {
+            asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+                         : "l"(blk + 16 * lane)
+                         : "memory");
+        }
+        return r;
+    }
+    __device__ __forceinline__ static void store(char* blk, u32 lane, const BlockRegs& r) {
+        if constexpr (TR::S == 100) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const u32 idx = lane + 32 * i;
+                if (idx < BB / 4) *(volatile u32*)(blk + 4 * idx) = r.w[i];
+            }
+        } else {
+            asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(blk + 16 * lane), "r"(r.w[0]),
+                         "r"(r.w[1]), "r"(r.w[2]), "r"(r.w[3])
+                         : "memory");
+        }
+    }
+    // key part `part` of the block's first element (warp-collective)
+    __device__ __forceinline__ static u64 first_key(const BlockRegs& r, u32 part) {
+        if constexpr (TR::S == 100) {
+            const u32 w0 = __shfl_sync(0xffffffffu, r.w[0], 0);
+            const u32 w1 = __shfl_sync(0xffffffffu, r.w[0], 1);
+            const u32 w2 = __shfl_sync(0xffffffffu, r.w[0], 2);
+            return part ? TRec::lo_of(w2) : TRec::hi_of(w0, w1);
+        } else {
+            const u32 w0 = __shfl_sync(0xffffffffu, r.w[0], 0);
+            const u32 w1 = __shfl_sync(0xffffffffu, r.w[1], 0);
+            typename TR::V v;
+            memset(&v, 0, sizeof(v));
+            const u64 raw = ((u64)w1 << 32) | w0;
+            memcpy(&v, &raw, 8);
+            return TR::key(v, part);
+        }
+    }
+};
 
 __device__ __forceinline__ void st_v4(void* p, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),

@@ -13,6 +13,7 @@
 #include "common.cuh"
 #include "k_base.cuh"
 #include "k_classify.cuh"
+#include "k_classify_rec.cuh"
 #include "k_cleanup.cuh"
 #include "k_permute.cuh"
 #include "k_sample.cuh"
@@ -295,9 +296,32 @@ static cudaError_t k2_setup(int* occ) {
                                                          K2Smem<TR, C::NT>::total);
 }
 
+constexpr int K2REC_THREADS = 256;
+
 template <class TR>
 static int prepare_kernels(void) {
     if (g_ws.k2_type == TR::TYPE) return IPS4O_OK;
+    if constexpr (TR::S == 100) {
+        int occ2 = 0, occ3 = 0;
+        CK(cudaFuncSetAttribute(k_classify_rec<K2REC_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)K2RecSmem<K2REC_THREADS>::total));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_classify_rec<K2REC_THREADS>, K2REC_THREADS,
+                                                         K2RecSmem<K2REC_THREADS>::total));
+        CK(cudaFuncSetAttribute(k_base_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase::smem));
+        CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                K1_SAMPLE_BIG * 8));
+        CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                K1_SAMPLE * 8));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_permute<TR>, K3_THREADS, 0));
+        if (occ2 < 1 || occ3 < 1) {
+            snprintf(g_errbuf, sizeof g_errbuf, "occupancy query returned %d/%d", occ2, occ3);
+            return IPS4O_ECUDA;
+        }
+        g_ws.k2_blocks = (u32)(occ2 * g_ws.num_sms);
+        g_ws.k3_blocks = (u32)(occ3 * g_ws.num_sms);
+        g_ws.k2_type = TR::TYPE;
+        return IPS4O_OK;
+    } else {
     CK(set_base_attrs<TR>());
     CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             K1_SAMPLE_BIG * 8));
@@ -315,6 +339,7 @@ static int prepare_kernels(void) {
     g_ws.k3_blocks = (u32)(occ3 * g_ws.num_sms);
     g_ws.k2_type = TR::TYPE;
     return IPS4O_OK;
+    }
 }
 
 template <class TR>
@@ -373,14 +398,16 @@ static void plan_batch(const TaskDesc* tasks, u32 T, uintptr_t base_addr, u32* S
     u32 S = 0;
     for (u32 i = 0; i < T; ++i) {
         const u64 lo = tasks[i].lo, hi = tasks[i].hi;
-        u64 g = lo;
-        while (((base_addr + g * TR::S) & 15u) != 0 && g < hi) ++g;
+        u64 g = lo;  // records: the block grid starts at lo (4-byte copies, no TMA)
+        if (TR::S != 100)
+            while (((base_addr + g * TR::S) & 15u) != 0 && g < hi) ++g;
         TaskParam& tp = g_ws.h_tp[i];
         memset(&tp, 0, sizeof tp);
         tp.lo = lo;
         tp.hi = hi;
         tp.g = g;
         tp.nblocks = (u32)((hi - g + B - 1) / B);
+        tp.part = tasks[i].part;
         const u64 main = hi - g;
         u64 ns = std::max<u64>(1, (main + L / 2) / L);
         u64 Lt = ((main + ns - 1) / ns + B - 1) / B * B;
@@ -436,7 +463,9 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
             LAUNCH(KK_SAMPLE, (k_sample<TR, K1_SAMPLE><<<T, K1_THREADS, K1_SAMPLE * 8, st>>>(A)));
     }
     const u32 g2 = std::min<u32>(S, g_ws.k2_blocks);
-    if (k2_variant() == 1) {
+    if constexpr (TR::S == 100) {
+        LAUNCH(KK_CLASSIFY, (k_classify_rec<K2REC_THREADS><<<g2, K2REC_THREADS, K2RecSmem<K2REC_THREADS>::total, st>>>(A)));
+    } else if (k2_variant() == 1) {
         typedef K2Cfg1<TR> C;
         LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E, C::MINB><<<g2, C::NT, K2Smem<TR, C::NT>::total, st>>>(A)));
     } else {
@@ -488,17 +517,29 @@ static int run_base_class(void* data, u32 count, TaskDesc* d_tasks, cudaStream_t
 // counts[c] tasks of size class c at d_queues + c*QCAP
 template <class TR>
 static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStream_t st) {
-    int rc = run_base_class<TR, 128>(data, counts[0], d_queues, st);
-    if (!rc) rc = run_base_class<TR, 256>(data, counts[1], d_queues + QCAP, st);
-    if (!rc) rc = run_base_class<TR, 512>(data, counts[2], d_queues + 2 * QCAP, st);
-    if (!rc && counts[3]) {
-        if (TR::CAP < 16384) {
-            snprintf(g_errbuf, sizeof g_errbuf, "base task above the type's capacity");
+    if constexpr (TR::S == 100) {
+        if (counts[1] || counts[2] || counts[3]) {
+            snprintf(g_errbuf, sizeof g_errbuf, "record base task above capacity");
             return IPS4O_EINTERNAL;
         }
-        rc = run_base_class<TR, (TR::CAP >= 16384 ? 1024 : 512)>(data, counts[3], d_queues + 3 * QCAP, st);
+        if (!counts[0]) return IPS4O_OK;
+        const u32 grid = std::min<u32>(counts[0], 4u * g_ws.num_sms);
+        LAUNCH(KK_BASE, (k_base_rec<<<grid, KREC_THREADS, RecBase::smem, st>>>(d_queues, counts[0], data)));
+        g_stats.base_tasks += counts[0];
+        return IPS4O_OK;
+    } else {
+        int rc = run_base_class<TR, 128>(data, counts[0], d_queues, st);
+        if (!rc) rc = run_base_class<TR, 256>(data, counts[1], d_queues + QCAP, st);
+        if (!rc) rc = run_base_class<TR, 512>(data, counts[2], d_queues + 2 * QCAP, st);
+        if (!rc && counts[3]) {
+            if (TR::CAP < 16384) {
+                snprintf(g_errbuf, sizeof g_errbuf, "base task above the type's capacity");
+                return IPS4O_EINTERNAL;
+            }
+            rc = run_base_class<TR, (TR::CAP >= 16384 ? 1024 : 512)>(data, counts[3], d_queues + 3 * QCAP, st);
+        }
+        return rc;
     }
-    return rc;
 }
 
 template <class TR>
@@ -511,14 +552,14 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
     if (n <= (u64)TR::CAP) {
         g_stats.base_elements += n;
         const u32 c = base_class(n);
-        g_ws.h_q[0] = TaskDesc{0, n};
+        g_ws.h_q[0] = TaskDesc{0, n, 0u, 0u};
         CK(cudaMemcpyAsync(g_ws.q_base + (size_t)c * QCAP, g_ws.h_q, sizeof(TaskDesc),
                            cudaMemcpyHostToDevice, st));
         u32 counts[NUM_BASE_CLASSES] = {0, 0, 0, 0};
         counts[c] = 1;
         return run_base<TR>(data, counts, g_ws.q_base, st);
     }
-    std::vector<TaskDesc> cur(1, TaskDesc{0, n}), next;
+    std::vector<TaskDesc> cur(1, TaskDesc{0, n, 0u, 0u}), next;
     u64 seed = 0x1234567ull;
     while (!cur.empty()) {
         g_stats.levels++;
@@ -580,10 +621,6 @@ static int check_args(const void* p, u64 n, int type) {
         snprintf(g_errbuf, sizeof g_errbuf, "unknown element type %d", type);
         return IPS4O_EINVAL;
     }
-    if (type == IPS4O_REC100_K10) {
-        snprintf(g_errbuf, sizeof g_errbuf, "element type rec100 is not implemented in this build");
-        return IPS4O_EINVAL;
-    }
     if (n >= (1ull << 40)) {
         snprintf(g_errbuf, sizeof g_errbuf, "n too large");
         return IPS4O_EINVAL;
@@ -593,7 +630,7 @@ static int check_args(const void* p, u64 n, int type) {
         return IPS4O_EINVAL;
     }
     const uintptr_t a = (uintptr_t)p;
-    const int need = type == IPS4O_PAIR_U64 ? 16 : 8;
+    const int need = type == IPS4O_PAIR_U64 ? 16 : type == IPS4O_REC100_K10 ? 4 : 8;
     if (n > 0 && (a % need)) {
         snprintf(g_errbuf, sizeof g_errbuf, "data pointer not %d-byte aligned", need);
         return IPS4O_EALIGN;
@@ -652,7 +689,7 @@ static int debug_partition_impl(void* d, u64 n, const void* h_spl, u32 nspl, int
         return IPS4O_EINVAL;
     }
     CK(cudaMemcpyAsync(g_ws.dsplit, keys.data(), 8ull * nspl, cudaMemcpyHostToDevice, st));
-    TaskDesc td{0, n};
+    TaskDesc td{0, n, 0u, 0u};
     u32 S = 0;
     plan_batch<TR>(&td, 1, (uintptr_t)d, &S);
     rc = run_level<TR>(d, 1, S, st, true, nspl, (u32)eq, 0, 1);
@@ -686,6 +723,7 @@ int ips4o_sort(void* d_data, uint64_t n, int elem_type, void* stream) {
         case IPS4O_U64: return sort_impl<TU64>(d_data, n, st);
         case IPS4O_F64: return sort_impl<TF64>(d_data, n, st);
         case IPS4O_PAIR_U64: return sort_impl<TPair>(d_data, n, st);
+        case IPS4O_REC100_K10: return sort_impl<TRec>(d_data, n, st);
         default: return IPS4O_EINVAL;
     }
 }
@@ -800,6 +838,8 @@ int ips4o_debug_classify(const void* d_in, uint64_t n, int elem_type, const void
         case IPS4O_F64: return debug_classify_impl<TF64>(d_in, n, h_splitters, nspl, eq, d_bucket_out, st);
         case IPS4O_PAIR_U64:
             return debug_classify_impl<TPair>(d_in, n, h_splitters, nspl, eq, d_bucket_out, st);
+        case IPS4O_REC100_K10:
+            return debug_classify_impl<TRec>(d_in, n, h_splitters, nspl, eq, d_bucket_out, st);
         default: return IPS4O_EINVAL;
     }
 }
@@ -824,6 +864,8 @@ int ips4o_debug_partition_once(void* d_data, uint64_t n, int elem_type, const vo
             return debug_partition_impl<TF64>(d_data, n, h_splitters, nspl, eq, (u64*)h_bounds_out, K_out, st);
         case IPS4O_PAIR_U64:
             return debug_partition_impl<TPair>(d_data, n, h_splitters, nspl, eq, (u64*)h_bounds_out, K_out, st);
+        case IPS4O_REC100_K10:
+            return debug_partition_impl<TRec>(d_data, n, h_splitters, nspl, eq, (u64*)h_bounds_out, K_out, st);
         default: return IPS4O_EINVAL;
     }
 }

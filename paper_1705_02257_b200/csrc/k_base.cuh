@@ -31,10 +31,86 @@ __device__ __forceinline__ void ce(typename TR::V& a, typename TR::V& b, bool up
     b = sw ? x : y;
 }
 
+// Sorts the n elements held in s[padidx(0..n)) in place (block-wide; all threads call it).
+// Precondition: positions [n, n16) hold TR::pad(); ends with a __syncthreads().
+template <class TR, int THREADS, int ITEMS>
+__device__ __forceinline__ void block_sort_smem(typename TR::V* s, u32 n) {
+    typedef typename TR::V V;
+    constexpr u32 TILE = THREADS * ITEMS;
+    const u32 tid = threadIdx.x;
+    const u32 n16 = (n + ITEMS - 1) / ITEMS * ITEMS;  // only these positions are touched
+    const bool active = tid * ITEMS < n;
+    V v[ITEMS];
+    if (active) {
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) v[k] = s[padidx(tid * ITEMS + k)];
+        // 1. bitonic network over the thread's ITEMS registers (ascending)
+#pragma unroll
+        for (int kk = 2; kk <= ITEMS; kk <<= 1) {
+#pragma unroll
+            for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const int l = i ^ jj;
+                    if (l > i) ce<TR>(v[i], v[l], (i & kk) == 0);
+                }
+            }
+        }
+    }
+    // 2. merge passes over the n16 real positions only (runs are merged by their real
+    //    lengths, so padding beyond n16 is never read).  While a run pair lies inside one
+    //    warp's 32*ITEMS elements a warp barrier suffices.
+#pragma unroll 1
+    for (u32 w = ITEMS; w < TILE; w <<= 1) {
+        const bool warp_local = 2 * w <= 32u * ITEMS;
+        if (warp_local) __syncwarp(); else __syncthreads();
+        if (active) {
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) s[padidx(tid * ITEMS + k)] = v[k];
+        }
+        if (warp_local) __syncwarp(); else __syncthreads();
+        if (!active) continue;
+        const u32 out0 = tid * ITEMS;
+        const u32 ps = out0 & ~(2 * w - 1);  // start of the run pair
+        const u32 diag = out0 - ps;
+        const u32 A0 = ps, B0 = ps + w;
+        const u32 ra = n16 > A0 ? (n16 - A0 < w ? n16 - A0 : w) : 0u;
+        const u32 rb = n16 > B0 ? (n16 - B0 < w ? n16 - B0 : w) : 0u;
+        // merge path over A[0, ra) and B[0, rb): number of A elements among the first diag
+        u32 lo = diag > rb ? diag - rb : 0u, hi = diag < ra ? diag : ra;
+        while (lo < hi) {
+            const u32 mid = (lo + hi) >> 1;
+            if (TR::less(s[padidx(B0 + diag - 1 - mid)], s[padidx(A0 + mid)])) hi = mid;
+            else lo = mid + 1;
+        }
+        u32 ai = A0 + lo, bi = B0 + (diag - lo);
+        const u32 ae = A0 + ra, be = B0 + rb;
+        V av = s[padidx(ai < ae ? ai : A0)];
+        V bv = s[padidx(bi < be ? bi : (rb ? B0 : A0))];
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            const bool takeA = ai < ae && (bi >= be || !TR::less(bv, av));
+            v[k] = takeA ? av : bv;
+            if (takeA) {
+                ++ai;
+                av = s[padidx(ai < ae ? ai : A0)];
+            } else {
+                ++bi;
+                bv = s[padidx(bi < be ? bi : (rb ? B0 : A0))];
+            }
+        }
+    }
+    __syncthreads();
+    if (active) {
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) s[padidx(tid * ITEMS + k)] = v[k];
+    }
+    __syncthreads();
+}
+
 template <class TR, int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS) k_base_merge(const TaskDesc* tasks, u32 ntasks, void* vdata) {
     typedef typename TR::V V;
-    constexpr u32 TILE = THREADS * ITEMS;
     extern __shared__ __align__(16) unsigned char smem5[];
     V* s = reinterpret_cast<V*>(smem5);
     V* data = reinterpret_cast<V*>(vdata);
@@ -42,79 +118,59 @@ __global__ void __launch_bounds__(THREADS) k_base_merge(const TaskDesc* tasks, u
     for (u32 ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
         const TaskDesc td = tasks[ti];
         const u32 n = (u32)(td.hi - td.lo);
-        const u32 n16 = (n + ITEMS - 1) / ITEMS * ITEMS;  // only these positions are touched
+        const u32 n16 = (n + ITEMS - 1) / ITEMS * ITEMS;
         V* g = data + td.lo;
         // coalesced load; the last thread's items past n are padding
         for (u32 i = tid; i < n16; i += THREADS) s[padidx(i)] = i < n ? g[i] : TR::pad();
         __syncthreads();
-        const bool active = tid * ITEMS < n;
-        V v[ITEMS];
-        if (active) {
-#pragma unroll
-            for (int k = 0; k < ITEMS; ++k) v[k] = s[padidx(tid * ITEMS + k)];
-            // 1. bitonic network over the thread's ITEMS registers (ascending)
-#pragma unroll
-            for (int kk = 2; kk <= ITEMS; kk <<= 1) {
-#pragma unroll
-                for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-#pragma unroll
-                    for (int i = 0; i < ITEMS; ++i) {
-                        const int l = i ^ jj;
-                        if (l > i) ce<TR>(v[i], v[l], (i & kk) == 0);
-                    }
-                }
-            }
-        }
-        // 2. merge passes over the n16 real positions only (runs are merged by their real
-        //    lengths, so padding beyond n16 is never read).  While a run pair lies inside
-        //    one warp's 32*ITEMS elements a warp barrier suffices.
-#pragma unroll 1
-        for (u32 w = ITEMS; w < TILE; w <<= 1) {
-            const bool warp_local = 2 * w <= 32u * ITEMS;
-            if (warp_local) __syncwarp(); else __syncthreads();
-            if (active) {
-#pragma unroll
-                for (int k = 0; k < ITEMS; ++k) s[padidx(tid * ITEMS + k)] = v[k];
-            }
-            if (warp_local) __syncwarp(); else __syncthreads();
-            if (!active) continue;
-            const u32 out0 = tid * ITEMS;
-            const u32 ps = out0 & ~(2 * w - 1);  // start of the run pair
-            const u32 diag = out0 - ps;
-            const u32 A0 = ps, B0 = ps + w;
-            const u32 ra = n16 > A0 ? (n16 - A0 < w ? n16 - A0 : w) : 0u;
-            const u32 rb = n16 > B0 ? (n16 - B0 < w ? n16 - B0 : w) : 0u;
-            // merge path over A[0, ra) and B[0, rb): number of A elements among the first diag
-            u32 lo = diag > rb ? diag - rb : 0u, hi = diag < ra ? diag : ra;
-            while (lo < hi) {
-                const u32 mid = (lo + hi) >> 1;
-                if (TR::less(s[padidx(B0 + diag - 1 - mid)], s[padidx(A0 + mid)])) hi = mid;
-                else lo = mid + 1;
-            }
-            u32 ai = A0 + lo, bi = B0 + (diag - lo);
-            const u32 ae = A0 + ra, be = B0 + rb;
-            V av = s[padidx(ai < ae ? ai : A0)];
-            V bv = s[padidx(bi < be ? bi : (rb ? B0 : A0))];
-#pragma unroll
-            for (int k = 0; k < ITEMS; ++k) {
-                const bool takeA = ai < ae && (bi >= be || !TR::less(bv, av));
-                v[k] = takeA ? av : bv;
-                if (takeA) {
-                    ++ai;
-                    av = s[padidx(ai < ae ? ai : A0)];
-                } else {
-                    ++bi;
-                    bv = s[padidx(bi < be ? bi : (rb ? B0 : A0))];
-                }
-            }
-        }
-        __syncthreads();
-        if (active) {
-#pragma unroll
-            for (int k = 0; k < ITEMS; ++k) s[padidx(tid * ITEMS + k)] = v[k];
-        }
-        __syncthreads();
+        block_sort_smem<TR, THREADS, ITEMS>(s, n);
         for (u32 i = tid; i < n; i += THREADS) g[i] = s[padidx(i)];
+        __syncthreads();
+    }
+}
+
+// Records: sort (key part 0, key part 1 << 32 | index) items in shared memory, then gather
+// the records into their sorted positions through a shared-memory copy of the leaf.
+struct TRecItem {
+    typedef ulonglong2 V;
+    __device__ __forceinline__ static bool less(V a, V b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
+    __host__ __device__ __forceinline__ static V pad() { return make_ulonglong2(~0ull, ~0ull); }
+};
+constexpr int KREC_THREADS = 256, KREC_ITEMS = 4;  // CAP = 1024 records
+struct RecBase {
+    static constexpr size_t items_bytes = (size_t)padidx(KREC_THREADS * KREC_ITEMS) * 16 + 16;
+    static constexpr size_t smem = items_bytes + (size_t)KREC_THREADS * KREC_ITEMS * 100;
+};
+
+__global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks, u32 ntasks, void* vdata) {
+    extern __shared__ __align__(16) unsigned char smem5[];
+    ulonglong2* it = reinterpret_cast<ulonglong2*>(smem5);
+    u32* srec = reinterpret_cast<u32*>(smem5 + RecBase::items_bytes);
+    u32* gw = reinterpret_cast<u32*>(vdata);
+    const u32 tid = threadIdx.x;
+    for (u32 ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
+        const TaskDesc td = tasks[ti];
+        const u32 n = (u32)(td.hi - td.lo);
+        const u32 n16 = (n + KREC_ITEMS - 1) / KREC_ITEMS * KREC_ITEMS;
+        u32* g = gw + td.lo * 25;
+        for (u32 i = tid; i < n * 25; i += KREC_THREADS) srec[i] = g[i];
+        __syncthreads();
+        for (u32 i = tid; i < n16; i += KREC_THREADS) {
+            ulonglong2 x = TRecItem::pad();
+            if (i < n) {
+                const u32* r = srec + i * 25;
+                x.x = TRec::hi_of(r[0], r[1]);
+                x.y = (TRec::lo_of(r[2]) << 32) | i;
+            }
+            it[padidx(i)] = x;
+        }
+        __syncthreads();
+        block_sort_smem<TRecItem, KREC_THREADS, KREC_ITEMS>(it, n);
+        for (u32 i = tid; i < n * 25; i += KREC_THREADS) {
+            const u32 r = i / 25, wd = i - r * 25;
+            const u32 src = (u32)(it[padidx(r)].y & 0xFFFFFFFFu);
+            g[i] = srec[src * 25 + wd];
+        }
         __syncthreads();
     }
 }
@@ -137,7 +193,7 @@ __global__ void k_debug_classify(const void* vin, u64 n, const u64* tree_g, cons
     const typename TR::V* in = reinterpret_cast<const typename TR::V*>(vin);
     const u32 logk = tp->logk, kp = tp->kprime, eq = tp->eq;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
-        out[i] = classify_key(TR::key(in[i]), tree, spl, logk, kp, eq);
+        out[i] = classify_key(TR::key(in[i], 0), tree, spl, logk, kp, eq);
 }
 
 }  // namespace ips4o

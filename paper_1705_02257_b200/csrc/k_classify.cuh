@@ -76,24 +76,34 @@ __device__ __forceinline__ void k2_load_full(const typename TR::V* __restrict__ 
 // Branchless descent for all E elements of the thread, level by level so that the E
 // independent shared-memory lookups of a level are in flight together.  LOGK = 8 is the
 // k' = 256 case of the big levels; LOGK = 0 takes the depth at run time.
-// Branchless descent for all E elements of the thread, level by level so that the E
-// independent shared-memory lookups of a level are in flight together.  LOGK = 8 is the
-// k' = 256 case of the big levels; LOGK = 0 takes the depth at run time.
 // The comparison outcome of level l is bit (logk-1-l) of the leaf index i, so a ballot of
 // it per level gives, at the end, the set of lanes whose element fell into the same leaf
 // ("peers", the warp-aggregation mask) without a separate MATCH.ANY; the equality test
 // and the validity of the element add one ballot each.
+template <int E, int LOGK>
+__device__ __forceinline__ void k2_classify_keys(const u64 (&key)[E], u32 valid, bool full,
+                                                 const u64* tree, const u64* spl, u32 logk,
+                                                 u32 kprime, u32 eq, u32 (&bk)[E], u32 (&peers)[E]);
+
 template <class TR, int E, int LOGK>
 __device__ __forceinline__ void k2_classify(const typename TR::V (&v)[E], u32 valid, bool full,
                                             const u64* tree, const u64* spl, u32 logk, u32 kprime,
                                             u32 eq, u32 (&bk)[E], u32 (&peers)[E]) {
     u64 key[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) key[e] = TR::key(v[e], 0);
+    k2_classify_keys<E, LOGK>(key, valid, full, tree, spl, logk, kprime, eq, bk, peers);
+}
+
+template <int E, int LOGK>
+__device__ __forceinline__ void k2_classify_keys(const u64 (&key)[E], u32 valid, bool full,
+                                                 const u64* tree, const u64* spl, u32 logk,
+                                                 u32 kprime, u32 eq, u32 (&bk)[E], u32 (&peers)[E]) {
     u32 a[E];  // byte offset 8*j of the current tree node
     const u64 root = tree[1];
     const char* tb = reinterpret_cast<const char*>(tree);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        key[e] = TR::key(v[e]);
         const bool p = key[e] >= root;  // level 0 from a register: j = 2 + [root <= e]
         const u32 x = __ballot_sync(0xffffffffu, p);
         peers[e] = p ? x : ~x;

@@ -122,20 +122,28 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
         const u64 dst = (u64)k < hl ? e0 + k : ts + (k - hl);
         data[dst] = val;
     }
-    // emit the bucket (equality buckets are never recursed into)
+    // emit the bucket.  Equality buckets are never recursed into; for
+    // records an equality bucket of key part 0 (equal first 8 key bytes) still has to be
+    // ordered by part 1, so it becomes a task on the next part.
     if (tid == 0 && A.emit) {
         const u64 sz = e1 - e0;
         const bool eqb = tp.eq && (b & 1u);
-        if (sz > 1 && !eqb) {
+        u32 part = tp.part;
+        bool emit = sz > 1;
+        if (eqb) {
+            if (part + 1 < (u32)TR::PARTS) ++part;
+            else emit = false;
+        }
+        if (emit) {
             if (sz <= A.base_cap) {
                 atomicAdd((unsigned long long*)A.base_elems, (unsigned long long)sz);
                 const u32 c = base_class(sz);
                 u32 i = atomicAdd(&A.ctr[CTR_BASE0 + c], 1u);
-                if (i < A.q_cap) A.q_base[(u64)c * A.q_cap + i] = TaskDesc{e0, e1};
+                if (i < A.q_cap) A.q_base[(u64)c * A.q_cap + i] = TaskDesc{e0, e1, 0u, 0u};
                 else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
             } else {
                 u32 i = atomicAdd(&A.ctr[CTR_NEXT], 1u);
-                if (i < A.q_cap) A.q_next[i] = TaskDesc{e0, e1};
+                if (i < A.q_cap) A.q_next[i] = TaskDesc{e0, e1, part, 0u};
                 else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
             }
         }

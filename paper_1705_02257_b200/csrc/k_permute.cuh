@@ -156,23 +156,19 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
         }
         src = __shfl_sync(0xffffffffu, src, 0);
         dst = __shfl_sync(0xffffffffu, dst, 0);
-        const BlockLane v = ld_blk(base + src * (B * TR::S) + lane * LANE_BYTES);
-        st_blk(base + dst * (B * TR::S) + lane * LANE_BYTES, v);
+        const BlockRegs v = BlockIO<TR>::load(base + src * (B * TR::S), lane);
+        BlockIO<TR>::store(base + dst * (B * TR::S), lane, v);
     }
 }
 
 // ------------------------------------------------------------------ permutation
 
+// destination bucket of a block: classify its first element (warp-collective key fetch,
+// the classification itself by every lane on the same value)
 template <class TR>
-__device__ __forceinline__ u32 block_dest(const BlockLane& first_lane0, const u64* tree, const u64* spl,
-                                          u32 logk, u32 kprime, u32 eq) {
-    // the key is the first 8 bytes of the block's first element (all 8/16-byte types)
-    u64 raw;
-    memcpy(&raw, &first_lane0, 8);
-    typename TR::V v;
-    memset(&v, 0, sizeof(v));
-    memcpy(&v, &raw, 8);
-    return classify_key(TR::key(v), tree, spl, logk, kprime, eq);
+__device__ __forceinline__ u32 block_dest(const BlockRegs& r, const u64* tree, const u64* spl,
+                                          u32 logk, u32 kprime, u32 eq, u32 part) {
+    return classify_key(BlockIO<TR>::first_key(r, part), tree, spl, logk, kprime, eq);
 }
 
 // next bucket (cyclic over nwords*32 buckets, starting at gb inclusive) whose bit in
@@ -260,15 +256,13 @@ __global__ void __launch_bounds__(K3_THREADS, 8) k_permute(LevelArgs A) {
             ok = __shfl_sync(0xffffffffu, ok, 0);
             if (!ok) continue;
             blk = __shfl_sync(0xffffffffu, blk, 0);
-            BlockLane cur = ld_blk(tbase + (u64)blk * BB + lane * LANE_BYTES);
+            BlockRegs cur = BlockIO<TR>::load(tbase + (u64)blk * BB, lane);
             __threadfence();
             __syncwarp();
             if (lane == 0) atomicSub(&A.readers[gb], 1u);
             // ---- chain: place the block, swapping with unprocessed blocks on the way
             for (;;) {
-                u32 dest = 0;
-                if (lane == 0) dest = block_dest<TR>(cur, s_tree, s_spl, tp.logk, tp.kprime, tp.eq);
-                dest = __shfl_sync(0xffffffffu, dest, 0);
+                const u32 dest = block_dest<TR>(cur, s_tree, s_spl, tp.logk, tp.kprime, tp.eq, tp.part);
                 const u32 gbd = t * MAXK + dest;
                 u64 old = 0;
                 if (lane == 0) old = atomicAdd((unsigned long long*)&A.wr[gbd], 1ull << 32);  // w += 1
@@ -277,12 +271,10 @@ __global__ void __launch_bounds__(K3_THREADS, 8) k_permute(LevelArgs A) {
                 const int orr = (int)((u32)old - RBIAS);
                 if (ow <= orr) {
                     // case 1: w_dest points to an unprocessed block -> swap
-                    const BlockLane oth = ld_blk(tbase + (u64)ow * BB + lane * LANE_BYTES);
-                    u32 od = 0;
-                    if (lane == 0) od = block_dest<TR>(oth, s_tree, s_spl, tp.logk, tp.kprime, tp.eq);
-                    od = __shfl_sync(0xffffffffu, od, 0);
+                    const BlockRegs oth = BlockIO<TR>::load(tbase + (u64)ow * BB, lane);
+                    const u32 od = block_dest<TR>(oth, s_tree, s_spl, tp.logk, tp.kprime, tp.eq, tp.part);
                     if (od == dest) continue;  // already in place: skip it
-                    st_blk(tbase + (u64)ow * BB + lane * LANE_BYTES, cur);
+                    BlockIO<TR>::store(tbase + (u64)ow * BB, lane, cur);
                     cur = oth;
                 } else {
                     // case 2: w_dest points to an empty block -> wait for readers, write, refill
@@ -294,10 +286,10 @@ __global__ void __launch_bounds__(K3_THREADS, 8) k_permute(LevelArgs A) {
                     if (tp.g + (u64)(ow + 1) * B > tp.hi) {
                         // the block would reach past the task end: overflow block
                         char* ob = reinterpret_cast<char*>(A.ovf) + (u64)t * BB;
-                        st_blk(ob + lane * LANE_BYTES, cur);
+                        BlockIO<TR>::store(ob, lane, cur);
                         if (lane == 0) A.ovf_owner[t] = (int)dest;
                     } else {
-                        st_blk(tbase + (u64)ow * BB + lane * LANE_BYTES, cur);
+                        BlockIO<TR>::store(tbase + (u64)ow * BB, lane, cur);
                     }
                     break;
                 }

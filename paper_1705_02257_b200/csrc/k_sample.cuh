@@ -61,13 +61,13 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
     const V* data = reinterpret_cast<const V*>(A.data);
 
     // Bucket count: the last levels use an adaptive k aimed at
-    // base-case tiles of ~4096 elements: k = min(256, max(4, pow2_ceil(n/4096))).
+    // base-case tiles of ~LEAF elements: k = min(256, max(4, pow2_ceil(n/LEAF))).
     // Oversampling: the paper's alpha = 0.2 log n is a CPU-cache choice;
     // sorting the sample costs the same ~10 us here for any alpha <= 2048/k, so the GPU
     // takes alpha = max(0.2 log2 n, 2048/k - 1 rounded down), which keeps subproblems
     // close to their expected size (fewer extra levels).  Any alpha gives the same output.
     u32 k = 4;
-    while ((u64)k * 4096 < n && k < (u32)MAXK) k *= 2;
+    while ((u64)k * TR::LEAF < n && k < (u32)MAXK) k *= 2;
     u32 alpha = (u32)llround(0.2 * log2((double)n));
     if (alpha < 1) alpha = 1;
     const u32 amax = (SAMPLE - 1) / k;
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
             u64 a = lo + (u64)((unsigned __int128)n * j / m);
             u64 b = lo + (u64)((unsigned __int128)n * (j + 1) / m);
             u64 r = mix64(A.seed ^ mix64(lo * 0x9E3779B97F4A7C15ull + j));
-            key = TR::key(data[a + r % (b - a)]);
+            key = TR::key(data[a + r % (b - a)], tp->part);
         }
         keys[j] = key;
     }

@@ -25,8 +25,8 @@ import workloads as W  # noqa: E402
 from gpu_util import (check_equal_to_oracle, digest, keys_nondecreasing, to_dev,  # noqa: E402
                             to_host)
 
-TYPES = [W.ELEM_U64, W.ELEM_F64, W.ELEM_PAIR]
-CAP = {W.ELEM_U64: 16384, W.ELEM_F64: 16384, W.ELEM_PAIR: 8192}
+TYPES = [W.ELEM_U64, W.ELEM_F64, W.ELEM_PAIR, W.ELEM_REC100]
+CAP = {W.ELEM_U64: 16384, W.ELEM_F64: 16384, W.ELEM_PAIR: 8192, W.ELEM_REC100: 1024}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -60,6 +60,14 @@ def _gen(et, n, seed, kind="uniform"):
         if kind == "max":
             a[:, 0] = np.where(rng.random(n) < 0.5, np.uint64(2**64 - 1), np.uint64(0))
         return a
+    if et == W.ELEM_REC100:
+        a = W.rec100(n, seed)
+        if kind == "few":   # 3 values of key bytes 0..7, 5 of bytes 8..9: equality buckets on part 0
+            a[:, :8] = (rng.integers(0, 3, size=n)[:, None] * np.array([1, 7, 0, 0, 0, 0, 0, 9])).astype(np.uint8)
+            a[:, 8:10] = rng.integers(0, 5, size=(n, 1)).astype(np.uint8)
+        if kind == "max":
+            a[:, :10] = np.where(rng.random(n)[:, None] < 0.5, 255, 0).astype(np.uint8)
+        return a
     raise ValueError
 
 
@@ -77,10 +85,24 @@ def _spl_keys(spl, et):
 
 
 def _oracle_spl(spl, et):
-    """The oracle takes splitters as elements of the sorted type (pairs: key, payload 0)."""
+    """The oracle takes splitters as elements of the sorted type (pairs: key, payload 0;
+    records: key bytes 0..7 = the big-endian u64 splitter, bytes 8..9 = 0, so that the
+    oracle's 10-byte comparison and the GPU's part-0 comparison agree, ties going right)."""
     if et == W.ELEM_PAIR:
         return np.stack([spl.astype(np.uint64), np.zeros(spl.shape[0], np.uint64)], axis=1)
+    if et == W.ELEM_REC100:
+        r = np.zeros((spl.shape[0], 100), np.uint8)
+        r[:, :8] = spl.astype(">u8").view(np.uint8).reshape(-1, 8)
+        return r
     return spl
+
+
+def _keys_of(a, et):
+    if et == W.ELEM_PAIR:
+        return a[:, 0]
+    if et == W.ELEM_REC100:
+        return np.ascontiguousarray(a[:, :8]).view(">u8").ravel().astype(np.uint64)
+    return a
 
 
 @pytest.mark.parametrize("et", TYPES)
@@ -102,6 +124,11 @@ def test_classify_vs_oracle(et, eq):
             elems = np.concatenate([rng.integers(0, 1 << 40, size=5000, dtype=np.uint64), spl])
         if et == W.ELEM_PAIR:
             el = np.stack([elems.astype(np.uint64), np.arange(elems.shape[0], dtype=np.uint64)], axis=1)
+        elif et == W.ELEM_REC100:
+            if eq:
+                continue   # record splitters compare on key part 0 only: no 10-byte equality test
+            el = W.rec100(elems.shape[0], trial)
+            el[:, :8] = elems.astype(">u8").view(np.uint8).reshape(-1, 8)
         else:
             el = elems
         exp = oracle.classify(_oracle_spl(spl, et), eq, el)
@@ -120,7 +147,7 @@ def test_classify_vs_oracle(et, eq):
 def _partition_case(et, n, nspl, eq, seed, offset=0, kind="uniform"):
     rng = np.random.default_rng(seed)
     a = _gen(et, n + offset, seed, kind)
-    keys = a[:, 0] if et == W.ELEM_PAIR else a
+    keys = _keys_of(a, et)
     pool = np.unique(keys[offset:])
     nspl = min(nspl, pool.shape[0])
     spl = np.sort(rng.choice(pool, size=nspl, replace=False))
@@ -128,7 +155,7 @@ def _partition_case(et, n, nspl, eq, seed, offset=0, kind="uniform"):
     sub = np.ascontiguousarray(a[offset:])
     o_out, o_bounds = oracle.partition_with(sub, _oracle_spl(spl, et), eq, 16)
     d = to_dev(a, et)
-    esz = 16 if et == W.ELEM_PAIR else 8
+    esz = W.ELEM_SIZE[et]
     buf, ptr, ns = ips4o.splitters_buffer(_spl_keys(spl, et), et)
     bounds, K = ips4o.ips4o_debug_partition_once(d.data_ptr() + offset * esz, n, et, ptr, ns, eq,
                                                  torch.cuda.current_stream().cuda_stream)
@@ -146,6 +173,9 @@ def _partition_case(et, n, nspl, eq, seed, offset=0, kind="uniform"):
         if et == W.ELEM_PAIR:
             gs = np.sort(gs.view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k", "v"])
             os_ = np.sort(os_.view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k", "v"])
+        elif et == W.ELEM_REC100:
+            gs = np.sort(np.ascontiguousarray(gs).view("S100").ravel())
+            os_ = np.sort(np.ascontiguousarray(os_).view("S100").ravel())
         else:
             gs, os_ = np.sort(gs), np.sort(os_)
         assert np.array_equal(gs, os_)
@@ -156,6 +186,8 @@ def test_partition_once_vs_oracle(et):
     cases = [(64, 3, False), (1000, 7, False), (4099, 255, False), (100_003, 255, False),
              (300_001, 100, True), (2_000_003, 255, False), (1_500_017, 127, True)]
     for i, (n, nspl, eq) in enumerate(cases):
+        if et == W.ELEM_REC100 and (eq or n > 400_000):
+            continue
         _partition_case(et, n, nspl, eq, seed=7 + i)
 
 
@@ -176,11 +208,12 @@ def test_partition_once_duplicates_and_skew():
 # ------------------------------------------------------------ (iv) whole sorts
 
 SIZES = [0, 1, 2, 3, 17, 1000, 16383, 16384, 16385, 40_000, 131_073, 1_000_003, 3_000_017]
+SIZES_REC = [0, 1, 2, 3, 17, 1023, 1024, 1025, 5000, 70_001, 300_007]
 
 
 @pytest.mark.parametrize("et", TYPES)
 def test_sort_sizes_vs_oracle(et):
-    for i, n in enumerate(SIZES):
+    for i, n in enumerate(SIZES_REC if et == W.ELEM_REC100 else SIZES):
         a = _gen(et, n, 1000 + i)
         got = _sort_gpu(a, et)
         exp = oracle.sort(a)
@@ -190,17 +223,17 @@ def test_sort_sizes_vs_oracle(et):
 @pytest.mark.parametrize("et", TYPES)
 @pytest.mark.parametrize("kind", ["few", "max"])
 def test_sort_duplicates_vs_oracle(et, kind):
-    for n in (5000, 70_001, 2_000_000):
+    for n in ((5000, 70_001, 400_000) if et == W.ELEM_REC100 else (5000, 70_001, 2_000_000)):
         a = _gen(et, n, 77, kind)
         check_equal_to_oracle(et, a, _sort_gpu(a, et), oracle.sort(a))
 
 
 @pytest.mark.parametrize("dist", ["rootdup", "twodup", "eightdup", "almostsorted", "reversesorted",
                                   "sorted", "zeros", "ones", "uniform", "f64_uniform", "f64_exponential",
-                                  "pair16"])
+                                  "pair16", "rec100"])
 def test_distributions_vs_oracle(dist):
     for seed in (1, 2, 3):
-        et, a = W.make(dist, 1 << 21, seed)
+        et, a = W.make(dist, (1 << 18) if dist == "rec100" else (1 << 21), seed)
         check_equal_to_oracle(et, a, _sort_gpu(a, et), oracle.sort(a))
 
 
@@ -250,7 +283,7 @@ def test_sort_host_entry_point():
 
 
 def test_type_switching_and_reuse():
-    for et in (W.ELEM_PAIR, W.ELEM_U64, W.ELEM_F64, W.ELEM_PAIR):
+    for et in (W.ELEM_PAIR, W.ELEM_U64, W.ELEM_REC100, W.ELEM_F64, W.ELEM_PAIR):
         a = _gen(et, 200_001, 5)
         check_equal_to_oracle(et, a, _sort_gpu(a, et), oracle.sort(a))
 
@@ -259,7 +292,7 @@ def test_type_switching_and_reuse():
 
 FULL = [("uniform", 28), ("f64_uniform", 28), ("f64_exponential", 28), ("rootdup", 27),
         ("twodup", 27), ("eightdup", 27), ("almostsorted", 27), ("reversesorted", 27),
-        ("zeros", 27), ("pair16", 27)]
+        ("zeros", 27), ("pair16", 27), ("rec100", 24)]
 
 
 @pytest.mark.parametrize("dist,e", FULL)
