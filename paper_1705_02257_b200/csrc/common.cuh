@@ -14,7 +14,10 @@ constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer (SURVEY 
 constexpr u32 INV_BUCKET = 0xFFFFu;  // "no element" marker in classification registers
 constexpr int K3_THREADS = 256;      // block permutation CTA (one chain per warp)
 constexpr int K4_THREADS = 256;      // cleanup CTA
-constexpr int BLOCK_BYTES = 512;  // block b*s in bytes for the 8/16-byte types (records: 400)
+#ifndef IPS4O_BLOCK_BYTES
+#define IPS4O_BLOCK_BYTES 512
+#endif
+constexpr int BLOCK_BYTES = IPS4O_BLOCK_BYTES;  // block b*s in bytes for the 8/16-byte types (records: 400)
 
 // ----------------------------------------------------------------- element traits
 // key(): order-preserving unsigned 64-bit image of the sort key.
@@ -114,7 +117,7 @@ constexpr int NUM_BASE_CLASSES = 4;
 __host__ __device__ __forceinline__ u32 base_class(u64 n) {
     return n <= 2048 ? 0u : n <= 4096 ? 1u : n <= 8192 ? 2u : 3u;
 }
-enum { ERR_SPILL = 1, ERR_CONSERVE = 2, ERR_QUEUE = 4, ERR_CAPACITY = 8 };
+enum { ERR_SPILL = 1, ERR_CONSERVE = 2, ERR_QUEUE = 4, ERR_CAPACITY = 8, ERR_PROGRESS = 16 };
 
 struct LevelArgs {
     void* data;

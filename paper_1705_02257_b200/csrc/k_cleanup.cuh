@@ -134,6 +134,12 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
             if (part + 1 < (u32)TR::PARTS) ++part;
             else emit = false;
         }
+        if (emit && !eqb && sz == tp.hi - tp.lo) {
+            // no progress: a splitter choice that leaves the whole task in one
+            // interval bucket would recurse forever -- report instead of looping
+            atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_PROGRESS);
+            emit = false;
+        }
         if (emit) {
             if (sz <= A.base_cap) {
                 atomicAdd((unsigned long long*)A.base_elems, (unsigned long long)sz);

@@ -72,9 +72,11 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
     if (alpha < 1) alpha = 1;
     const u32 amax = (SAMPLE - 1) / k;
     if (alpha < amax) alpha = amax;
-    u32 m = alpha * k - 1;
-    if (m > SAMPLE - 1) m = SAMPLE - 1;
-    if ((u64)m > n) m = (u32)n;
+    // the sample must fit the task (m <= n): a task smaller than the shared-memory sample
+    // (records: 1025..4095 elements) takes alpha = (n+1)/k (>= 1 since n > k here)
+    const u64 acap = (n + 1) / k;
+    if ((u64)alpha > acap) alpha = (u32)(acap > 0 ? acap : 1);
+    const u32 m = alpha * k - 1;
     // stratified random sample without replacement: one element per stratum
     for (u32 j = threadIdx.x; j < (u32)SAMPLE; j += blockDim.x) {
         u64 key = ~0ull;
