@@ -11,8 +11,20 @@ typedef unsigned int u32;
 
 constexpr int MAXK = 256;            // buckets per step: k = 256, or 2k'-1 <= 255 with eq
 constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer
+// Each bucket's permutation control word (packed (w, r), then its reader count) sits in its
+// own 256-byte line, so that the pointer atomics of the k buckets spread over the L2
+// slices instead of sharing the few slices a dense array maps to.
+constexpr int CTL_STRIDE = 32;       // u64 words per bucket control line (256 B)
 constexpr u32 INV_BUCKET = 0xFFFFu;  // "no element" marker in classification registers
-constexpr int K3_THREADS = 256;      // block permutation CTA (one chain per warp)
+constexpr int K3_THREADS = 256;      // block permutation CTA
+#ifndef IPS4O_K3_SLOTS
+#define IPS4O_K3_SLOTS 4
+#endif
+constexpr int K3_SLOTS = IPS4O_K3_SLOTS;  // independent chains per warp
+#ifndef IPS4O_K3_MINB
+#define IPS4O_K3_MINB (IPS4O_K3_SLOTS <= 2 ? 6 : IPS4O_K3_SLOTS <= 4 ? 4 : 2)
+#endif
+constexpr int K3_MINB = IPS4O_K3_MINB;  // CTAs per SM (register budget 65536 / (256 * MINB))
 constexpr int K4_THREADS = 256;      // cleanup CTA
 #ifndef IPS4O_BLOCK_BYTES
 #define IPS4O_BLOCK_BYTES 512
@@ -141,8 +153,8 @@ struct LevelArgs {
     u32* dblk;        // [T][257] delimiters d_i (block index, rounded up)
     u32* nfb;         // [T][256] full blocks of bucket i
     u32* mov;         // [T][257] prefix of Appendix-A moves over buckets
-    u64* wr;          // [T][256] packed (w:32 | r+RBIAS:32) block pointers
-    u32* readers;     // [T][256]
+    u64* wr;          // [T][256] control lines: word 0 packed (w:32 | r+RBIAS:32) block
+                      // pointers, word 1 (low half) the bucket's reader count
     u32* done;        // [T][8]   bucket has no unprocessed block left
     u32* tdone;       // [T/32]   task has no unprocessed block left
     u32* cflag;       // [T][256] cleanup: overhang saved
@@ -160,6 +172,11 @@ struct LevelArgs {
 };
 
 // ---------------------------------------------------------------- device helpers
+
+__device__ __forceinline__ u64* ctl_wr(u64* wr, u64 t, u32 b) { return wr + (t * MAXK + b) * CTL_STRIDE; }
+__device__ __forceinline__ u32* ctl_readers(u64* wr, u64 t, u32 b) {
+    return reinterpret_cast<u32*>(ctl_wr(wr, t, b) + 1);
+}
 
 __device__ __forceinline__ u32 lanemask_lt() {
     u32 r;
@@ -268,6 +285,22 @@ __device__ __forceinline__ u32 ld_acquire_u32(const u32* p) {
 }
 __device__ __forceinline__ void st_release_u32(u32* p, u32 v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// scoped atomics for the permutation's pointer / reader protocol
+__device__ __forceinline__ u64 atom_add_acqrel_u64(u64* p, u64 v) {
+    u64 old;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void red_add_release_u32(u32* p, u32 v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ u32 atom_add_acquire_u32(u32* p, u32 v) {
+    u32 old;
+    asm volatile("atom.acquire.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
 }
 
 __host__ __device__ __forceinline__ u64 mix64(u64 z) {

@@ -118,7 +118,7 @@ static size_t fixed_bytes() {
     add((size_t)MAXT * MAXK * 4 * 3);          // nfb, readers, cflag
     add((size_t)MAXT * (MAXK / 32) * 4);       // done
     add(MAXT / 32 * 4);                        // tdone
-    add((size_t)MAXT * MAXK * 8);              // wr
+    add((size_t)MAXT * MAXK * 8 * CTL_STRIDE);  // wr control lines
     add((size_t)MAXT * BLOCK_BYTES);           // ovf
     add(MAXT * 4);                             // ovf_owner
     add((size_t)QCAP * sizeof(TaskDesc) * (1 + NUM_BASE_CLASSES));  // queues
@@ -192,7 +192,7 @@ static int ensure_ws(u64 n, int esize) {
     g_ws.cflag = g_ws.readers + (size_t)MAXT * MAXK;
     g_ws.done = (u32*)take((size_t)MAXT * (MAXK / 32) * 4);
     g_ws.tdone = (u32*)take(MAXT / 32 * 4);
-    g_ws.wr = (u64*)take((size_t)MAXT * MAXK * 8);
+    g_ws.wr = (u64*)take((size_t)MAXT * MAXK * 8 * CTL_STRIDE);
     g_ws.ovf = take((size_t)MAXT * BLOCK_BYTES);
     g_ws.ovf_owner = (int*)take(MAXT * 4);
     char* q = take((size_t)QCAP * sizeof(TaskDesc) * (1 + NUM_BASE_CLASSES));
@@ -368,7 +368,6 @@ static LevelArgs level_args(void* data, u32 T, u32 S, int emit, u64 seed) {
     A.nfb = g_ws.nfb;
     A.mov = g_ws.mov;
     A.wr = g_ws.wr;
-    A.readers = g_ws.readers;
     A.done = g_ws.done;
     A.tdone = g_ws.tdone;
     A.cflag = g_ws.cflag;
@@ -485,7 +484,34 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
         memcpy(g_ws.h_tdone, tw, nwd * 4);
         CK(cudaMemcpyAsync(g_ws.tdone, g_ws.h_tdone, nwd * 4, cudaMemcpyHostToDevice, st));
     }
+#ifdef IPS4O_K3_TIMELINE
+    {
+        static unsigned int zero[4096];
+        unsigned long long t0 = 0;
+        cudaStreamSynchronize(st);
+        cudaMemcpyToSymbol(g_k3_hist, zero, sizeof zero);
+        // a timestamp slightly after the launch: the kernel's first events define t0 instead
+        LAUNCH(KK_OTHER, (k_timer_start<<<1, 1, 0, st>>>()));
+        (void)t0;
+    }
+#endif
     LAUNCH(KK_PERMUTE, (k_permute<TR><<<g_ws.k3_blocks, K3_THREADS, 0, st>>>(A)));
+#ifdef IPS4O_K3_TIMELINE
+    {
+        static unsigned int h[4096];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_k3_hist, sizeof h);
+        unsigned long long tp = 0, tt = 0;
+        int last = 0;
+        for (int i = 0; i < 2048; ++i) { tp += h[i]; tt += h[2048 + i]; if (h[i] || h[2048 + i]) last = i; }
+        fprintf(stderr, "K3 timeline T=%u: placements %llu takes %llu, last bin %d us\n", T, tp, tt, last);
+        for (int i = 0; i <= last; i += (last > 40 ? last / 40 : 1)) {
+            unsigned long long a = 0, b = 0;
+            for (int j = i; j < i + (last > 40 ? last / 40 : 1) && j <= last; ++j) { a += h[j]; b += h[2048 + j]; }
+            fprintf(stderr, "  t=%4d us  place %8llu  take %8llu\n", i, a, b);
+        }
+    }
+#endif
     LAUNCH(KK_CLEANUP, (k_cleanup<TR><<<T * MAXK, K4_THREADS, 0, st>>>(A)));
     CK(cudaMemcpyAsync(g_ws.h_ctr, g_ws.ctr, CTR_N * 4 + 16, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

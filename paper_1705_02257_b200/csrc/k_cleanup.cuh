@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
     const u32* dbl = A.dblk + (u64)t * (MAXK + 1);
     const u64 e0 = bnd[b], e1 = bnd[b + 1];
     const u32 d = dbl[b];
-    const u32 wfin = (u32)(A.wr[(u64)t * MAXK + b] >> 32);
+    const u32 wfin = (u32)(*ctl_wr(A.wr, t, b) >> 32);
     const bool own_ovf = A.ovf_owner[t] == (int)b;
     const u64 db_el = tp.g + (u64)d * B;
     const u64 in_end = own_ovf ? tp.g + (u64)(tp.nblocks - 1) * B : tp.g + (u64)wfin * B;

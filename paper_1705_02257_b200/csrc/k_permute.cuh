@@ -84,8 +84,8 @@ __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
     A.mov[(u64)t * (MAXK + 1) + b] = woff + incl - moves;
     if (b == MAXK - 1) A.mov[(u64)t * (MAXK + 1) + MAXK] = woff + incl;
     // w_i = d_i, r_i = d_i + nf_i - 1 (block indices; r biased)
-    A.wr[(u64)t * MAXK + b] = ((u64)d << 32) | (u64)(u32)(d + nf - 1u + RBIAS);
-    A.readers[(u64)t * MAXK + b] = 0;
+    *ctl_wr(A.wr, t, b) = ((u64)d << 32) | (u64)(u32)(d + nf - 1u + RBIAS);
+    *ctl_readers(A.wr, t, b) = 0;
     A.cflag[(u64)t * MAXK + b] = 0;
     const u32 dn_bit = (b >= tp.K || nf == 0) ? 1u : 0u;
     const u32 bal = __ballot_sync(0xffffffffu, dn_bit);
@@ -163,12 +163,24 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
 
 // ------------------------------------------------------------------ permutation
 
-// destination bucket of a block: classify its first element (warp-collective key fetch,
-// the classification itself by every lane on the same value)
-template <class TR>
-__device__ __forceinline__ u32 block_dest(const BlockRegs& r, const u64* tree, const u64* spl,
-                                          u32 logk, u32 kprime, u32 eq, u32 part) {
-    return classify_key(BlockIO<TR>::first_key(r, part), tree, spl, logk, kprime, eq);
+// Warp-cooperative classification of one key held by every lane (the first element of a
+// block): the number of padded splitters <= key.  That count is exactly the leaf the
+// branchless descent of PAPER.md:138-142 reaches (j <- 2j + [a_j <= e] over a complete BST
+// of the sorted splitters computes this rank; ties go right), found here with
+// two ballots over groups of 8 splitters instead of 8 dependent lookups by every lane.
+// slot[p] = s_{p+1} (p < nsl = k'-1, padded); glast = slot[8*lane+7] when valid.  With
+// equality buckets one more comparison against the lower splitter.
+__device__ __forceinline__ u32 warp_classify(u64 key, const u64* slot, u32 nsl, u32 eq, u32 lane,
+                                             u64 glast, bool gok) {
+    const u32 c1 = __popc(__ballot_sync(0xffffffffu, gok && key >= glast));
+    const u32 p = 8 * c1 + (lane & 7u);
+    const bool ok = lane < 8u && p < nsl && key >= slot[p < nsl ? p : 0u];
+    const u32 i = 8 * c1 + __popc(__ballot_sync(0xffffffffu, ok));
+    if (eq) {
+        const bool isq = i >= 1u && slot[i >= 1u ? i - 1u : 0u] >= key;
+        return 2 * i - (isq ? 1u : 0u);
+    }
+    return i;
 }
 
 // next bucket (cyclic over nwords*32 buckets, starting at gb inclusive) whose bit in
@@ -196,14 +208,63 @@ __device__ __forceinline__ u32 next_clear_bit(const u32* bits, u32 nwords, u32 g
     return 0xFFFFFFFFu;
 }
 
-// Block permutation.  Each CTA works on one task at a time (its classifier in shared
-// memory), starting from a task chosen by its index so that CTAs spread over the tasks;
-// when the task has no unprocessed block left it moves to the next unfinished task.
+// first not-done bucket at or after b (cyclic over K buckets); ~0u if every bucket is done.
+// Serial scan by one lane over the task's done words (rare: once per exhausted bucket).
+__device__ __forceinline__ u32 next_open_bucket(const u32* done, u32 b, u32 K) {
+    const u32 nw = (K + 31) / 32;
+    for (u32 i = 0; i <= nw; ++i) {
+        const u32 wi = ((b >> 5) + i) % nw;
+        u32 word = *(volatile const u32*)(done + wi);
+        if (i == 0) word |= (1u << (b & 31)) - 1u;             // bits >= b in the first word
+        if (i == nw) word |= ~((1u << (b & 31)) - 1u);         // wrap-around: bits < b
+        if (wi == nw - 1 && (K & 31)) word |= ~((1u << (K & 31)) - 1u);
+        if (word != 0xFFFFFFFFu) return wi * 32 + (__ffs(~word) - 1);
+    }
+    return 0xFFFFFFFFu;
+}
+
+// Block permutation.  Each CTA works on one task at a time (its
+// splitters in shared memory) and moves on to the next unfinished task when none of the
+// task's buckets has an unprocessed block left.  Each warp runs K3_SLOTS independent
+// chains (the paper's threads) in lock step, so that their atomic round trips and block
+// loads overlap: lane c performs the pointer atomics of chain c, all 32 lanes move the
+// blocks (16 B per lane of a 512-B block), and each chain's swap buffer lives in registers.
+// Per round:
+//   (a) chains without a block take one from their primary bucket: readers++ (release),
+//       then r <- r-1 on the packed (w, r) word; a failed take (r < w) marks the bucket
+//       done and the chain moves to the next open bucket;
+//   (b) every held block is classified by its first element; w_dest <- w_dest+1;
+//       if the old w <= old r the target is an unprocessed block: read it, and unless it
+//       already belongs to dest (skip) write ours there and carry it on;
+//       otherwise the target is empty: wait for the bucket's readers at the crossing
+//       (PAPER.md:298-302), write (or use the overflow block past the end,
+//       PAPER.md:220-221) and the chain is free again.
+#ifdef IPS4O_K3_TIMELINE
+__device__ unsigned int g_k3_hist[4096];
+__device__ unsigned long long g_k3_t0;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__global__ void k_timer_start() { g_k3_t0 = gtimer(); }
+#define K3_TL_EVENT(kind)                                                                      \
+    do {                                                                                       \
+        const unsigned long long dt_ = (gtimer() - g_k3_t0) / 1000ull;                         \
+        atomicAdd(&g_k3_hist[(kind) * 2048 + (dt_ < 2047 ? dt_ : 2047)], 1u);                   \
+    } while (0)
+#else
+#define K3_TL_EVENT(kind) do {} while (0)
+#endif
+
 template <class TR>
-__global__ void __launch_bounds__(K3_THREADS, 8) k_permute(LevelArgs A) {
+__global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A) {
     constexpr int B = TR::B;
     constexpr u32 BB = B * TR::S;  // block bytes
-    __shared__ u64 s_tree[MAXK], s_spl[MAXK];
+    constexpr int C = K3_SLOTS;
+    constexpr u32 CM = (1u << C) - 1u;
+    __shared__ u64 s_spl[MAXK];
+    __shared__ u32 s_next;
     const u32 tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
     const u32 nw = blockDim.x >> 5;
     const u32 T = A.ntasks;
@@ -215,85 +276,144 @@ __global__ void __launch_bounds__(K3_THREADS, 8) k_permute(LevelArgs A) {
         // next unfinished task (cyclic from t); exit when every task is finished
         if (tid < 32) {
             const u32 nt = next_clear_bit(A.tdone, tnwords, t, lane);
-            if (lane == 0) s_tree[0] = nt;  // slot 0 of the tree is unused: borrow it
+            if (lane == 0) s_next = nt;
         }
         __syncthreads();
-        const u32 nt = (u32)s_tree[0];
-        __syncthreads();
+        const u32 nt = s_next;
         if (nt == 0xFFFFFFFFu || nt >= T) return;
         t = nt;
-        if (tid < (u32)MAXK) {
-            s_tree[tid] = A.tree[(u64)t * MAXK + tid];
-            s_spl[tid] = A.spl[(u64)t * MAXK + tid];
-        }
+        if (tid < (u32)MAXK) s_spl[tid] = A.spl[(u64)t * MAXK + tid];
         __syncthreads();
         const TaskParam tp = A.tp[t];
-        const u32* done = A.done + (u64)t * (MAXK / 32);
+        u32* done = A.done + (u64)t * (MAXK / 32);
         char* tbase = data + tp.g * TR::S;
-        // primary buckets spread over the task's buckets
-        u32 b = (u32)(((u64)blockIdx.x * nw + wi) * 97u % tp.K);
+        const u64* slot = s_spl + 1;
+        const u32 nsl = tp.kprime - 1u;
+        const bool gok = 8 * lane + 7 < nsl;
+        const u64 glast = gok ? slot[8 * lane + 7] : 0ull;
+
+        // per-chain scalars live in lane c (c < C); block registers in every lane
+        u32 my_pb = (u32)((((u64)blockIdx.x * nw + wi) * C + lane) * 97u % tp.K);
+        bool my_alive = lane < (u32)C;
+        u32 my_dest = 0;
+        u32 held = 0;  // warp-uniform: chains holding a block (classified, my_dest valid)
+        BlockRegs cur[C];
 
         for (;;) {
-            // ---- take an unprocessed block from the primary bucket (r <- r-1)
-            b = next_clear_bit(done, MAXK / 32, b, lane);
-            if (b == 0xFFFFFFFFu) break;
-            const u32 gb = t * MAXK + b;
-            int blk = 0, ok = 0;
-            if (lane == 0) {
-                atomicAdd(&A.readers[gb], 1u);
-                __threadfence();
-                const u64 old = atomicAdd((unsigned long long*)&A.wr[gb], ~0ull);  // r -= 1
-                const int ow = (int)(u32)(old >> 32);
-                const int orr = (int)((u32)old - RBIAS);
-                if (orr < ow) {
-                    atomicSub(&A.readers[gb], 1u);
-                    atomicOr(&A.done[(u64)t * (MAXK / 32) + (b >> 5)], 1u << (b & 31));
+            // ---- 1. one pointer atomic per chain: free chains take (r <- r-1 on their
+            //         primary bucket, after announcing themselves as readers), chains with a
+            //         block claim their destination slot (w <- w+1)
+            const bool my_held = lane < (u32)C && ((held >> lane) & 1u);
+            bool my_take = my_alive && !my_held;
+            if (my_take) {
+                const u32 b = next_open_bucket(done, my_pb, tp.K);
+                if (b == 0xFFFFFFFFu) {
+                    my_alive = false;
+                    my_take = false;
                 } else {
-                    ok = 1;
-                    blk = orr;
+                    my_pb = b;
                 }
             }
-            ok = __shfl_sync(0xffffffffu, ok, 0);
-            if (!ok) continue;
-            blk = __shfl_sync(0xffffffffu, blk, 0);
-            BlockRegs cur = BlockIO<TR>::load(tbase + (u64)blk * BB, lane);
-            __threadfence();
-            __syncwarp();
-            if (lane == 0) atomicSub(&A.readers[gb], 1u);
-            // ---- chain: place the block, swapping with unprocessed blocks on the way
-            for (;;) {
-                const u32 dest = block_dest<TR>(cur, s_tree, s_spl, tp.logk, tp.kprime, tp.eq, tp.part);
-                const u32 gbd = t * MAXK + dest;
-                u64 old = 0;
-                if (lane == 0) old = atomicAdd((unsigned long long*)&A.wr[gbd], 1ull << 32);  // w += 1
-                old = __shfl_sync(0xffffffffu, old, 0);
-                const int ow = (int)(u32)(old >> 32);
-                const int orr = (int)((u32)old - RBIAS);
-                if (ow <= orr) {
-                    // case 1: w_dest points to an unprocessed block -> swap
-                    const BlockRegs oth = BlockIO<TR>::load(tbase + (u64)ow * BB, lane);
-                    const u32 od = block_dest<TR>(oth, s_tree, s_spl, tp.logk, tp.kprime, tp.eq, tp.part);
-                    if (od == dest) continue;  // already in place: skip it
-                    BlockIO<TR>::store(tbase + (u64)ow * BB, lane, cur);
-                    cur = oth;
+            u64 my_old = 0;
+            if (my_take || my_held) {
+                u64 op = 1ull << 32;
+                u64* wp = ctl_wr(A.wr, t, my_dest);
+                if (my_take) {
+                    // the reader announcement is performed before the take (acquire: no later
+                    // memory operation of this thread is performed before it)
+                    atom_add_acquire_u32(ctl_readers(A.wr, t, my_pb), 1u);
+                    op = ~0ull;
+                    wp = ctl_wr(A.wr, t, my_pb);
+                }
+                my_old = atomicAdd((unsigned long long*)wp, op);
+            }
+            const int my_ow = (int)(u32)(my_old >> 32);
+            const int my_orr = (int)((u32)my_old - RBIAS);
+            if (my_held) K3_TL_EVENT(0);   // a placement attempt (1 us bins)
+            if (my_take) K3_TL_EVENT(1);   // a take attempt
+            // 2. decode: source block of this round's load (taken block / swap target)
+            int my_src = -1;
+            bool my_write = false;
+            if (my_take) {
+                if (my_orr < my_ow) {  // nothing left to take in this bucket
+                    atomicSub(ctl_readers(A.wr, t, my_pb), 1u);
+                    atomicOr(&done[my_pb >> 5], 1u << (my_pb & 31));
                 } else {
-                    // case 2: w_dest points to an empty block -> wait for readers, write, refill
-                    if (lane == 0) {
-                        while (*(volatile u32*)&A.readers[gbd] != 0u) __nanosleep(64);
-                        __threadfence();
+                    my_src = my_orr;
+                }
+            } else if (my_held) {
+                if (my_ow <= my_orr) my_src = my_ow;  // unprocessed block at w: swap
+                else my_write = true;                 // empty block at w: write
+            }
+            const u32 ld = __ballot_sync(0xffffffffu, my_src >= 0) & CM;
+            const u32 wrt = __ballot_sync(0xffffffffu, my_write) & CM;
+            const u32 tk = __ballot_sync(0xffffffffu, my_take && my_src >= 0) & CM;
+            const u32 alive = __ballot_sync(0xffffffffu, my_alive) & CM;
+            if (!ld && !wrt && !held) {
+                if (!alive) break;
+                continue;
+            }
+            // 3. all block loads of the round in flight together
+            BlockRegs nxt[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int src = __shfl_sync(0xffffffffu, my_src, c);
+                if ((ld >> c) & 1u) nxt[c] = BlockIO<TR>::load(tbase + (u64)src * BB, lane);
+            }
+            // 4. taken blocks: release the readers once every lane's read has completed (before
+            //    any wait below: a chain of this warp may be the reader another one waits for)
+            if (tk) {
+                u32 x = 0;
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    if ((tk >> c) & 1u) x |= nxt[c].w[0] | nxt[c].w[1] | nxt[c].w[2] | nxt[c].w[3];
+                if (__any_sync(0xffffffffu, x == 0x9E3779B9u)) __nanosleep(0);  // forces the loads
+                if (my_take && my_src >= 0) atomicSub(ctl_readers(A.wr, t, my_pb), 1u);
+            }
+            // 5. writes into empty blocks: wait for the bucket's readers at the crossing
+            //    (PAPER.md:298-302), then write (past the end: the overflow block)
+            if (wrt) {
+                if (my_write) {
+                    while (*(volatile u32*)ctl_readers(A.wr, t, my_dest) != 0u) __nanosleep(64);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const int ow = __shfl_sync(0xffffffffu, my_ow, c);
+                    const u32 dc = __shfl_sync(0xffffffffu, my_dest, c);
+                    if ((wrt >> c) & 1u) {
+                        if (tp.g + (u64)(ow + 1) * B > tp.hi) {
+                            char* ob = reinterpret_cast<char*>(A.ovf) + (u64)t * BB;
+                            BlockIO<TR>::store(ob, lane, cur[c]);
+                            if (lane == 0) A.ovf_owner[t] = (int)dc;
+                        } else {
+                            BlockIO<TR>::store(tbase + (u64)ow * BB, lane, cur[c]);
+                        }
                     }
-                    __syncwarp();
-                    if (tp.g + (u64)(ow + 1) * B > tp.hi) {
-                        // the block would reach past the task end: overflow block
-                        char* ob = reinterpret_cast<char*>(A.ovf) + (u64)t * BB;
-                        BlockIO<TR>::store(ob, lane, cur);
-                        if (lane == 0) A.ovf_owner[t] = (int)dest;
-                    } else {
-                        BlockIO<TR>::store(tbase + (u64)ow * BB, lane, cur);
+                }
+                held &= ~wrt;
+            }
+            // 6. consume the loads: taken blocks become held; swap targets are classified -- already in
+            //    place: skip, else ours is written there and we carry on
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                if (!((ld >> c) & 1u)) continue;
+                const u32 d = warp_classify(BlockIO<TR>::first_key(nxt[c], tp.part), slot, nsl, tp.eq, lane,
+                                            glast, gok);
+                if ((tk >> c) & 1u) {
+                    cur[c] = nxt[c];
+                    if (lane == (u32)c) my_dest = d;
+                } else {
+                    const u32 dc = __shfl_sync(0xffffffffu, my_dest, c);
+                    if (d != dc) {
+                        const int ow = __shfl_sync(0xffffffffu, my_ow, c);
+                        BlockIO<TR>::store(tbase + (u64)ow * BB, lane, cur[c]);
+                        cur[c] = nxt[c];
+                        if (lane == (u32)c) my_dest = d;
                     }
-                    break;
                 }
             }
+            held |= tk;
         }
         __syncthreads();
         if (tid == 0) atomicOr(&A.tdone[t >> 5], 1u << (t & 31));
