@@ -11,10 +11,9 @@ typedef unsigned int u32;
 
 constexpr int MAXK = 256;            // buckets per step: k = 256, or 2k'-1 <= 255 with eq
 constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer
-// Each bucket's permutation control word (packed (w, r), then its reader count) sits in its
-// own 256-byte line, so that the pointer atomics of the k buckets spread over the L2
-// slices instead of sharing the few slices a dense array maps to.
-constexpr int CTL_STRIDE = 32;       // u64 words per bucket control line (256 B)
+// Each bucket's permutation control pair: the packed (w, r) word, then its reader count.
+// (Spreading the pairs over 256-byte lines -- one L2 slice each -- measured no faster.)
+constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
 constexpr u32 INV_BUCKET = 0xFFFFu;  // "no element" marker in classification registers
 constexpr int K3_THREADS = 256;      // block permutation CTA
 #ifndef IPS4O_K3_SLOTS

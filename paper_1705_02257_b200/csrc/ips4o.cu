@@ -70,7 +70,7 @@ struct Workspace {
     u32 *s_count, *s_fill, *s_spoff, *s_nfull, *prefF, *prefE;
     u64* s_spbase;
     u64* bnd;
-    u32 *dblk, *nfb, *mov, *readers, *done, *cflag, *tdone;
+    u32 *dblk, *nfb, *mov, *done, *cflag, *tdone;
     u64* wr;
     void* ovf;
     int* ovf_owner;
@@ -115,7 +115,7 @@ static size_t fixed_bytes() {
     add(MAXS * 8 + MAXS * 4 * 3);              // s_spbase, s_nfull, prefF, prefE
     add((size_t)MAXT * (MAXK + 1) * 8);        // bnd
     add((size_t)MAXT * (MAXK + 1) * 4 * 2);    // dblk, mov
-    add((size_t)MAXT * MAXK * 4 * 3);          // nfb, readers, cflag
+    add((size_t)MAXT * MAXK * 4 * 2);          // nfb, cflag
     add((size_t)MAXT * (MAXK / 32) * 4);       // done
     add(MAXT / 32 * 4);                        // tdone
     add((size_t)MAXT * MAXK * 8 * CTL_STRIDE);  // wr control lines
@@ -186,10 +186,9 @@ static int ensure_ws(u64 n, int esize) {
     char* dm = take((size_t)MAXT * (MAXK + 1) * 4 * 2);
     g_ws.dblk = (u32*)dm;
     g_ws.mov = g_ws.dblk + (size_t)MAXT * (MAXK + 1);
-    char* nr = take((size_t)MAXT * MAXK * 4 * 3);
+    char* nr = take((size_t)MAXT * MAXK * 4 * 2);
     g_ws.nfb = (u32*)nr;
-    g_ws.readers = g_ws.nfb + (size_t)MAXT * MAXK;
-    g_ws.cflag = g_ws.readers + (size_t)MAXT * MAXK;
+    g_ws.cflag = g_ws.nfb + (size_t)MAXT * MAXK;
     g_ws.done = (u32*)take((size_t)MAXT * (MAXK / 32) * 4);
     g_ws.tdone = (u32*)take(MAXT / 32 * 4);
     g_ws.wr = (u64*)take((size_t)MAXT * MAXK * 8 * CTL_STRIDE);
