@@ -14,6 +14,8 @@ constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer (SURVEY 
 // Each bucket's permutation control pair: the packed (w, r) word, then its reader count.
 // (Spreading the pairs over 256-byte lines -- one L2 slice each -- measured no faster.)
 constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
+constexpr int TREE_COPIES = 16;      // replicated splitter tree in K2 (one copy per half-warp lane)
+constexpr u32 TREE_NODE_BYTES = 8 * TREE_COPIES;
 constexpr u32 INV_BUCKET = 0xFFFFu;  // "no element" marker in classification registers
 constexpr int K3_THREADS = 256;      // block permutation CTA
 #ifndef IPS4O_K3_SLOTS

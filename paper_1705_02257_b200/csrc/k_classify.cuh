@@ -28,7 +28,8 @@ struct K2Smem {
     static constexpr size_t wcnt_bytes = (size_t)NW * MAXK * 2;
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
     static constexpr size_t arr_bytes = 4 * MAXK * 4;
-    static constexpr size_t total = buf_bytes + wcnt_bytes + tree_bytes + arr_bytes;
+    static constexpr size_t rtree_bytes = (size_t)MAXK * TREE_COPIES * 8;
+    static constexpr size_t total = buf_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes;
 };
 
 // Loads one tile (<= NT*E elements from tb, len valid) into raw 16-byte registers; bit e of
@@ -95,43 +96,63 @@ __device__ __forceinline__ void k2_classify(const typename TR::V (&v)[E], u32 va
     k2_classify_keys<E, LOGK>(key, valid, full, tree, spl, logk, kprime, eq, bk, peers);
 }
 
+// One level of the branchless descent for one key: node = a[j];
+// p = [node <= key]; j <- 2j + p (as a byte offset in this lane's tree copy:
+// a <- 2a + (p ? t1 : t0)), and the ballot of p refines the key's peer mask.  Written in
+// PTX so that the comparison is evaluated once and feeds the ballot, the mask update and
+// the index update (8 SASS instructions per level and key).
+__device__ __forceinline__ void descend_step(u64 key, u32 sbase, u32& a, u32& peers, u32 t0, u32 t1) {
+    asm("{\n\t"
+        ".reg .pred p;\n\t"
+        ".reg .b32 x, m, t, ad;\n\t"
+        ".reg .b64 nd;\n\t"
+        "add.u32 ad, %2, %0;\n\t"
+        "ld.shared.u64 nd, [ad];\n\t"
+        "setp.ge.u64 p, %3, nd;\n\t"
+        "vote.sync.ballot.b32 x, p, 0xffffffff;\n\t"
+        "selp.b32 m, 0, 0xffffffff, p;\n\t"
+        "xor.b32 x, x, m;\n\t"
+        "and.b32 %1, %1, x;\n\t"
+        "selp.b32 t, %5, %4, p;\n\t"
+        "mad.lo.u32 %0, %0, 2, t;\n\t"
+        "}"
+        : "+r"(a), "+r"(peers)
+        : "r"(sbase), "l"(key), "r"(t0), "r"(t1));
+}
+
 template <int E, int LOGK>
 __device__ __forceinline__ void k2_classify_keys(const u64 (&key)[E], u32 valid, bool full,
                                                  const u64* tree, const u64* spl, u32 logk,
                                                  u32 kprime, u32 eq, u32 (&bk)[E], u32 (&peers)[E]) {
-    u32 a[E];  // byte offset 8*j of the current tree node
-    const u64 root = tree[1];
+    // tree: the replicated layout of rtree_fill (node j of copy c at byte 128*j + 8*c); lane
+    // l reads copy l % 16, so the 16 lanes of a half-warp never share a bank pair: every
+    // lookup is one conflict-free 64-bit load whatever nodes the keys lead to.
+    u32 a[E];  // byte offset of the current node in this lane's copy
+    const u32 cofs = (threadIdx.x & (TREE_COPIES - 1)) * 8u;
+    const u32 t0 = 0u - cofs, t1 = TREE_NODE_BYTES - cofs;  // a' = 2a + (p ? t1 : t0)
+    const u64 root = tree[cofs / 8 + TREE_COPIES];           // node 1 (any copy)
     const char* tb = reinterpret_cast<const char*>(tree);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         const bool p = key[e] >= root;  // level 0 from a register: j = 2 + [root <= e]
         const u32 x = __ballot_sync(0xffffffffu, p);
         peers[e] = p ? x : ~x;
-        a[e] = p ? 24u : 16u;
+        a[e] = (p ? 3u : 2u) * TREE_NODE_BYTES + cofs;
     }
+    const u32 sb = (u32)__cvta_generic_to_shared(tb);
     if (LOGK == 8) {
 #pragma unroll
         for (int l = 1; l < 8; ++l)
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const bool p = key[e] >= *reinterpret_cast<const u64*>(tb + a[e]);
-                const u32 x = __ballot_sync(0xffffffffu, p);
-                peers[e] &= p ? x : ~x;
-                a[e] = (a[e] << 1) + (p ? 8u : 0u);
-            }
+            for (int e = 0; e < E; ++e) descend_step(key[e], sb, a[e], peers[e], t0, t1);
     } else {
         for (u32 l = 1; l < logk; ++l)
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const bool p = key[e] >= *reinterpret_cast<const u64*>(tb + a[e]);
-                const u32 x = __ballot_sync(0xffffffffu, p);
-                peers[e] &= p ? x : ~x;
-                a[e] = (a[e] << 1) + (p ? 8u : 0u);
-            }
+            for (int e = 0; e < E; ++e) descend_step(key[e], sb, a[e], peers[e], t0, t1);
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        u32 i = (a[e] >> 3) - kprime;
+        u32 i = (a[e] - cofs) / TREE_NODE_BYTES - kprime;
         if (eq) {
             const u32 ii = i ? i : 1u;
             const bool isq = i >= 1u && spl[ii] >= key[e];
@@ -146,6 +167,12 @@ __device__ __forceinline__ void k2_classify_keys(const u64 (&key)[E], u32 valid,
         }
         bk[e] = ok ? i : INV_BUCKET;
     }
+}
+
+// Fill the replicated tree (TREE_COPIES interleaved copies of the 256-node BFS array) from
+// the task's tree in global memory.  Block-wide; the caller synchronises.
+__device__ __forceinline__ void rtree_fill(u64* rtree, const u64* gtree, u32 tid, u32 nthreads) {
+    for (u32 i = tid; i < (u32)MAXK * TREE_COPIES; i += nthreads) rtree[i] = gtree[i / TREE_COPIES];
 }
 
 template <class TR, int NT, int E, int LOGK>
@@ -267,6 +294,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
     u32* cnt = fill + MAXK;
     u32* slotb = cnt + MAXK;
     u32* nfl = slotb + MAXK;
+    u64* rtree = reinterpret_cast<u64*>(smem + SM::buf_bytes + SM::wcnt_bytes + SM::tree_bytes + SM::arr_bytes);
     __shared__ u32 s_stripe, s_nflushed, s_wsum[NT / 32];
     __shared__ u64 s_spbase;
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -290,6 +318,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
 #pragma unroll
             for (int ww = 0; ww < NT / 32; ++ww) wcnt[ww * MAXK + tid] = 0;
         }
+        rtree_fill(rtree, A.tree + (u64)sd.task * MAXK, tid, NT);
         if (tid == 0) s_nflushed = 0;
         __syncthreads();
         const u64 mb = sd.begin > tp.g ? sd.begin : tp.g;  // stripe main region start (block aligned)
@@ -306,10 +335,10 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
                 const u64 tb = mb + ti * TILE;
                 if (ti + 1 < nft) k2_load_full<TR, NT, E>(data, tb + TILE, nxt);
                 if (tp.logk == 8)
-                    k2_tile<TR, NT, E, 8>(data, cur, ALL, false, mb, cap, buf, wcnt, tree, spl, fill, cnt,
+                    k2_tile<TR, NT, E, 8>(data, cur, ALL, false, mb, cap, buf, wcnt, rtree, spl, fill, cnt,
                                           slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
                 else
-                    k2_tile<TR, NT, E, 0>(data, cur, ALL, false, mb, cap, buf, wcnt, tree, spl, fill, cnt,
+                    k2_tile<TR, NT, E, 0>(data, cur, ALL, false, mb, cap, buf, wcnt, rtree, spl, fill, cnt,
                                           slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
 #pragma unroll
                 for (int e = 0; e < E / TR::VEC; ++e) cur[e] = nxt[e];
@@ -317,7 +346,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             const u64 tb = mb + nft * TILE;
             if (tb < me) {
                 const u32 vt = k2_load<TR, NT, E>(data, tb, (u32)(me - tb), cur);
-                k2_tile<TR, NT, E, 0>(data, cur, vt, false, mb, cap, buf, wcnt, tree, spl, fill, cnt,
+                k2_tile<TR, NT, E, 0>(data, cur, vt, false, mb, cap, buf, wcnt, rtree, spl, fill, cnt,
                                       slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
             }
         }
@@ -327,7 +356,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             const u64 hend = tp.g < tp.hi ? tp.g : tp.hi;
             uint4 hv[E / TR::VEC];
             const u32 hval = k2_load<TR, NT, E>(data, tp.lo, (u32)(hend - tp.lo), hv);
-            k2_tile<TR, NT, E, 0>(data, hv, hval, true, mb, cap, buf, wcnt, tree, spl, fill, cnt, slotb, nfl,
+            k2_tile<TR, NT, E, 0>(data, hv, hval, true, mb, cap, buf, wcnt, rtree, spl, fill, cnt, slotb, nfl,
                            &s_nflushed, tp.logk, tp.kprime, tp.eq);
         }
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area

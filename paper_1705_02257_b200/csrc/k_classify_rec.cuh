@@ -20,7 +20,8 @@ struct K2RecSmem {
     static constexpr size_t wcnt_bytes = (size_t)NW * MAXK * 2;
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
     static constexpr size_t arr_bytes = 4 * MAXK * 4;
-    static constexpr size_t total = buf_bytes + stage_bytes + wcnt_bytes + tree_bytes + arr_bytes;
+    static constexpr size_t rtree_bytes = (size_t)MAXK * TREE_COPIES * 8;
+    static constexpr size_t total = buf_bytes + stage_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes;
 };
 
 __device__ __forceinline__ void copy_rec(u32* dst, const u32* src) {
@@ -44,6 +45,8 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
     u32* cnt = fill + MAXK;
     u32* slotb = cnt + MAXK;
     u32* nfl = slotb + MAXK;
+    u64* rtree = reinterpret_cast<u64*>(smem + SM::buf_bytes + SM::stage_bytes + SM::wcnt_bytes + SM::tree_bytes +
+                                        SM::arr_bytes);
     __shared__ u32 s_stripe, s_nflushed, s_wsum[NW];
     __shared__ u64 s_spbase;
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -66,6 +69,7 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
             cnt[b] = 0;
             for (int ww = 0; ww < NW; ++ww) wcnt[ww * MAXK + b] = 0;
         }
+        rtree_fill(rtree, A.tree + (u64)sd.task * MAXK, tid, NT);
         if (tid == 0) s_nflushed = 0;
         __syncthreads();
         const u64 mb = sd.begin, me = sd.end;  // g == lo for records: no head region
@@ -82,9 +86,9 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
             u32 bk[1], peers[1];
             const bool full = __all_sync(0xffffffffu, valid);
             if (tp.logk == 8)
-                k2_classify_keys<1, 8>(key, valid ? 1u : 0u, full, tree, spl, tp.logk, tp.kprime, tp.eq, bk, peers);
+                k2_classify_keys<1, 8>(key, valid ? 1u : 0u, full, rtree, spl, tp.logk, tp.kprime, tp.eq, bk, peers);
             else
-                k2_classify_keys<1, 0>(key, valid ? 1u : 0u, full, tree, spl, tp.logk, tp.kprime, tp.eq, bk, peers);
+                k2_classify_keys<1, 0>(key, valid ? 1u : 0u, full, rtree, spl, tp.logk, tp.kprime, tp.eq, bk, peers);
             // warp-aggregated ranking
             const u32 b = bk[0];
             const u32 leader = __ffs(peers[0]) - 1;
