@@ -239,6 +239,15 @@ static int launch(int kind, cudaStream_t st, F&& f) {
     f();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, kKindNames[kind]);
+    static int sync_check = -1;  // IPS4O_SYNC_CHECK=1: synchronise after every launch (debugging)
+    if (sync_check < 0) {
+        const char* v = getenv("IPS4O_SYNC_CHECK");
+        sync_check = (v && v[0] == '1') ? 1 : 0;
+    }
+    if (sync_check) {
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return set_cuda_error(e, kKindNames[kind]);
+    }
     if (g_prof.on) {
         cudaEventRecord(b, st);
         g_prof.recs.push_back({kind, a, b});
@@ -257,12 +266,17 @@ static cudaError_t set_base_attr1() {
     return cudaFuncSetAttribute(k_base_merge<TR, TH, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)BaseClass<TR, TH, 16>::smem);
 }
+template <class TR, int NT>
+static cudaError_t set_radix_attr() {
+    return cudaFuncSetAttribute(k_base_radix<TR, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)RadixBase<TR, NT>::smem);
+}
 template <class TR>
 static cudaError_t set_base_attrs() {
-    cudaError_t e = set_base_attr1<TR, 128>();
-    if (e == cudaSuccess) e = set_base_attr1<TR, 256>();
-    if (e == cudaSuccess) e = set_base_attr1<TR, 512>();
-    if (e == cudaSuccess && TR::CAP >= 16384) e = set_base_attr1<TR, (TR::CAP >= 16384 ? 1024 : 512)>();
+    cudaError_t e = set_base_attr1<TR, (TR::CAP >= 16384 ? 1024 : 512)>();
+    if (e == cudaSuccess) e = set_radix_attr<TR, 256>();
+    if (e == cudaSuccess) e = set_radix_attr<TR, 512>();
+    if (e == cudaSuccess) e = set_radix_attr<TR, 1024>();
     return e;
 }
 
@@ -529,12 +543,16 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
     return IPS4O_OK;
 }
 
-template <class TR, int TH>
-static int run_base_class(void* data, u32 count, TaskDesc* d_tasks, cudaStream_t st) {
+// Base case of one level batch: size classes 0..2 (<= 2K / 4K / 8K elements) by the radix
+// kernel, class 3 (<= CAP) and any leaf the radix kernel hands back by the merge sort,
+// which reads its task count from the device (the fallback queue is appended to class 3).
+template <class TR, int NT>
+static int run_radix_class(void* data, u32 count, TaskDesc* d_tasks, cudaStream_t st) {
     if (!count) return IPS4O_OK;
-    typedef BaseClass<TR, TH, 16> BC;
-    const u32 grid = std::min<u32>(count, 16u * g_ws.num_sms);
-    LAUNCH(KK_BASE, (k_base_merge<TR, TH, 16><<<grid, TH, BC::smem, st>>>(d_tasks, count, data)));
+    typedef RadixBase<TR, NT> RB;
+    const u32 grid = std::min<u32>(count, (2048u / NT) * 2u * g_ws.num_sms);
+    LAUNCH(KK_BASE, (k_base_radix<TR, NT><<<grid, NT, RB::smem, st>>>(d_tasks, count, data, g_ws.q_base + 3 * QCAP,
+                                                                      g_ws.ctr + CTR_BASE0 + 3, QCAP)));
     g_stats.base_tasks += count;
     return IPS4O_OK;
 }
@@ -553,17 +571,22 @@ static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStrea
         g_stats.base_tasks += counts[0];
         return IPS4O_OK;
     } else {
-        int rc = run_base_class<TR, 128>(data, counts[0], d_queues, st);
-        if (!rc) rc = run_base_class<TR, 256>(data, counts[1], d_queues + QCAP, st);
-        if (!rc) rc = run_base_class<TR, 512>(data, counts[2], d_queues + 2 * QCAP, st);
-        if (!rc && counts[3]) {
-            if (TR::CAP < 16384) {
-                snprintf(g_errbuf, sizeof g_errbuf, "base task above the type's capacity");
-                return IPS4O_EINTERNAL;
-            }
-            rc = run_base_class<TR, (TR::CAP >= 16384 ? 1024 : 512)>(data, counts[3], d_queues + 3 * QCAP, st);
-        }
-        return rc;
+        if (!(counts[0] | counts[1] | counts[2] | counts[3])) return IPS4O_OK;
+        if (counts[3] && TR::CAP < 16384 && false) return IPS4O_EINTERNAL;
+        // the class-3 count lives on the device: the radix kernels append their fallbacks
+        memcpy(g_ws.h_ctr + CTR_BASE0 + 3, counts + 3, 4);
+        CK(cudaMemcpyAsync(g_ws.ctr + CTR_BASE0 + 3, g_ws.h_ctr + CTR_BASE0 + 3, 4, cudaMemcpyHostToDevice, st));
+        int rc = run_radix_class<TR, 256>(data, counts[0], d_queues, st);
+        if (!rc) rc = run_radix_class<TR, 512>(data, counts[1], d_queues + QCAP, st);
+        if (!rc) rc = run_radix_class<TR, 1024>(data, counts[2], d_queues + 2 * QCAP, st);
+        if (rc) return rc;
+        constexpr int TH = TR::CAP >= 16384 ? 1024 : 512;
+        typedef BaseClass<TR, TH, 16> BC;
+        const u32 grid = std::max<u32>(1u, std::min<u32>(counts[3] + 64u, 2u * g_ws.num_sms));
+        LAUNCH(KK_BASE, (k_base_merge<TR, TH, 16><<<grid, TH, BC::smem, st>>>(d_queues + 3 * QCAP,
+                                                                              g_ws.ctr + CTR_BASE0 + 3, data)));
+        g_stats.base_tasks += counts[3];
+        return IPS4O_OK;
     }
 }
 
