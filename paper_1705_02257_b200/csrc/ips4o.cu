@@ -266,17 +266,17 @@ static cudaError_t set_base_attr1() {
     return cudaFuncSetAttribute(k_base_merge<TR, TH, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)BaseClass<TR, TH, 16>::smem);
 }
-template <class TR, int NT>
-static cudaError_t set_radix_attr() {
-    return cudaFuncSetAttribute(k_base_radix<TR, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)RadixBase<TR, NT>::smem);
+template <class TR, int NT, int E>
+static cudaError_t set_cell_attr() {
+    return cudaFuncSetAttribute(k_base_cell<TR, NT, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)CellBase<TR, NT, E>::smem);
 }
 template <class TR>
 static cudaError_t set_base_attrs() {
     cudaError_t e = set_base_attr1<TR, (TR::CAP >= 16384 ? 1024 : 512)>();
-    if (e == cudaSuccess) e = set_radix_attr<TR, 256>();
-    if (e == cudaSuccess) e = set_radix_attr<TR, 512>();
-    if (e == cudaSuccess) e = set_radix_attr<TR, 1024>();
+    if (e == cudaSuccess) e = set_cell_attr<TR, 256, 8>();
+    if (e == cudaSuccess) e = set_cell_attr<TR, 512, 8>();
+    if (e == cudaSuccess) e = set_cell_attr<TR, 512, 16>();
     return e;
 }
 
@@ -543,16 +543,16 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
     return IPS4O_OK;
 }
 
-// Base case of one level batch: size classes 0..2 (<= 2K / 4K / 8K elements) by the radix
-// kernel, class 3 (<= CAP) and any leaf the radix kernel hands back by the merge sort,
+// Base case of one level batch: size classes 0..2 (<= 2K / 4K / 8K elements) by the cell
+// kernel, class 3 (<= CAP) and any leaf the cell kernel hands back by the merge sort,
 // which reads its task count from the device (the fallback queue is appended to class 3).
-template <class TR, int NT>
-static int run_radix_class(void* data, u32 count, TaskDesc* d_tasks, cudaStream_t st) {
+template <class TR, int NT, int E>
+static int run_cell_class(void* data, u32 count, TaskDesc* d_tasks, cudaStream_t st) {
     if (!count) return IPS4O_OK;
-    typedef RadixBase<TR, NT> RB;
+    typedef CellBase<TR, NT, E> CB;
     const u32 grid = std::min<u32>(count, (2048u / NT) * 2u * g_ws.num_sms);
-    LAUNCH(KK_BASE, (k_base_radix<TR, NT><<<grid, NT, RB::smem, st>>>(d_tasks, count, data, g_ws.q_base + 3 * QCAP,
-                                                                      g_ws.ctr + CTR_BASE0 + 3, QCAP)));
+    LAUNCH(KK_BASE, (k_base_cell<TR, NT, E><<<grid, NT, CB::smem, st>>>(d_tasks, count, data, g_ws.q_base + 3 * QCAP,
+                                                                        g_ws.ctr + CTR_BASE0 + 3, QCAP)));
     g_stats.base_tasks += count;
     return IPS4O_OK;
 }
@@ -573,12 +573,12 @@ static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStrea
     } else {
         if (!(counts[0] | counts[1] | counts[2] | counts[3])) return IPS4O_OK;
         if (counts[3] && TR::CAP < 16384 && false) return IPS4O_EINTERNAL;
-        // the class-3 count lives on the device: the radix kernels append their fallbacks
+        // the class-3 count lives on the device: the cell kernels append their fallbacks
         memcpy(g_ws.h_ctr + CTR_BASE0 + 3, counts + 3, 4);
         CK(cudaMemcpyAsync(g_ws.ctr + CTR_BASE0 + 3, g_ws.h_ctr + CTR_BASE0 + 3, 4, cudaMemcpyHostToDevice, st));
-        int rc = run_radix_class<TR, 256>(data, counts[0], d_queues, st);
-        if (!rc) rc = run_radix_class<TR, 512>(data, counts[1], d_queues + QCAP, st);
-        if (!rc) rc = run_radix_class<TR, 1024>(data, counts[2], d_queues + 2 * QCAP, st);
+        int rc = run_cell_class<TR, 256, 8>(data, counts[0], d_queues, st);
+        if (!rc) rc = run_cell_class<TR, 512, 8>(data, counts[1], d_queues + QCAP, st);
+        if (!rc) rc = run_cell_class<TR, 512, 16>(data, counts[2], d_queues + 2 * QCAP, st);
         if (rc) return rc;
         constexpr int TH = TR::CAP >= 16384 ? 1024 : 512;
         typedef BaseClass<TR, TH, 16> BC;

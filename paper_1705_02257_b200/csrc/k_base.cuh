@@ -176,82 +176,71 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
     }
 }
 
-// ---------------------------------------------------------------- radix base case
+// ---------------------------------------------------------------- cell base case
 //
-// Leaves of up to 8192 elements (8/16-byte types) are sorted by one CTA entirely in shared
-// memory.  A merge sort spends one pass over shared memory per bit of order it establishes;
-// a k-way distribution establishes log2(k) bits per pass (the point of the paper's
-// samplesort), and for a leaf -- whose keys already lie between two
-// splitters -- the distribution needs no splitters: the keys' most significant varying bits
-// are a monotone bucket function.  So:
-//   1. load the leaf (coalesced) into registers, "warp-striped" (warp w holds positions
-//      [32*E*w, 32*E*(w+1)), lane l every 32nd of them), and find its key range
-//      [kmin, kmax]; (key - kmin) is order-preserving with h = bitlen(kmax - kmin) bits;
-//   2. two stable 8-bit counting passes (least significant digit first) over the window
-//      [h-16, h) of (key - kmin): per pass, warp-aggregated ranks from 8 ballots
-//      (no shared-memory atomics), per-warp digit counters turned into offsets by one
-//      thread per digit, and a scatter into the shared-memory tile;
-//   3. the leaf is now ordered by its 16 most significant varying bits; runs of keys equal
-//      in that window (rare: a few pairs per leaf for spread keys; equal keys need nothing)
-//      are finished by insertion sort -- the paper's own base-case sort --
-//      in place in shared memory;
-//   4. coalesced write-back.
-// A leaf whose runs would need too much insertion work is handed to the merge-sort kernel
-// (fallback queue) untouched.  Padding elements (positions >= n in a partly filled warp)
-// get the largest digit and, the passes being stable, stay behind every real element.
-template <class TR, int NT>
-struct RadixBase {
-    static constexpr int E = 8;
-    static constexpr int NW = NT / 32;
-    static constexpr u32 TILE = NT * E;
+// Leaves of up to 8192 elements (8/16-byte types) are sorted by one CTA in shared memory.
+// A leaf's keys already lie between two splitters, so one more distribution step needs no
+// splitters: the key range [kmin, kmax] is cut into 2^cb >= n equal cells by the top cb
+// significant bits of (key - kmin), an order-preserving map.  Then, as in the paper
+// (distribution down to tiny subproblems, finished by insertion sort):
+//   1. coalesced load into registers, the key range (warp shuffles + shared atomics);
+//   2. cell of every element; its rank inside the cell is the value a shared-memory
+//      atomic increment of the cell counter returns (order inside a cell is irrelevant);
+//   3. exclusive scan of the cell counts (each thread owns a run of cells), scatter of
+//      every element to base[cell] + rank;
+//   4. every cell holding two or more elements (about 1 per cell on average) is finished
+//      by insertion sort in place;
+//   5. coalesced write-back.
+// A leaf whose cells would need too much insertion work (keys clustered far below the
+// resolution of the cells) is handed to the merge-sort kernel (fallback queue) untouched.
+template <class TR, int NT, int E>
+struct CellBase {
+    static constexpr u32 TILE = NT * E;                  // a power of two
+    static constexpr u32 CPT = TILE / NT;                // cells per thread at most (= E)
     static constexpr size_t x_bytes = (size_t)TILE * sizeof(typename TR::V);
-    static constexpr size_t cnt_bytes = (size_t)NW * 256 * 2;
+    static constexpr size_t cnt_bytes = (size_t)(TILE + TILE / 16 + 2) * 4;
     static constexpr size_t smem = x_bytes + cnt_bytes;
 };
-constexpr u32 RADIX_FIX_BUDGET = 2048;  // insertion-sort moves per thread before falling back
+__device__ __forceinline__ u32 cpad(u32 c) { return c + (c >> 4); }
+constexpr u32 CELL_FIX_BUDGET = 4096;  // insertion-sort moves per thread before falling back
 
-template <class TR, int NT>
-__global__ void __launch_bounds__(NT) k_base_radix(const TaskDesc* tasks, u32 ntasks, void* vdata,
-                                                   TaskDesc* fb_queue, u32* fb_count, u32 fb_cap) {
+template <class TR, int NT, int E>
+__global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 ? 2 : 1)) k_base_cell(const TaskDesc* tasks, u32 ntasks, void* vdata,
+                                                  TaskDesc* fb_queue, u32* fb_count, u32 fb_cap) {
     typedef typename TR::V V;
-    typedef RadixBase<TR, NT> RB;
-    constexpr int E = RB::E, NW = RB::NW;
-    extern __shared__ __align__(16) unsigned char smr[];
-    V* X = reinterpret_cast<V*>(smr);
-    unsigned short* cnt0 = reinterpret_cast<unsigned short*>(smr + RB::x_bytes);
+    typedef CellBase<TR, NT, E> CB;
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(16) unsigned char smc[];
+    V* X = reinterpret_cast<V*>(smc);
+    u32* cnt = reinterpret_cast<u32*>(smc + CB::x_bytes);
     __shared__ u64 s_range[2];
-    __shared__ u32 s_flag, s_wsum[8], s_dbase[256], s_part[NT];
+    __shared__ u32 s_flag, s_wsum[NW];
     V* data = reinterpret_cast<V*>(vdata);
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const u32 lt = lanemask_lt();
-    // counters start at zero; each pass zeroes its set once the scatter is done
-    for (u32 i = tid; i < (u32)NW * 256u; i += NT) cnt0[i] = 0;
     for (u32 ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
         const TaskDesc td = tasks[ti];
         const u32 n = (u32)(td.hi - td.lo);
         V* g = data + td.lo;
-        __syncthreads();  // the previous leaf is finished (tile, flags)
+        const u32 cb = n > 1 ? 32u - (u32)__clz(n - 1) : 1u;  // 2^cb >= n cells
+        const u32 ncell = 1u << cb;
+        __syncthreads();  // the previous leaf is finished
         if (tid == 0) {
             s_range[0] = ~0ull;
             s_range[1] = 0ull;
             s_flag = 0;
         }
-        __syncthreads();
-        // 1. load (warp-striped) and the key range [kmin, kmax] of the leaf
-        const u32 wbase = w * 32u * E;
-        const bool wact = wbase < n;
+        for (u32 i = tid; i <= ncell; i += NT) cnt[cpad(i)] = 0;
+        // 1. load (element j*NT + tid) and the key range
         V v[E];
         u64 kmin = ~0ull, kmax = 0ull;
 #pragma unroll
         for (int j = 0; j < E; ++j) {
-            const u32 idx = wbase + j * 32 + lane;
+            const u32 idx = j * NT + tid;
             if (idx < n) {
                 v[j] = g[idx];
                 const u64 k = TR::key(v[j]);
                 kmin = k < kmin ? k : kmin;
                 kmax = k > kmax ? k : kmax;
-            } else {
-                v[j] = TR::pad();
             }
         }
 #pragma unroll
@@ -260,7 +249,8 @@ __global__ void __launch_bounds__(NT) k_base_radix(const TaskDesc* tasks, u32 nt
             kmin = a < kmin ? a : kmin;
             kmax = b > kmax ? b : kmax;
         }
-        if (lane == 0 && wact) {
+        __syncthreads();
+        if (lane == 0 && w * 32 < n) {
             atomicMin(&s_range[0], kmin);
             atomicMax(&s_range[1], kmax);
         }
@@ -268,161 +258,79 @@ __global__ void __launch_bounds__(NT) k_base_radix(const TaskDesc* tasks, u32 nt
         kmin = s_range[0];
         const u64 span = s_range[1] - kmin;
         if (span == 0) continue;  // all keys equal: already sorted (no write)
-        // the keys are ordered by (key - kmin); its h significant bits, the top 16 of them
-        // in the counting passes
         const u32 h = 64u - (u32)__clzll((long long)span);
-        const u32 lo_bit = h > 16u ? h - 16u : 0u;
-        const u32 npass = (h - lo_bit + 7u) / 8u;
-        // 2. stable counting passes over the window [lo_bit, h)
-        for (u32 p = 0; p < npass; ++p) {
-            const u32 shift = lo_bit + 8u * p;
-            unsigned short* cnt = cnt0;
-            u32 pos[E], dig[E];
-            if (wact) {
+        const u32 lo_bit = h > cb ? h - cb : 0u;
+        // 2. cell and rank inside the cell
+        u32 cr[E];  // cell | rank << 16
 #pragma unroll
-                for (int j = 0; j < E; ++j) {
-                    // digit of (key - kmin); padding takes the largest digit
-                    const bool real = wbase + j * 32 + lane < n;
-                    const u32 d = real ? (u32)((TR::key(v[j]) - kmin) >> shift) & 255u : 255u;
-                    dig[j] = d;
-                    u32 peers = 0xffffffffu;
-#pragma unroll
-                    for (int b = 0; b < 8; ++b) {
-                        const bool bit = (d >> b) & 1u;
-                        const u32 x = __ballot_sync(0xffffffffu, bit);
-                        peers &= bit ? x : ~x;
-                    }
-                    const u32 leader = __ffs(peers) - 1;
-                    u32 base = 0;
-                    if (lane == leader) {
-                        base = cnt[w * 256 + d];
-                        cnt[w * 256 + d] = (unsigned short)(base + __popc(peers));
-                    }
-                    base = __shfl_sync(0xffffffffu, base, leader);
-                    pos[j] = base + __popc(peers & lt);
-                    __syncwarp();
-                }
-            }
-            __syncthreads();
-            // offsets: thread (q, d) owns digit d of warps [8q, 8q+8); group partial sums,
-            // exclusive prefixes over groups and over digits, then per-warp offsets
-            const u32 d = tid & 255u, q = tid >> 8;
-            u32 c[8], part = 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                c[k] = cnt[(8 * q + k) * 256 + d];
-                const u32 t = part;
-                part += c[k];
-                c[k] = t;
-            }
-            s_part[q * 256 + d] = part;
-            __syncthreads();
-            if (q == 0) {
-                u32 tot = 0;
-#pragma unroll
-                for (int qq = 0; qq < NT / 256; ++qq) {
-                    const u32 x = s_part[qq * 256 + d];
-                    s_part[qq * 256 + d] = tot;
-                    tot += x;
-                }
-                u32 incl = tot;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= (u32)o) incl += y;
-                }
-                if (lane == 31) s_wsum[w] = incl;
-                s_dbase[d] = incl - tot;
-            }
-            __syncthreads();
-            {
-                u32 base = s_dbase[d] + s_part[q * 256 + d];
-                for (u32 ww = 0; ww < (d >> 5); ++ww) base += s_wsum[ww];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) cnt[(8 * q + k) * 256 + d] = (unsigned short)(base + c[k]);
-            }
-            __syncthreads();
-            if (wact) {
-#pragma unroll
-                for (int j = 0; j < E; ++j) X[cnt[w * 256 + dig[j]] + pos[j]] = v[j];
-            }
-            __syncthreads();
-            // the counters are free again: zero them for the next pass or leaf
-            for (u32 i = tid; i < (u32)NW * 256u; i += NT) cnt[i] = 0;
-            if (wact) {
-#pragma unroll
-                for (int j = 0; j < E; ++j) v[j] = X[wbase + j * 32 + lane];
-            }
-            __syncthreads();
-        }
-        // 3. runs of keys equal in the window but not equal: insertion sort (in place).
-        //    Thread t scans positions [t*per, (t+1)*per) in order and sorts every run that
-        //    starts there (a run may extend into the next thread's range, which skips it).
-        if (lo_bit > 0) {
-            u32 budget = RADIX_FIX_BUDGET;
-            const u32 per = (n + NT - 1) / NT;
-            const u32 i0 = tid * per, i1 = i0 + per < n ? i0 + per : n;
-            if (i0 < i1) {
-                // window of the element before the range: a run entering the range belongs
-                // to the previous thread
-                u64 wprev = i0 > 0 ? (TR::key(X[i0 - 1]) - kmin) >> lo_bit : ~0ull;
-                u32 rs = i0;          // start of the current run
-                bool own = false;     // the current run started inside this range
-                for (u32 i = i0; i < n; ++i) {
-                    const u64 wi = (TR::key(X[i]) - kmin) >> lo_bit;
-                    if (wi != wprev) {
-                        // run [rs, i) ends: sort it if it is ours and longer than one
-                        if (own && i - rs > 1) {
-                            for (u32 k = rs + 1; k < i && budget; ++k) {
-                                const V x = X[k];
-                                u32 q = k;
-                                while (q > rs && TR::less(x, X[q - 1]) && budget) {
-                                    X[q] = X[q - 1];
-                                    --q;
-                                    --budget;
-                                }
-                                X[q] = x;
-                            }
-                        }
-                        if (i >= i1) break;  // runs starting beyond the range are not ours
-                        rs = i;
-                        own = true;
-                        wprev = wi;
-                    }
-                    if (i + 1 == n && own && n - rs > 1) {
-                        for (u32 k = rs + 1; k < n && budget; ++k) {
-                            const V x = X[k];
-                            u32 q = k;
-                            while (q > rs && TR::less(x, X[q - 1]) && budget) {
-                                X[q] = X[q - 1];
-                                --q;
-                                --budget;
-                            }
-                            X[q] = x;
-                        }
-                    }
-                }
-                if (!budget) s_flag = 1;
-            }
-            __syncthreads();
-            if (s_flag) {
-                // too much insertion work: hand the untouched leaf to the merge sort
-                if (tid == 0) {
-                    const u32 q = atomicAdd(fb_count, 1u);
-                    if (q < fb_cap) fb_queue[q] = td;
-                }
-                continue;
-            }
-            // 4a. write back from the (fixed-up) tile
-            for (u32 i = tid; i < n; i += NT) g[i] = X[i];
-        } else if (wact) {
-            // 4b. the last pass left the sorted leaf in registers (warp-striped)
-#pragma unroll
-            for (int j = 0; j < E; ++j) {
-                const u32 idx = wbase + j * 32 + lane;
-                if (idx < n) g[idx] = v[j];
+        for (int j = 0; j < E; ++j) {
+            const u32 idx = j * NT + tid;
+            if (idx < n) {
+                const u32 c = (u32)((TR::key(v[j]) - kmin) >> lo_bit);
+                cr[j] = c | (atomicAdd(&cnt[cpad(c)], 1u) << 16);
             }
         }
+        __syncthreads();
+        // 3. exclusive scan of the counts: thread t owns cells [t*cpt, (t+1)*cpt) (the
+        //    counter array is padded by one word per 16 cells: conflict-free runs)
+        const u32 cpt = ncell > NT ? ncell / NT : 1u;
+        const u32 c0 = tid * cpt;
+        u32 sum = 0;
+        for (u32 k = 0; k < cpt; ++k)
+            if (c0 + k < ncell) sum += cnt[cpad(c0 + k)];
+        u32 incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (u32)o) incl += y;
+        }
+        if (lane == 31) s_wsum[w] = incl;
+        __syncthreads();
+        u32 base = incl - sum;
+        for (u32 ww = 0; ww < w; ++ww) base += s_wsum[ww];
+        for (u32 k = 0, run = base; k < cpt; ++k) {
+            if (c0 + k < ncell) {
+                const u32 x = cnt[cpad(c0 + k)];
+                cnt[cpad(c0 + k)] = run;
+                run += x;
+            }
+        }
+        if (tid == NT - 1) cnt[cpad(ncell)] = n;  // end of the last cell
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const u32 idx = j * NT + tid;
+            if (idx < n) X[cnt[cpad(cr[j] & 0xFFFFu)] + (cr[j] >> 16)] = v[j];
+        }
+        __syncthreads();
+        // 4. insertion sort inside every cell of two or more elements
+        u32 budget = CELL_FIX_BUDGET;
+        for (u32 k = 0; k < cpt; ++k) {
+            if (c0 + k >= ncell) break;
+            const u32 s0 = cnt[cpad(c0 + k)], s1 = cnt[cpad(c0 + k + 1)];
+            for (u32 i = s0 + 1; i < s1 && budget; ++i) {
+                const V x = X[i];
+                u32 q = i;
+                while (q > s0 && TR::less(x, X[q - 1]) && budget) {
+                    X[q] = X[q - 1];
+                    --q;
+                    --budget;
+                }
+                X[q] = x;
+            }
+        }
+        if (!budget) s_flag = 1;
+        __syncthreads();
+        if (s_flag) {
+            // too much insertion work: hand the untouched leaf to the merge sort
+            if (tid == 0) {
+                const u32 q = atomicAdd(fb_count, 1u);
+                if (q < fb_cap) fb_queue[q] = td;
+            }
+            continue;
+        }
+        // 5. write back
+        for (u32 i = tid; i < n; i += NT) g[i] = X[i];
     }
 }
 
