@@ -180,16 +180,17 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
 //
 // Leaves of up to 8192 elements (8/16-byte types) are sorted by one CTA in shared memory.
 // A leaf's keys already lie between two splitters, so one more distribution step needs no
-// splitters: the key range [kmin, kmax] is cut into 2^cb >= n equal cells by the top cb
-// significant bits of (key - kmin), an order-preserving map.  Then, as in the paper
+// splitters: the key range [kmin, kmax] is cut into 2^cb >= n equal cells by the
+// order-preserving map floor((key - kmin) * 2^cb / (kmax - kmin + 1)).  Then, as in the paper
 // (distribution down to tiny subproblems, finished by insertion sort):
 //   1. coalesced load into registers, the key range (warp shuffles + shared atomics);
 //   2. cell of every element; its rank inside the cell is the value a shared-memory
 //      atomic increment of the cell counter returns (order inside a cell is irrelevant);
 //   3. exclusive scan of the cell counts (each thread owns a run of cells), scatter of
 //      every element to base[cell] + rank;
-//   4. every cell holding two or more elements (about 1 per cell on average) is finished
-//      by insertion sort in place;
+//   4. the elements of a cell (about one per cell on average) are put in order: each
+//      element of a small cell counts the cell's elements preceding it; a large cell
+//      (duplicates, clustered keys) is finished by insertion sort in place;
 //   5. coalesced write-back.
 // A leaf whose cells would need too much insertion work (keys clustered far below the
 // resolution of the cells) is handed to the merge-sort kernel (fallback queue) untouched.
@@ -203,6 +204,7 @@ struct CellBase {
 };
 __device__ __forceinline__ u32 cpad(u32 c) { return c + (c >> 4); }
 constexpr u32 CELL_FIX_BUDGET = 4096;  // insertion-sort moves per thread before falling back
+constexpr u32 CELL_SMALL = 16;         // cells up to this size are ordered by parallel counting
 
 template <class TR, int NT, int E>
 __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 ? 2 : 1)) k_base_cell(const TaskDesc* tasks, u32 ntasks, void* vdata,
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
     extern __shared__ __align__(16) unsigned char smc[];
     V* X = reinterpret_cast<V*>(smc);
     u32* cnt = reinterpret_cast<u32*>(smc + CB::x_bytes);
-    __shared__ u64 s_range[2];
+    __shared__ u64 s_range[2], s_mul;
     __shared__ u32 s_flag, s_wsum[NW];
     V* data = reinterpret_cast<V*>(vdata);
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -258,15 +260,19 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
         kmin = s_range[0];
         const u64 span = s_range[1] - kmin;
         if (span == 0) continue;  // all keys equal: already sorted (no write)
-        const u32 h = 64u - (u32)__clzll((long long)span);
-        const u32 lo_bit = h > cb ? h - cb : 0u;
+        // cell(key) = floor((key - kmin) * ncell / (span + 1)) as the high half of a 64x64
+        // product with a per-leaf multiplier: monotone, onto [0, ncell)
+        if (tid == 0) s_mul = span < ncell ? 0ull : (u64)(((unsigned __int128)ncell << 64) / ((unsigned __int128)span + 1));
+        __syncthreads();
+        const u64 mul = s_mul;
         // 2. cell and rank inside the cell
         u32 cr[E];  // cell | rank << 16
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             const u32 idx = j * NT + tid;
             if (idx < n) {
-                const u32 c = (u32)((TR::key(v[j]) - kmin) >> lo_bit);
+                const u64 x = TR::key(v[j]) - kmin;
+                const u32 c = mul ? (u32)__umul64hi(x, mul) : (u32)x;
                 cr[j] = c | (atomicAdd(&cnt[cpad(c)], 1u) << 16);
             }
         }
@@ -303,11 +309,38 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
             if (idx < n) X[cnt[cpad(cr[j] & 0xFFFFu)] + (cr[j] >> 16)] = v[j];
         }
         __syncthreads();
-        // 4. insertion sort inside every cell of two or more elements
+        // 4. order inside the cells.  An element of a cell of m <= CELL_SMALL elements finds
+        //    its place by counting the cell's elements that precede it (smaller key, or equal
+        //    key and lower rank) -- all elements in parallel; larger cells (duplicates,
+        //    clusters) are finished by insertion sort by their owner thread.
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const u32 idx = j * NT + tid;
+            u32 fin = 0xFFFFFFFFu;  // final position (replaces cell | rank in cr[j])
+            if (idx < n) {
+                const u32 c = cr[j] & 0xFFFFu, r = cr[j] >> 16;
+                const u32 s0 = cnt[cpad(c)], m = cnt[cpad(c + 1)] - s0;
+                if (m <= CELL_SMALL) {
+                    const u64 kv = TR::key(v[j]);
+                    u32 before = 0;
+                    for (u32 q = 0; q < m; ++q) {
+                        const u64 ke = TR::key(X[s0 + q]);
+                        before += (ke < kv || (ke == kv && q < r)) ? 1u : 0u;
+                    }
+                    fin = s0 + before;
+                }
+            }
+            cr[j] = fin;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < E; ++j)
+            if (cr[j] != 0xFFFFFFFFu) X[cr[j]] = v[j];
         u32 budget = CELL_FIX_BUDGET;
         for (u32 k = 0; k < cpt; ++k) {
             if (c0 + k >= ncell) break;
             const u32 s0 = cnt[cpad(c0 + k)], s1 = cnt[cpad(c0 + k + 1)];
+            if (s1 - s0 <= CELL_SMALL) continue;
             for (u32 i = s0 + 1; i < s1 && budget; ++i) {
                 const V x = X[i];
                 u32 q = i;

@@ -25,9 +25,9 @@ struct K2Smem {
     static constexpr int B = TR::B;
     static constexpr int NW = NT / 32;
     static constexpr size_t buf_bytes = (size_t)MAXK * B * sizeof(V);
-    static constexpr size_t wcnt_bytes = (size_t)NW * MAXK * 2;
+    static constexpr size_t wcnt_bytes = 0;
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
-    static constexpr size_t arr_bytes = 4 * MAXK * 4;
+    static constexpr size_t arr_bytes = 5 * MAXK * 4;
     static constexpr size_t rtree_bytes = (size_t)MAXK * TREE_COPIES * 8;
     static constexpr size_t total = buf_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes;
 };
@@ -175,52 +175,90 @@ __device__ __forceinline__ void rtree_fill(u64* rtree, const u64* gtree, u32 tid
     for (u32 i = tid; i < (u32)MAXK * TREE_COPIES; i += nthreads) rtree[i] = gtree[i / TREE_COPIES];
 }
 
+// One level of the branchless descent without a peer mask (the ranks come from shared-
+// memory atomics): 5 SASS instructions per level and key.
+__device__ __forceinline__ void descend_step_nb(u64 key, u32 sbase, u32& a, u32 t0, u32 t1) {
+    asm("{\n\t"
+        ".reg .pred p;\n\t"
+        ".reg .b32 t, ad;\n\t"
+        ".reg .b64 nd;\n\t"
+        "add.u32 ad, %1, %0;\n\t"
+        "ld.shared.u64 nd, [ad];\n\t"
+        "setp.ge.u64 p, %2, nd;\n\t"
+        "selp.b32 t, %4, %3, p;\n\t"
+        "mad.lo.u32 %0, %0, 2, t;\n\t"
+        "}"
+        : "+r"(a)
+        : "r"(sbase), "l"(key), "r"(t0), "r"(t1));
+}
+
+// Branchless classification of E keys through the replicated tree,
+// level by level so that the E lookups of a level are in flight together.
+template <int E, int LOGK>
+__device__ __forceinline__ void k2_bucket_keys(const u64 (&key)[E], u32 valid, const u64* tree, const u64* spl,
+                                               u32 logk, u32 kprime, u32 eq, u32 (&bk)[E]) {
+    u32 a[E];
+    const u32 cofs = (threadIdx.x & (TREE_COPIES - 1)) * 8u;
+    const u32 t0 = 0u - cofs, t1 = TREE_NODE_BYTES - cofs;
+    const u64 root = tree[cofs / 8 + TREE_COPIES];
+    const u32 sb = (u32)__cvta_generic_to_shared(tree);
+#pragma unroll
+    for (int e = 0; e < E; ++e) a[e] = (key[e] >= root ? 3u : 2u) * TREE_NODE_BYTES + cofs;
+    if (LOGK == 8) {
+#pragma unroll
+        for (int l = 1; l < 8; ++l)
+#pragma unroll
+            for (int e = 0; e < E; ++e) descend_step_nb(key[e], sb, a[e], t0, t1);
+    } else {
+        for (u32 l = 1; l < logk; ++l)
+#pragma unroll
+            for (int e = 0; e < E; ++e) descend_step_nb(key[e], sb, a[e], t0, t1);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        u32 i = (a[e] - cofs) / TREE_NODE_BYTES - kprime;
+        if (eq) {
+            const u32 ii = i ? i : 1u;
+            const bool isq = i >= 1u && spl[ii] >= key[e];
+            i = 2 * i - (isq ? 1u : 0u);
+        }
+        bk[e] = ((valid >> e) & 1u) ? i : INV_BUCKET;
+    }
+}
+
 template <class TR, int NT, int E, int LOGK>
 __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const uint4 (&raw)[E / TR::VEC],
                                         u32 valid, bool final_tile, u64 mb, u32 cap,
-                                        typename TR::V* buf, unsigned short* wcnt,
+                                        typename TR::V* buf, u32* fbase,
                                         const u64* tree, const u64* spl, u32* fill, u32* cnt,
                                         u32* slotb, u32* nfl, u32* s_nflushed, u32 logk,
                                         u32 kprime, u32 eq) {
     typedef typename TR::V V;
     constexpr int B = TR::B;
-    const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const u32 tid = threadIdx.x;
     V v[E];
 #pragma unroll
     for (int i = 0; i < E / TR::VEC; ++i) memcpy(&v[i * TR::VEC], &raw[i], 16);
-    u32 bk[E];
-    u32 pos[E];
-    // 1. classify (+ per-slot peer masks for the warp aggregation)
-    u32 peers[E];
-    k2_classify<TR, E, LOGK>(v, valid, __all_sync(0xffffffffu, valid == (1u << E) - 1u), tree, spl,
-                             logk, kprime, eq, bk, peers);
-    // 2. warp-aggregated ranking: the leaders' counter updates in slot order
-    const u32 lt = lanemask_lt();
+    // 1. classify; 2. rank: the position of the element in its bucket's stream of this
+    //    stripe is the value a shared-memory atomic increment of the bucket count returns
+    //    (elements of a bucket may take any order)
+    u32 bk[E], pos[E];
+    {
+        u64 key[E];
 #pragma unroll
-    for (int j = 0; j < E; ++j) {
-        const u32 b = bk[j];
-        const u32 leader = __ffs(peers[j]) - 1;
-        u32 base = 0;
-        if (lane == leader && b != INV_BUCKET) {
-            base = wcnt[w * MAXK + b];
-            wcnt[w * MAXK + b] = (unsigned short)(base + __popc(peers[j]));
-        }
-        base = __shfl_sync(0xffffffffu, base, leader);
-        pos[j] = base + __popc(peers[j] & lt);
-        __syncwarp();
+        for (int e = 0; e < E; ++e) key[e] = TR::key(v[e], 0);
+        k2_bucket_keys<E, LOGK>(key, valid, tree, spl, logk, kprime, eq, bk);
     }
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+        if (bk[j] != INV_BUCKET) pos[j] = atomicAdd(&cnt[bk[j]], 1u);
     __syncthreads();
-    // 3. per bucket: offsets over warps, completed blocks, flush slots
+    // 3. per bucket: blocks completed in this tile and their flush slots.  fbase[b] = stream
+    //    position of the buffer's first element (the elements flushed so far).
     if (tid < (u32)MAXK) {
         const u32 b = tid;
-        const u32 f = fill[b];
-        u32 run = f;
-#pragma unroll
-        for (int ww = 0; ww < NT / 32; ++ww) {
-            u32 c = wcnt[ww * MAXK + b];
-            wcnt[ww * MAXK + b] = (unsigned short)run;
-            run += c;
-        }
+        const u32 f0 = fbase[b];
+        const u32 run = cnt[b] - f0;  // buffered + new elements
         u32 nf = run / B, slot = 0;
         if (nf) {
             if (final_tile) {
@@ -238,7 +276,6 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         }
         nfl[b] = nf;
         slotb[b] = slot;
-        cnt[b] += run - f;
         fill[b] = run - nf * B;
     }
     __syncthreads();
@@ -248,7 +285,7 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     for (int j = 0; j < E; ++j) {
         const u32 b = bk[j];
         if (b == INV_BUCKET) continue;
-        const u32 p = (u32)wcnt[w * MAXK + b] + pos[j];
+        const u32 p = pos[j] - fbase[b];
         const u32 q = p / B, off = p % B, nf = nfl[b];
         if (q == 0) {
             buf[b * B + off] = v[j];
@@ -265,18 +302,15 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     if (tid < (u32)MAXK && nfl[tid]) {
         bulk_s2g(data + mb + (u64)slotb[tid] * B, buf + tid * B, B * sizeof(V));
         bulk_commit();
+        fbase[tid] += nfl[tid] * B;
         bulk_wait_read0();
     }
     __syncthreads();
-    // 6. remainders start the next buffer; reset per-warp counters
+    // 6. remainders start the next buffer (the next tile's barriers order these writes
+    //    before any later flush)
 #pragma unroll
     for (int j = 0; j < E; ++j)
         if (defer & (1u << j)) buf[bk[j] * B + pos[j]] = v[j];
-    if (tid < (u32)MAXK) {
-#pragma unroll
-        for (int ww = 0; ww < NT / 32; ++ww) wcnt[ww * MAXK + tid] = 0;
-    }
-    __syncthreads();
 }
 
 template <class TR, int NT, int E, int MINB>
@@ -287,13 +321,13 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
     constexpr u32 TILE = NT * E;
     extern __shared__ __align__(128) unsigned char smem[];
     V* buf = reinterpret_cast<V*>(smem);
-    unsigned short* wcnt = reinterpret_cast<unsigned short*>(smem + SM::buf_bytes);
     u64* tree = reinterpret_cast<u64*>(smem + SM::buf_bytes + SM::wcnt_bytes);
     u64* spl = tree + MAXK;
     u32* fill = reinterpret_cast<u32*>(spl + MAXK);
     u32* cnt = fill + MAXK;
     u32* slotb = cnt + MAXK;
     u32* nfl = slotb + MAXK;
+    u32* fbase = nfl + MAXK;
     u64* rtree = reinterpret_cast<u64*>(smem + SM::buf_bytes + SM::wcnt_bytes + SM::tree_bytes + SM::arr_bytes);
     __shared__ u32 s_stripe, s_nflushed, s_wsum[NT / 32];
     __shared__ u64 s_spbase;
@@ -315,8 +349,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             spl[tid] = A.spl[(u64)sd.task * MAXK + tid];
             fill[tid] = 0;
             cnt[tid] = 0;
-#pragma unroll
-            for (int ww = 0; ww < NT / 32; ++ww) wcnt[ww * MAXK + tid] = 0;
+            fbase[tid] = 0;
         }
         rtree_fill(rtree, A.tree + (u64)sd.task * MAXK, tid, NT);
         if (tid == 0) s_nflushed = 0;
@@ -335,10 +368,10 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
                 const u64 tb = mb + ti * TILE;
                 if (ti + 1 < nft) k2_load_full<TR, NT, E>(data, tb + TILE, nxt);
                 if (tp.logk == 8)
-                    k2_tile<TR, NT, E, 8>(data, cur, ALL, false, mb, cap, buf, wcnt, rtree, spl, fill, cnt,
+                    k2_tile<TR, NT, E, 8>(data, cur, ALL, false, mb, cap, buf, fbase, rtree, spl, fill, cnt,
                                           slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
                 else
-                    k2_tile<TR, NT, E, 0>(data, cur, ALL, false, mb, cap, buf, wcnt, rtree, spl, fill, cnt,
+                    k2_tile<TR, NT, E, 0>(data, cur, ALL, false, mb, cap, buf, fbase, rtree, spl, fill, cnt,
                                           slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
 #pragma unroll
                 for (int e = 0; e < E / TR::VEC; ++e) cur[e] = nxt[e];
@@ -346,7 +379,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             const u64 tb = mb + nft * TILE;
             if (tb < me) {
                 const u32 vt = k2_load<TR, NT, E>(data, tb, (u32)(me - tb), cur);
-                k2_tile<TR, NT, E, 0>(data, cur, vt, false, mb, cap, buf, wcnt, rtree, spl, fill, cnt,
+                k2_tile<TR, NT, E, 0>(data, cur, vt, false, mb, cap, buf, fbase, rtree, spl, fill, cnt,
                                       slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
             }
         }
@@ -356,7 +389,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             const u64 hend = tp.g < tp.hi ? tp.g : tp.hi;
             uint4 hv[E / TR::VEC];
             const u32 hval = k2_load<TR, NT, E>(data, tp.lo, (u32)(hend - tp.lo), hv);
-            k2_tile<TR, NT, E, 0>(data, hv, hval, true, mb, cap, buf, wcnt, rtree, spl, fill, cnt, slotb, nfl,
+            k2_tile<TR, NT, E, 0>(data, hv, hval, true, mb, cap, buf, fbase, rtree, spl, fill, cnt, slotb, nfl,
                            &s_nflushed, tp.logk, tp.kprime, tp.eq);
         }
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area
