@@ -14,7 +14,7 @@ constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer (SURVEY 
 // Each bucket's permutation control pair: the packed (w, r) word, then its reader count.
 // (Spreading the pairs over 256-byte lines -- one L2 slice each -- measured no faster.)
 constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
-constexpr int TREE_COPIES = 16;      // replicated splitter tree in K2 (one copy per half-warp lane)
+constexpr int TREE_COPIES = 8;       // replicated splitter tree in K2 (lanes l, l+8 of a half-warp share a copy)
 constexpr u32 TREE_NODE_BYTES = 8 * TREE_COPIES;
 constexpr u32 INV_BUCKET = 0xFFFFu;  // "no element" marker in classification registers
 constexpr int K3_THREADS = 256;      // block permutation CTA
@@ -268,6 +268,26 @@ __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, u32 bytes
     u32 s = (u32)__cvta_generic_to_shared(ssrc);
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s),
                  "r"(bytes)
+                 : "memory");
+}
+// TMA bulk copy global -> shared with mbarrier transaction-count completion
+__device__ __forceinline__ void mbar_init(u64* mbar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((u32)__cvta_generic_to_shared(mbar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, u32 bytes, u64* mbar) {
+    const u32 mb = (u32)__cvta_generic_to_shared(mbar), sd = (u32)__cvta_generic_to_shared(sdst);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sd), "l"(gsrc), "r"(bytes), "r"(mb)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* mbar, u32 parity) {
+    const u32 mb = (u32)__cvta_generic_to_shared(mbar);
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra W;\n\t}" ::"r"(mb), "r"(parity)
                  : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }

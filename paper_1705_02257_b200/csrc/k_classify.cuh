@@ -29,7 +29,8 @@ struct K2Smem {
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
     static constexpr size_t arr_bytes = 5 * MAXK * 4;
     static constexpr size_t rtree_bytes = (size_t)MAXK * TREE_COPIES * 8;
-    static constexpr size_t total = buf_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes;
+    static constexpr size_t stage_bytes = (size_t)2 * NT * (16 / TR::S * 4) * TR::S;  // 2 tiles
+    static constexpr size_t total = buf_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes + stage_bytes;
 };
 
 // Loads one tile (<= NT*E elements from tb, len valid) into raw 16-byte registers; bit e of
@@ -226,13 +227,25 @@ __device__ __forceinline__ void k2_bucket_keys(const u64 (&key)[E], u32 valid, c
     }
 }
 
+// Elements of a tile that start a bucket's next buffer block while the buffer's completed
+// block is still being flushed: kept in registers and written into the buffer during the
+// next tile's placement, after the flush has read the buffer (so the TMA read latency
+// overlaps the next tile's classification instead of stalling a barrier).
+template <class TR, int E>
+struct K2Defer {
+    typename TR::V v[E];
+    u32 off[E], bk[E];
+    u32 mask;
+};
+
 template <class TR, int NT, int E, int LOGK>
 __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const uint4 (&raw)[E / TR::VEC],
                                         u32 valid, bool final_tile, u64 mb, u32 cap,
                                         typename TR::V* buf, u32* fbase,
                                         const u64* tree, const u64* spl, u32* fill, u32* cnt,
                                         u32* slotb, u32* nfl, u32* s_nflushed, u32 logk,
-                                        u32 kprime, u32 eq) {
+                                        u32 kprime, u32 eq, const typename TR::V* refill,
+                                        typename TR::V* refill_stage, u64* refill_mbar, K2Defer<TR, E>& df) {
     typedef typename TR::V V;
     constexpr int B = TR::B;
     const u32 tid = threadIdx.x;
@@ -253,12 +266,19 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     for (int j = 0; j < E; ++j)
         if (bk[j] != INV_BUCKET) pos[j] = atomicAdd(&cnt[bk[j]], 1u);
     __syncthreads();
-    // 3. per bucket: blocks completed in this tile and their flush slots.  fbase[b] = stream
-    //    position of the buffer's first element (the elements flushed so far).
+    if (refill && tid == 0) {
+        // every thread has read the stage: load the tile two ahead into it (WAR across the
+        // generic and async proxies: fence first)
+        fence_proxy_async_smem();
+        bulk_g2s(refill_stage, refill, NT * E * sizeof(V), refill_mbar);
+    }
+    // 3. per bucket: the previous tile's flush has read the buffer; blocks completed in
+    //    this tile and their flush slots.  fbase[b] = stream position of the buffer's
+    //    first element (the elements flushed so far).
     if (tid < (u32)MAXK) {
+        bulk_wait_read0();
         const u32 b = tid;
-        const u32 f0 = fbase[b];
-        const u32 run = cnt[b] - f0;  // buffered + new elements
+        const u32 run = cnt[b] - fbase[b];  // buffered (incl. deferred) + new elements
         u32 nf = run / B, slot = 0;
         if (nf) {
             if (final_tile) {
@@ -279,7 +299,12 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         fill[b] = run - nf * B;
     }
     __syncthreads();
-    // 4. place: first block -> smem buffer, later complete blocks -> straight to the stripe
+    // 4. place: the previous tile's deferred elements, then this tile's: first block ->
+    //    smem buffer, later complete blocks -> straight to the stripe, the start of the
+    //    next block -> deferred
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+        if (df.mask & (1u << j)) buf[df.bk[j] * B + df.off[j]] = df.v[j];
     u32 defer = 0;
 #pragma unroll
     for (int j = 0; j < E; ++j) {
@@ -292,25 +317,35 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         } else if (q < nf) {
             data[mb + (u64)(slotb[b] + q) * B + off] = v[j];
         } else {
-            pos[j] = p - nf * B;
+            df.v[j] = v[j];
+            df.off[j] = p - nf * B;
+            df.bk[j] = b;
             defer |= 1u << j;
         }
     }
+    df.mask = defer;
     fence_proxy_async_smem();
     __syncthreads();
-    // 5. flush complete buffer blocks with TMA bulk copies
+    // 5. flush complete buffer blocks with TMA bulk copies (their reads are awaited at the
+    //    next tile's step 3)
     if (tid < (u32)MAXK && nfl[tid]) {
         bulk_s2g(data + mb + (u64)slotb[tid] * B, buf + tid * B, B * sizeof(V));
         bulk_commit();
         fbase[tid] += nfl[tid] * B;
-        bulk_wait_read0();
     }
+}
+
+// End of a stripe: the last flushes have read their buffers; deferred elements join the
+// buffers (which then hold every partial block).
+template <class TR, int E>
+__device__ __forceinline__ void k2_drain(typename TR::V* buf, K2Defer<TR, E>& df) {
+    if (threadIdx.x < (u32)MAXK) bulk_wait_read0();
     __syncthreads();
-    // 6. remainders start the next buffer (the next tile's barriers order these writes
-    //    before any later flush)
 #pragma unroll
     for (int j = 0; j < E; ++j)
-        if (defer & (1u << j)) buf[bk[j] * B + pos[j]] = v[j];
+        if (df.mask & (1u << j)) buf[df.bk[j] * TR::B + df.off[j]] = df.v[j];
+    df.mask = 0;
+    __syncthreads();
 }
 
 template <class TR, int NT, int E, int MINB>
@@ -329,8 +364,18 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
     u32* nfl = slotb + MAXK;
     u32* fbase = nfl + MAXK;
     u64* rtree = reinterpret_cast<u64*>(smem + SM::buf_bytes + SM::wcnt_bytes + SM::tree_bytes + SM::arr_bytes);
+    V* stage = reinterpret_cast<V*>(smem + SM::buf_bytes + SM::wcnt_bytes + SM::tree_bytes + SM::arr_bytes +
+                                    SM::rtree_bytes);
     __shared__ u32 s_stripe, s_nflushed, s_wsum[NT / 32];
     __shared__ u64 s_spbase;
+    __shared__ __align__(8) u64 s_mbar[2];
+    u32 phase = 0;  // parity of the next completion of each stage's mbarrier (bits 0, 1)
+    if (threadIdx.x == 0) {
+        mbar_init(&s_mbar[0], 1);
+        mbar_init(&s_mbar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     V* data = reinterpret_cast<V*>(A.data);
 
@@ -356,31 +401,45 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
         __syncthreads();
         const u64 mb = sd.begin > tp.g ? sd.begin : tp.g;  // stripe main region start (block aligned)
         const u64 me = sd.end;
+        K2Defer<TR, E> df;
+        df.mask = 0;
         const u32 cap = me > mb ? (u32)((me - mb) / B) : 0u;
         if (mb < me) {
-            // full tiles: straight-line 128-bit loads, the next tile prefetched into registers
-            // while this one is processed; then the (single) partial tail tile
+            // full tiles: staged in shared memory by TMA bulk loads two tiles ahead (a tile
+            // is contiguous: one cp.async.bulk each, completion on the stage's mbarrier);
+            // then the (single) partial tail tile by direct 128-bit loads
             const u64 nft = (me - mb) / TILE;
-            uint4 cur[E / TR::VEC], nxt[E / TR::VEC];
+            uint4 cur[E / TR::VEC];
             constexpr u32 ALL = (E >= 32) ? 0xFFFFFFFFu : ((1u << E) - 1u);
-            if (nft > 0) k2_load_full<TR, NT, E>(data, mb, cur);
+            constexpr u32 TB = TILE * sizeof(V);
+            if (tid == 0) {
+                for (u64 k = 0; k < 2 && k < nft; ++k) bulk_g2s(stage + k * TILE, data + mb + k * TILE, TB, &s_mbar[k]);
+            }
             for (u64 ti = 0; ti < nft; ++ti) {
-                const u64 tb = mb + ti * TILE;
-                if (ti + 1 < nft) k2_load_full<TR, NT, E>(data, tb + TILE, nxt);
+                const u32 st = (u32)(ti & 1);
+                mbar_wait(&s_mbar[st], (phase >> st) & 1u);
+                phase ^= 1u << st;
+                const uint4* sp = reinterpret_cast<const uint4*>(stage + st * TILE);
+#pragma unroll
+                for (int i = 0; i < E / TR::VEC; ++i) cur[i] = sp[i * NT + tid];
+                // (the tile's first barrier follows every thread's reads of the stage; the
+                // refill of this stage for tile ti+2 is issued after it, inside k2_tile)
+                const V* refill = ti + 2 < nft ? data + mb + (ti + 2) * TILE : nullptr;
                 if (tp.logk == 8)
                     k2_tile<TR, NT, E, 8>(data, cur, ALL, false, mb, cap, buf, fbase, rtree, spl, fill, cnt,
-                                          slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
+                                          slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
+                                          refill, stage + st * TILE, &s_mbar[st], df);
                 else
                     k2_tile<TR, NT, E, 0>(data, cur, ALL, false, mb, cap, buf, fbase, rtree, spl, fill, cnt,
-                                          slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
-#pragma unroll
-                for (int e = 0; e < E / TR::VEC; ++e) cur[e] = nxt[e];
+                                          slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
+                                          refill, stage + st * TILE, &s_mbar[st], df);
             }
             const u64 tb = mb + nft * TILE;
             if (tb < me) {
                 const u32 vt = k2_load<TR, NT, E>(data, tb, (u32)(me - tb), cur);
                 k2_tile<TR, NT, E, 0>(data, cur, vt, false, mb, cap, buf, fbase, rtree, spl, fill, cnt,
-                                      slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq);
+                                      slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
+                                      nullptr, nullptr, nullptr, df);
             }
         }
         if (sd.first && tp.lo < tp.g) {
@@ -390,8 +449,9 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             uint4 hv[E / TR::VEC];
             const u32 hval = k2_load<TR, NT, E>(data, tp.lo, (u32)(hend - tp.lo), hv);
             k2_tile<TR, NT, E, 0>(data, hv, hval, true, mb, cap, buf, fbase, rtree, spl, fill, cnt, slotb, nfl,
-                           &s_nflushed, tp.logk, tp.kprime, tp.eq);
+                           &s_nflushed, tp.logk, tp.kprime, tp.eq, nullptr, nullptr, nullptr, df);
         }
+        k2_drain<TR, E>(buf, df);
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area
         u32 f = tid < (u32)MAXK ? fill[tid] : 0u;
         u32 incl = f;
