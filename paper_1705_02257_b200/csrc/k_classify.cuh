@@ -241,7 +241,7 @@ struct K2Defer {
 template <class TR, int NT, int E, int LOGK>
 __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const uint4 (&raw)[E / TR::VEC],
                                         u32 valid, bool final_tile, u64 mb, u32 cap,
-                                        typename TR::V* buf, u32* fbase,
+                                        typename TR::V* buf, u32* nbl,
                                         const u64* tree, const u64* spl, u32* fill, u32* cnt,
                                         u32* slotb, u32* nfl, u32* s_nflushed, u32 logk,
                                         u32 kprime, u32 eq, const typename TR::V* refill,
@@ -273,12 +273,13 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         bulk_g2s(refill_stage, refill, NT * E * sizeof(V), refill_mbar);
     }
     // 3. per bucket: the previous tile's flush has read the buffer; blocks completed in
-    //    this tile and their flush slots.  fbase[b] = stream position of the buffer's
-    //    first element (the elements flushed so far).
+    //    this tile and their flush slots.  cnt[b] counts the bucket's stream from the first
+    //    element of its buffer (the atomics above returned buffer-relative positions); it is
+    //    rebased past the blocks flushed now, nbl[b] counts the flushed blocks.
     if (tid < (u32)MAXK) {
         bulk_wait_read0();
         const u32 b = tid;
-        const u32 run = cnt[b] - fbase[b];  // buffered (incl. deferred) + new elements
+        const u32 run = cnt[b];  // buffered (incl. deferred) + new elements
         u32 nf = run / B, slot = 0;
         if (nf) {
             if (final_tile) {
@@ -296,7 +297,9 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         }
         nfl[b] = nf;
         slotb[b] = slot;
+        cnt[b] = run - nf * B;
         fill[b] = run - nf * B;
+        nbl[b] += nf;
     }
     __syncthreads();
     // 4. place: the previous tile's deferred elements, then this tile's: first block ->
@@ -310,17 +313,20 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     for (int j = 0; j < E; ++j) {
         const u32 b = bk[j];
         if (b == INV_BUCKET) continue;
-        const u32 p = pos[j] - fbase[b];
-        const u32 q = p / B, off = p % B, nf = nfl[b];
+        const u32 p = pos[j];
+        const u32 q = p / B, off = p % B;
         if (q == 0) {
             buf[b * B + off] = v[j];
-        } else if (q < nf) {
-            data[mb + (u64)(slotb[b] + q) * B + off] = v[j];
         } else {
-            df.v[j] = v[j];
-            df.off[j] = p - nf * B;
-            df.bk[j] = b;
-            defer |= 1u << j;
+            const u32 nf = nfl[b];
+            if (q < nf) {
+                data[mb + (u64)(slotb[b] + q) * B + off] = v[j];
+            } else {
+                df.v[j] = v[j];
+                df.off[j] = p - nf * B;
+                df.bk[j] = b;
+                defer |= 1u << j;
+            }
         }
     }
     df.mask = defer;
@@ -331,7 +337,6 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     if (tid < (u32)MAXK && nfl[tid]) {
         bulk_s2g(data + mb + (u64)slotb[tid] * B, buf + tid * B, B * sizeof(V));
         bulk_commit();
-        fbase[tid] += nfl[tid] * B;
     }
 }
 
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
     u32* cnt = fill + MAXK;
     u32* slotb = cnt + MAXK;
     u32* nfl = slotb + MAXK;
-    u32* fbase = nfl + MAXK;
+    u32* nbl = nfl + MAXK;
     u64* rtree = reinterpret_cast<u64*>(smem + SM::buf_bytes + SM::wcnt_bytes + SM::tree_bytes + SM::arr_bytes);
     V* stage = reinterpret_cast<V*>(smem + SM::buf_bytes + SM::wcnt_bytes + SM::tree_bytes + SM::arr_bytes +
                                     SM::rtree_bytes);
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             spl[tid] = A.spl[(u64)sd.task * MAXK + tid];
             fill[tid] = 0;
             cnt[tid] = 0;
-            fbase[tid] = 0;
+            nbl[tid] = 0;
         }
         rtree_fill(rtree, A.tree + (u64)sd.task * MAXK, tid, NT);
         if (tid == 0) s_nflushed = 0;
@@ -426,18 +431,18 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
                 // refill of this stage for tile ti+2 is issued after it, inside k2_tile)
                 const V* refill = ti + 2 < nft ? data + mb + (ti + 2) * TILE : nullptr;
                 if (tp.logk == 8)
-                    k2_tile<TR, NT, E, 8>(data, cur, ALL, false, mb, cap, buf, fbase, rtree, spl, fill, cnt,
+                    k2_tile<TR, NT, E, 8>(data, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                           slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
                                           refill, stage + st * TILE, &s_mbar[st], df);
                 else
-                    k2_tile<TR, NT, E, 0>(data, cur, ALL, false, mb, cap, buf, fbase, rtree, spl, fill, cnt,
+                    k2_tile<TR, NT, E, 0>(data, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                           slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
                                           refill, stage + st * TILE, &s_mbar[st], df);
             }
             const u64 tb = mb + nft * TILE;
             if (tb < me) {
                 const u32 vt = k2_load<TR, NT, E>(data, tb, (u32)(me - tb), cur);
-                k2_tile<TR, NT, E, 0>(data, cur, vt, false, mb, cap, buf, fbase, rtree, spl, fill, cnt,
+                k2_tile<TR, NT, E, 0>(data, cur, vt, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                       slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
                                       nullptr, nullptr, nullptr, df);
             }
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             const u64 hend = tp.g < tp.hi ? tp.g : tp.hi;
             uint4 hv[E / TR::VEC];
             const u32 hval = k2_load<TR, NT, E>(data, tp.lo, (u32)(hend - tp.lo), hv);
-            k2_tile<TR, NT, E, 0>(data, hv, hval, true, mb, cap, buf, fbase, rtree, spl, fill, cnt, slotb, nfl,
+            k2_tile<TR, NT, E, 0>(data, hv, hval, true, mb, cap, buf, nbl, rtree, spl, fill, cnt, slotb, nfl,
                            &s_nflushed, tp.logk, tp.kprime, tp.eq, nullptr, nullptr, nullptr, df);
         }
         k2_drain<TR, E>(buf, df);
@@ -471,7 +476,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
         if (tid == 0) s_spbase = atomicAdd((unsigned long long*)A.spill_ctr, (unsigned long long)total);
         __syncthreads();
         if (tid < (u32)MAXK) {
-            A.s_count[(u64)sidx * MAXK + tid] = cnt[tid];
+            A.s_count[(u64)sidx * MAXK + tid] = nbl[tid] * (u32)B + cnt[tid];
             A.s_fill[(u64)sidx * MAXK + tid] = f;
             A.s_spoff[(u64)sidx * MAXK + tid] = excl;
             slotb[tid] = excl;
