@@ -313,11 +313,13 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
         //    its place by counting the cell's elements that precede it (smaller key, or equal
         //    key and lower rank) -- all elements in parallel; larger cells (duplicates,
         //    clusters) are finished by insertion sort by their owner thread.
+        // With span < ncell every cell holds a single key value: nothing to order.
+        const bool exact = mul == 0;
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             const u32 idx = j * NT + tid;
             u32 fin = 0xFFFFFFFFu;  // final position (replaces cell | rank in cr[j])
-            if (idx < n) {
+            if (idx < n && !exact) {
                 const u32 c = cr[j] & 0xFFFFu, r = cr[j] >> 16;
                 const u32 s0 = cnt[cpad(c)], m = cnt[cpad(c + 1)] - s0;
                 if (m <= CELL_SMALL) {
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
         for (int j = 0; j < E; ++j)
             if (cr[j] != 0xFFFFFFFFu) X[cr[j]] = v[j];
         u32 budget = CELL_FIX_BUDGET;
-        for (u32 k = 0; k < cpt; ++k) {
+        for (u32 k = 0; k < cpt && !exact; ++k) {
             if (c0 + k >= ncell) break;
             const u32 s0 = cnt[cpad(c0 + k)], s1 = cnt[cpad(c0 + k + 1)];
             if (s1 - s0 <= CELL_SMALL) continue;
