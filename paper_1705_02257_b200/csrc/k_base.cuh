@@ -294,15 +294,26 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
         __syncthreads();
         u32 base = incl - sum;
         for (u32 ww = 0; ww < w; ++ww) base += s_wsum[ww];
+        u32 bigwork = 0;  // insertion work the large cells would need (~m^2 / 4 each)
         for (u32 k = 0, run = base; k < cpt; ++k) {
             if (c0 + k < ncell) {
                 const u32 x = cnt[cpad(c0 + k)];
                 cnt[cpad(c0 + k)] = run;
                 run += x;
+                if (x > CELL_SMALL) bigwork += x * x / 4;
             }
         }
         if (tid == NT - 1) cnt[cpad(ncell)] = n;  // end of the last cell
+        if (bigwork && mul) atomicAdd(&s_flag, bigwork);
         __syncthreads();
+        if (s_flag > CELL_FIX_BUDGET) {
+            // clustered keys (heavy duplicates in few cells): leave the leaf to the merge sort
+            if (tid == 0) {
+                const u32 q = atomicAdd(fb_count, 1u);
+                if (q < fb_cap) fb_queue[q] = td;
+            }
+            continue;
+        }
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             const u32 idx = j * NT + tid;
@@ -354,9 +365,9 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
                 X[q] = x;
             }
         }
-        if (!budget) s_flag = 1;
+        if (!budget) s_flag = 0xFFFFFFFFu;
         __syncthreads();
-        if (s_flag) {
+        if (s_flag == 0xFFFFFFFFu) {
             // too much insertion work: hand the untouched leaf to the merge sort
             if (tid == 0) {
                 const u32 q = atomicAdd(fb_count, 1u);
