@@ -201,16 +201,30 @@ __device__ __forceinline__ void k2_bucket_keys(const u64 (&key)[E], u32 valid, c
     u32 a[E];
     const u32 cofs = (threadIdx.x & (TREE_COPIES - 1)) * 8u;
     const u32 t0 = 0u - cofs, t1 = TREE_NODE_BYTES - cofs;
-    const u64 root = tree[cofs / 8 + TREE_COPIES];
     const u32 sb = (u32)__cvta_generic_to_shared(tree);
-#pragma unroll
-    for (int e = 0; e < E; ++e) a[e] = (key[e] >= root ? 3u : 2u) * TREE_NODE_BYTES + cofs;
     if (LOGK == 8) {
+        // levels 0-2 from registers (nodes 1..7, the same for every lane), then 3-7 from
+        // the replicated tree in shared memory
+        const u64 n1 = tree[1 * TREE_COPIES], n2 = tree[2 * TREE_COPIES], n3 = tree[3 * TREE_COPIES];
+        const u64 n4 = tree[4 * TREE_COPIES], n5 = tree[5 * TREE_COPIES], n6 = tree[6 * TREE_COPIES],
+                  n7 = tree[7 * TREE_COPIES];
 #pragma unroll
-        for (int l = 1; l < 8; ++l)
+        for (int e = 0; e < E; ++e) {
+            const bool p0 = key[e] >= n1;
+            const bool p1 = key[e] >= (p0 ? n3 : n2);
+            const u64 m2 = p0 ? (p1 ? n7 : n6) : (p1 ? n5 : n4);
+            const bool p2 = key[e] >= m2;
+            const u32 j = 8u + (p0 ? 4u : 0u) + (p1 ? 2u : 0u) + (p2 ? 1u : 0u);
+            a[e] = j * TREE_NODE_BYTES + cofs;
+        }
+#pragma unroll
+        for (int l = 3; l < 8; ++l)
 #pragma unroll
             for (int e = 0; e < E; ++e) descend_step_nb(key[e], sb, a[e], t0, t1);
     } else {
+        const u64 root = tree[cofs / 8 + TREE_COPIES];
+#pragma unroll
+        for (int e = 0; e < E; ++e) a[e] = (key[e] >= root ? 3u : 2u) * TREE_NODE_BYTES + cofs;
         for (u32 l = 1; l < logk; ++l)
 #pragma unroll
             for (int e = 0; e < E; ++e) descend_step_nb(key[e], sb, a[e], t0, t1);
