@@ -181,37 +181,40 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
 // Leaves of up to 8192 elements (8/16-byte types) are sorted by one CTA in shared memory.
 // A leaf's keys already lie between two splitters, so one more distribution step needs no
 // splitters: the key range [kmin, kmax] is cut into 2^cb >= n equal cells by the
-// order-preserving map floor((key - kmin) * 2^cb / (kmax - kmin + 1)).  Then, as in the paper
-// (distribution down to tiny subproblems, finished by insertion sort):
+// order-preserving map floor((key - kmin) * 2^cb / (kmax - kmin + 1)).  Then, as in the
+// paper (distribution down to tiny subproblems, finished by insertion sort):
 //   1. coalesced load into registers, the key range (warp shuffles + shared atomics);
 //   2. cell of every element; its rank inside the cell is the value a shared-memory
 //      atomic increment of the cell counter returns (order inside a cell is irrelevant);
-//   3. exclusive scan of the cell counts (each thread owns a run of cells), scatter of
-//      every element to base[cell] + rank;
-//   4. the elements of a cell (about one per cell on average) are put in order: each
-//      element of a small cell counts the cell's elements preceding it; a large cell
-//      (duplicates, clustered keys) is finished by insertion sort in place;
+//   3. exclusive scan of the cell counts -- thread t owns the run of cells [tE, tE+E), read
+//      and written with 128-bit accesses (the counter array has 4 pad words after each
+//      run, which also makes those accesses conflict-free) -- and the scatter of every
+//      element to base[cell] + rank;
+//   4. each thread orders the cells of its run (about one element per cell on average) by
+//      insertion sort in place;
 //   5. coalesced write-back.
-// A leaf whose cells would need too much insertion work (keys clustered far below the
-// resolution of the cells) is handed to the merge-sort kernel (fallback queue) untouched.
+// When every cell is a single key value (span < cells) step 4 has nothing to do.  A leaf
+// whose cells would need too much insertion work (keys clustered far below the resolution
+// of the cells, e.g. heavy duplicates) is handed to the merge-sort kernel (fallback queue)
+// untouched.
 template <class TR, int NT, int E>
 struct CellBase {
     static constexpr u32 TILE = NT * E;                  // a power of two
-    static constexpr u32 CPT = TILE / NT;                // cells per thread at most (= E)
     static constexpr size_t x_bytes = (size_t)TILE * sizeof(typename TR::V);
-    static constexpr size_t cnt_bytes = (size_t)(TILE + TILE / 16 + 2) * 4;
+    static constexpr size_t cnt_bytes = (size_t)((E + 4) * NT + 8) * 4;
     static constexpr size_t smem = x_bytes + cnt_bytes;
 };
-__device__ __forceinline__ u32 cpad(u32 c) { return c + (c >> 4); }
-constexpr u32 CELL_FIX_BUDGET = 4096;  // insertion-sort moves per thread before falling back
-constexpr u32 CELL_SMALL = 16;         // cells up to this size are ordered by parallel counting
+template <int E>
+__device__ __forceinline__ u32 cpad(u32 c) { return c + 4u * (c / E); }
+constexpr u32 CELL_FIX_BUDGET = 4096;  // insertion-sort moves per leaf and thread before falling back
 
 template <class TR, int NT, int E>
-__global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 ? 2 : 1)) k_base_cell(const TaskDesc* tasks, u32 ntasks, void* vdata,
-                                                  TaskDesc* fb_queue, u32* fb_count, u32 fb_cap) {
+__global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 ? 2 : 1))
+    k_base_cell(const TaskDesc* tasks, u32 ntasks, void* vdata, TaskDesc* fb_queue, u32* fb_count, u32 fb_cap) {
     typedef typename TR::V V;
     typedef CellBase<TR, NT, E> CB;
     constexpr int NW = NT / 32;
+    static_assert(E % 4 == 0, "cell runs are read as 128-bit vectors");
     extern __shared__ __align__(16) unsigned char smc[];
     V* X = reinterpret_cast<V*>(smc);
     u32* cnt = reinterpret_cast<u32*>(smc + CB::x_bytes);
@@ -219,6 +222,7 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
     __shared__ u32 s_flag, s_wsum[NW];
     V* data = reinterpret_cast<V*>(vdata);
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint4* myrun = reinterpret_cast<uint4*>(cnt + cpad<E>(tid * E));  // this thread's E counters
     for (u32 ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
         const TaskDesc td = tasks[ti];
         const u32 n = (u32)(td.hi - td.lo);
@@ -231,7 +235,8 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
             s_range[1] = 0ull;
             s_flag = 0;
         }
-        for (u32 i = tid; i <= ncell; i += NT) cnt[cpad(i)] = 0;
+#pragma unroll
+        for (int k = 0; k < E / 4; ++k) myrun[k] = make_uint4(0u, 0u, 0u, 0u);
         // 1. load (element j*NT + tid) and the key range
         V v[E];
         u64 kmin = ~0ull, kmax = 0ull;
@@ -273,17 +278,17 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
             if (idx < n) {
                 const u64 x = TR::key(v[j]) - kmin;
                 const u32 c = mul ? (u32)__umul64hi(x, mul) : (u32)x;
-                cr[j] = c | (atomicAdd(&cnt[cpad(c)], 1u) << 16);
+                cr[j] = c | (atomicAdd(&cnt[cpad<E>(c)], 1u) << 16);
             }
         }
         __syncthreads();
-        // 3. exclusive scan of the counts: thread t owns cells [t*cpt, (t+1)*cpt) (the
-        //    counter array is padded by one word per 16 cells: conflict-free runs)
-        const u32 cpt = ncell > NT ? ncell / NT : 1u;
-        const u32 c0 = tid * cpt;
+        // 3. exclusive scan of the counts (own run of E cells, 128-bit accesses)
         u32 sum = 0;
-        for (u32 k = 0; k < cpt; ++k)
-            if (c0 + k < ncell) sum += cnt[cpad(c0 + k)];
+#pragma unroll
+        for (int k = 0; k < E / 4; ++k) {
+            const uint4 q = myrun[k];
+            sum += q.x + q.y + q.z + q.w;
+        }
         u32 incl = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -294,16 +299,20 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
         __syncthreads();
         u32 base = incl - sum;
         for (u32 ww = 0; ww < w; ++ww) base += s_wsum[ww];
-        u32 bigwork = 0;  // insertion work the large cells would need (~m^2 / 4 each)
-        for (u32 k = 0, run = base; k < cpt; ++k) {
-            if (c0 + k < ncell) {
-                const u32 x = cnt[cpad(c0 + k)];
-                cnt[cpad(c0 + k)] = run;
-                run += x;
-                if (x > CELL_SMALL) bigwork += x * x / 4;
+        u32 bigwork = 0;  // insertion work of this run's cells (~m^2 / 4 for large cells)
+        {
+            u32 run = base;
+#pragma unroll
+            for (int k = 0; k < E / 4; ++k) {
+                uint4 q = myrun[k];
+                u32 x;
+                x = q.x; q.x = run; run += x; if (x > 8) bigwork += x * x / 4;
+                x = q.y; q.y = run; run += x; if (x > 8) bigwork += x * x / 4;
+                x = q.z; q.z = run; run += x; if (x > 8) bigwork += x * x / 4;
+                x = q.w; q.w = run; run += x; if (x > 8) bigwork += x * x / 4;
+                myrun[k] = q;
             }
         }
-        if (tid == NT - 1) cnt[cpad(ncell)] = n;  // end of the last cell
         if (bigwork && mul) atomicAdd(&s_flag, bigwork);
         __syncthreads();
         if (s_flag > CELL_FIX_BUDGET) {
@@ -317,64 +326,34 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             const u32 idx = j * NT + tid;
-            if (idx < n) X[cnt[cpad(cr[j] & 0xFFFFu)] + (cr[j] >> 16)] = v[j];
+            if (idx < n) X[cnt[cpad<E>(cr[j] & 0xFFFFu)] + (cr[j] >> 16)] = v[j];
         }
         __syncthreads();
-        // 4. order inside the cells.  An element of a cell of m <= CELL_SMALL elements finds
-        //    its place by counting the cell's elements that precede it (smaller key, or equal
-        //    key and lower rank) -- all elements in parallel; larger cells (duplicates,
-        //    clusters) are finished by insertion sort by their owner thread.
-        // With span < ncell every cell holds a single key value: nothing to order.
-        const bool exact = mul == 0;
+        // 4. insertion sort inside the cells of this thread's run; nothing
+        //    to do when every cell is a single key value
+        if (mul && tid * E < ncell) {
+            // end of the run: base of the next thread's first cell, or n
+            const u32 rend = (tid + 1) * E < ncell ? cnt[cpad<E>((tid + 1) * E)] : n;
 #pragma unroll
-        for (int j = 0; j < E; ++j) {
-            const u32 idx = j * NT + tid;
-            u32 fin = 0xFFFFFFFFu;  // final position (replaces cell | rank in cr[j])
-            if (idx < n && !exact) {
-                const u32 c = cr[j] & 0xFFFFu, r = cr[j] >> 16;
-                const u32 s0 = cnt[cpad(c)], m = cnt[cpad(c + 1)] - s0;
-                if (m <= CELL_SMALL) {
-                    const u64 kv = TR::key(v[j]);
-                    u32 before = 0;
-                    for (u32 q = 0; q < m; ++q) {
-                        const u64 ke = TR::key(X[s0 + q]);
-                        before += (ke < kv || (ke == kv && q < r)) ? 1u : 0u;
+            for (int k4 = 0; k4 < E / 4; ++k4) {
+                const uint4 q = myrun[k4];
+                const u32 bq[5] = {q.x, q.y, q.z, q.w, k4 + 1 < E / 4 ? myrun[k4 + 1].x : rend};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const u32 s0 = bq[k], s1 = bq[k + 1];
+                    for (u32 i = s0 + 1; i < s1; ++i) {
+                        const V x = X[i];
+                        u32 qq = i;
+                        while (qq > s0 && TR::less(x, X[qq - 1])) {
+                            X[qq] = X[qq - 1];
+                            --qq;
+                        }
+                        X[qq] = x;
                     }
-                    fin = s0 + before;
                 }
             }
-            cr[j] = fin;
         }
         __syncthreads();
-#pragma unroll
-        for (int j = 0; j < E; ++j)
-            if (cr[j] != 0xFFFFFFFFu) X[cr[j]] = v[j];
-        u32 budget = CELL_FIX_BUDGET;
-        for (u32 k = 0; k < cpt && !exact; ++k) {
-            if (c0 + k >= ncell) break;
-            const u32 s0 = cnt[cpad(c0 + k)], s1 = cnt[cpad(c0 + k + 1)];
-            if (s1 - s0 <= CELL_SMALL) continue;
-            for (u32 i = s0 + 1; i < s1 && budget; ++i) {
-                const V x = X[i];
-                u32 q = i;
-                while (q > s0 && TR::less(x, X[q - 1]) && budget) {
-                    X[q] = X[q - 1];
-                    --q;
-                    --budget;
-                }
-                X[q] = x;
-            }
-        }
-        if (!budget) s_flag = 0xFFFFFFFFu;
-        __syncthreads();
-        if (s_flag == 0xFFFFFFFFu) {
-            // too much insertion work: hand the untouched leaf to the merge sort
-            if (tid == 0) {
-                const u32 q = atomicAdd(fb_count, 1u);
-                if (q < fb_cap) fb_queue[q] = td;
-            }
-            continue;
-        }
         // 5. write back
         for (u32 i = tid; i < n; i += NT) g[i] = X[i];
     }
