@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
 //      run, which also makes those accesses conflict-free) -- and the scatter of every
 //      element to base[cell] + rank;
 //   4. each thread orders the cells of its run (about one element per cell on average) by
-//      insertion sort in place;
+//      one insertion sort of the run's positions (the cells are already in order);
 //   5. coalesced write-back.
 // When every cell is a single key value (span < cells) step 4 has nothing to do.  A leaf
 // whose cells would need too much insertion work (keys clustered far below the resolution
@@ -332,25 +332,19 @@ __global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 
         // 4. insertion sort inside the cells of this thread's run; nothing
         //    to do when every cell is a single key value
         if (mul && tid * E < ncell) {
-            // end of the run: base of the next thread's first cell, or n
-            const u32 rend = (tid + 1) * E < ncell ? cnt[cpad<E>((tid + 1) * E)] : n;
-#pragma unroll
-            for (int k4 = 0; k4 < E / 4; ++k4) {
-                const uint4 q = myrun[k4];
-                const u32 bq[5] = {q.x, q.y, q.z, q.w, k4 + 1 < E / 4 ? myrun[k4 + 1].x : rend};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const u32 s0 = bq[k], s1 = bq[k + 1];
-                    for (u32 i = s0 + 1; i < s1; ++i) {
-                        const V x = X[i];
-                        u32 qq = i;
-                        while (qq > s0 && TR::less(x, X[qq - 1])) {
-                            X[qq] = X[qq - 1];
-                            --qq;
-                        }
-                        X[qq] = x;
-                    }
+            // The run's positions [rs, re) hold its cells in cell order, and the cell map is
+            // monotone: an insertion sort of the whole run by key moves elements only inside
+            // their own cell, with no cell boundaries to track.
+            const u32 rs = myrun[0].x;
+            const u32 re = (tid + 1) * E < ncell ? cnt[cpad<E>((tid + 1) * E)] : n;
+            for (u32 i = rs + 1; i < re; ++i) {
+                const V x = X[i];
+                u32 q = i;
+                while (q > rs && TR::less(x, X[q - 1])) {
+                    X[q] = X[q - 1];
+                    --q;
                 }
+                if (q != i) X[q] = x;
             }
         }
         __syncthreads();
