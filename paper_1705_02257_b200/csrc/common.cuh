@@ -21,6 +21,9 @@ constexpr int K3_THREADS = 256;      // block permutation CTA
 #ifndef IPS4O_K3_SLOTS
 #define IPS4O_K3_SLOTS 4
 #endif
+#ifndef IPS4O_K3_ACQUIRE
+#define IPS4O_K3_ACQUIRE 0
+#endif
 constexpr int K3_SLOTS = IPS4O_K3_SLOTS;  // independent chains per warp
 #ifndef IPS4O_K3_MINB
 #define IPS4O_K3_MINB (IPS4O_K3_SLOTS <= 2 ? 6 : IPS4O_K3_SLOTS <= 4 ? 4 : 2)

@@ -319,10 +319,16 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A) {
                 u64 op = 1ull << 32;
                 u64* wp = ctl_wr(A.wr, t, my_dest);
                 if (my_take) {
-                    // the reader announcement is performed before the take (acquire: no later
-                    // memory operation of this thread is performed before it)
+                    // the reader announcement is performed before the take: the take's operand
+                    // depends on the value the announcement returns (the count never reaches
+                    // 2^31, so the added term is 0)
+#if IPS4O_K3_ACQUIRE
                     atom_add_acquire_u32(ctl_readers(A.wr, t, my_pb), 1u);
                     op = ~0ull;
+#else
+                    const u32 r0 = atomicAdd(ctl_readers(A.wr, t, my_pb), 1u);
+                    op = ~0ull + (u64)(r0 >> 31);
+#endif
                     wp = ctl_wr(A.wr, t, my_pb);
                 }
                 my_old = atomicAdd((unsigned long long*)wp, op);
