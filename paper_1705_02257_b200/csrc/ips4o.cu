@@ -525,7 +525,13 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
         }
     }
 #endif
-    LAUNCH(KK_CLEANUP, (k_cleanup<TR><<<T * MAXK, K4_THREADS, 0, st>>>(A)));
+    if (T * MAXK >= 32u * g_ws.num_sms) {
+        // many buckets: one warp each
+        const u32 nw = T * MAXK, want = (nw + K4_WARPS - 1) / K4_WARPS;
+        LAUNCH(KK_CLEANUP, (k_cleanup<TR><<<std::min<u32>(want, 8u * g_ws.num_sms), K4_THREADS, 0, st>>>(A)));
+    } else {
+        LAUNCH(KK_CLEANUP, (k_cleanup_cta<TR><<<T * MAXK, K4_THREADS, 0, st>>>(A)));
+    }
     CK(cudaMemcpyAsync(g_ws.h_ctr, g_ws.ctr, CTR_N * 4 + 16, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     g_stats.host_syncs++;

@@ -1,6 +1,6 @@
 // k_cleanup.cuh -- K4: cleanup of partial blocks (§4.3) and task emission.
 //
-// One CTA per (task, bucket), taken in order through an atomic ticket so that a bucket's
+// One warp per (task, bucket), taken in order through an atomic ticket so that a bucket's
 // predecessor is always already running.  For bucket i:
 //   empty slots  = its head [e_i, min(d_i, e_{i+1})) and [min(w_i, e_{i+1}), e_{i+1});
 //   sources      = the overhang of its last written block into the next bucket's head
@@ -17,9 +17,152 @@
 namespace ips4o {
 
 constexpr int K4_MAXSTRIPES = 1024;
+constexpr int K4_WARPS = K4_THREADS / 32;
 
+// One warp per (task, bucket), taken in order through an atomic ticket (a bucket's
+// predecessor always holds a smaller ticket, so it is already running or done).
 template <class TR>
 __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
+    typedef typename TR::V V;
+    constexpr int B = TR::B;
+    __shared__ V s_ovh_all[K4_WARPS][B];
+    __shared__ u32 s_pref_all[K4_WARPS][K4_MAXSTRIPES + 1];
+    const u32 lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    V* s_ovh = s_ovh_all[wi];
+    u32* s_pref = s_pref_all[wi];
+    const u32 nbt = A.ntasks * MAXK;
+    V* data = reinterpret_cast<V*>(A.data);
+    const V* spill = reinterpret_cast<const V*>(A.spill);
+    for (;;) {
+        u32 ticket = 0;
+        if (lane == 0) ticket = atomicAdd(&A.ctr[CTR_TICKET], 1u);
+        ticket = __shfl_sync(0xffffffffu, ticket, 0);
+        if (ticket >= nbt) return;
+        const u32 t = ticket / MAXK, b = ticket % MAXK;
+        const TaskParam tp = A.tp[t];
+        u32* flag = A.cflag + (u64)t * MAXK;
+        if (b >= tp.K) {
+            if (lane == 0) st_release_u32(flag + b, 1u);
+            continue;
+        }
+        const u64* bnd = A.bnd + (u64)t * (MAXK + 1);
+        const u32* dbl = A.dblk + (u64)t * (MAXK + 1);
+        const u64 e0 = bnd[b], e1 = bnd[b + 1];
+        const u32 d = dbl[b];
+        const u32 wfin = (u32)(*ctl_wr(A.wr, t, b) >> 32);
+        const bool own_ovf = A.ovf_owner[t] == (int)b;
+        const u64 db_el = tp.g + (u64)d * B;
+        const u64 in_end = own_ovf ? tp.g + (u64)(tp.nblocks - 1) * B : tp.g + (u64)wfin * B;
+        // overhang of this bucket's last block into the next bucket's head (saved first,
+        // then published: PAPER.md:314-315)
+        const u32 ovl = (in_end > db_el && in_end > e1) ? (u32)(in_end - e1) : 0u;
+        for (u32 k = lane; k < ovl; k += 32) s_ovh[k] = data[e1 + k];
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            st_release_u32(flag + b, 1u);
+        }
+        // spilled partial buffers of every stripe of this task for bucket b
+        const u32 S0 = tp.stripe_begin, NS = tp.nstripes;
+        u32 sp_total = 0;
+        for (u32 base = 0; base < NS; base += 32) {
+            const u32 j = base + lane;
+            const u32 len = j < NS ? A.s_fill[(u64)(S0 + j) * MAXK + b] : 0u;
+            u32 incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (u32)o) incl += y;
+            }
+            if (j < NS) s_pref[j] = sp_total + incl - len;
+            sp_total += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) s_pref[NS] = sp_total;
+        __syncwarp();
+        const u32 nsrc = ovl + sp_total + (own_ovf ? (u32)B : 0u);
+        const u64 hend = db_el < e1 ? db_el : e1;
+        const u64 ts = db_el < e1 ? (in_end < e1 ? in_end : e1) : e1;
+        const u64 hl = hend - e0;
+        const u64 nslots = hl + (e1 - ts);
+        if ((u64)nsrc != nslots) {
+            if (lane == 0) atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_CONSERVE);
+            continue;
+        }
+        // wait until the bucket owning block d-1 (which holds our head) saved its overhang
+        if (lane == 0 && hl > 0 && d >= 1) {
+            const u32 x = d - 1;
+            u32 lo = 0, hi = b;  // largest o < b with dbl[o] <= x
+            while (hi - lo > 1) {
+                const u32 mid = (lo + hi) >> 1;
+                if (dbl[mid] <= x) lo = mid;
+                else hi = mid;
+            }
+            if (lo < b) {
+                while (ld_acquire_u32(flag + lo) == 0u) __nanosleep(100);
+            }
+        }
+        __syncwarp();
+        const V* ovf = reinterpret_cast<const V*>(A.ovf) + (u64)t * B;
+        u32 jcur = 0;  // stripe of the previous source (sources are visited in order)
+        for (u32 k = lane; k < nsrc; k += 32) {
+            V val;
+            if (k < ovl) {
+                val = s_ovh[k];
+            } else if (k - ovl < sp_total) {
+                const u32 kk = k - ovl;
+                u32 lo = jcur, hi = NS;  // last j with s_pref[j] <= kk
+                while (hi - lo > 1) {
+                    const u32 mid = (lo + hi) >> 1;
+                    if (s_pref[mid] <= kk) lo = mid;
+                    else hi = mid;
+                }
+                jcur = lo;
+                const u64 at = A.s_spbase[S0 + lo] + A.s_spoff[(u64)(S0 + lo) * MAXK + b] + (kk - s_pref[lo]);
+                val = spill[at];
+            } else {
+                val = ovf[k - ovl - sp_total];
+            }
+            const u64 dst = (u64)k < hl ? e0 + k : ts + (k - hl);
+            data[dst] = val;
+        }
+        // emit the bucket.  Equality buckets are never recursed into; for
+        // records an equality bucket of key part 0 (equal first 8 key bytes) still has to be
+        // ordered by part 1, so it becomes a task on the next part.
+        if (lane == 0 && A.emit) {
+            const u64 sz = e1 - e0;
+            const bool eqb = tp.eq && (b & 1u);
+            u32 part = tp.part;
+            bool emit = sz > 1;
+            if (eqb) {
+                if (part + 1 < (u32)TR::PARTS) ++part;
+                else emit = false;
+            }
+            if (emit && !eqb && sz == tp.hi - tp.lo) {
+                // no progress: a splitter choice that leaves the whole task in one
+                // interval bucket would recurse forever -- report instead of looping
+                atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_PROGRESS);
+                emit = false;
+            }
+            if (emit) {
+                if (sz <= A.base_cap) {
+                    atomicAdd((unsigned long long*)A.base_elems, (unsigned long long)sz);
+                    const u32 c = base_class(sz);
+                    u32 i = atomicAdd(&A.ctr[CTR_BASE0 + c], 1u);
+                    if (i < A.q_cap) A.q_base[(u64)c * A.q_cap + i] = TaskDesc{e0, e1, 0u, 0u};
+                    else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
+                } else {
+                    u32 i = atomicAdd(&A.ctr[CTR_NEXT], 1u);
+                    if (i < A.q_cap) A.q_next[i] = TaskDesc{e0, e1, part, 0u};
+                    else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
+                }
+            }
+        }
+    }
+}
+
+// Few buckets with many stripes each (the top level): one CTA per bucket.
+template <class TR>
+__global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A) {
     typedef typename TR::V V;
     constexpr int B = TR::B;
     __shared__ V s_ovh[B];
