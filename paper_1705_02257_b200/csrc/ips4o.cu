@@ -322,9 +322,9 @@ static int prepare_kernels(void) {
                                                          K2RecSmem<K2REC_THREADS>::total));
         CK(cudaFuncSetAttribute(k_base_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase::smem));
         CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                K1_SAMPLE_BIG * 8));
+                                (int)(padidx(K1_SAMPLE_BIG) * 8 + 16)));
         CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                K1_SAMPLE * 8));
+                                (int)(padidx(K1_SAMPLE) * 8 + 16)));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_permute<TR>, K3_THREADS, 0));
         if (occ2 < 1 || occ3 < 1) {
             snprintf(g_errbuf, sizeof g_errbuf, "occupancy query returned %d/%d", occ2, occ3);
@@ -337,9 +337,9 @@ static int prepare_kernels(void) {
     } else {
     CK(set_base_attrs<TR>());
     CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            K1_SAMPLE_BIG * 8));
+                            (int)(padidx(K1_SAMPLE_BIG) * 8 + 16)));
     CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            K1_SAMPLE * 8));
+                            (int)(padidx(K1_SAMPLE) * 8 + 16)));
     int occ2 = 0, occ3 = 0;
     if (k2_variant() == 1) CK((k2_setup<TR, K2Cfg1<TR>>(&occ2)));
     else CK((k2_setup<TR, K2Cfg0<TR>>(&occ2)));
@@ -470,9 +470,9 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
         u64 maxn = 0;
         for (u32 i = 0; i < T; ++i) maxn = std::max<u64>(maxn, g_ws.h_tp[i].hi - g_ws.h_tp[i].lo);
         if (maxn >= K1_BIG_TASK)
-            LAUNCH(KK_SAMPLE, (k_sample<TR, K1_SAMPLE_BIG><<<T, K1_THREADS, K1_SAMPLE_BIG * 8, st>>>(A)));
+            LAUNCH(KK_SAMPLE, (k_sample<TR, K1_SAMPLE_BIG><<<T, K1_THREADS, padidx(K1_SAMPLE_BIG) * 8 + 16, st>>>(A)));
         else
-            LAUNCH(KK_SAMPLE, (k_sample<TR, K1_SAMPLE><<<T, K1_THREADS, K1_SAMPLE * 8, st>>>(A)));
+            LAUNCH(KK_SAMPLE, (k_sample<TR, K1_SAMPLE><<<T, K1_THREADS, padidx(K1_SAMPLE) * 8 + 16, st>>>(A)));
     }
     const u32 g2 = std::min<u32>(S, g_ws.k2_blocks);
     if constexpr (TR::S == 100) {

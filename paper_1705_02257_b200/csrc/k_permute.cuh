@@ -18,6 +18,8 @@
 
 namespace ips4o {
 
+constexpr int K2P_MAXST = 1024;  // stripes of one task staged in shared memory by k_prepare
+
 template <class TR>
 __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
     constexpr int B = TR::B;
@@ -27,8 +29,18 @@ __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
     const TaskParam tp = A.tp[t];
     const u32 S0 = tp.stripe_begin, NS = tp.nstripes;
 
-    // bucket size = sum over this task's stripes
+    // bucket size = sum over this task's stripes; the stripes' block
+    // ranges are staged in shared memory for the loops below
+    __shared__ u32 s_sb[K2P_MAXST], s_fe[K2P_MAXST];
+    const bool staged = NS <= (u32)K2P_MAXST;
+    if (staged) {
+        for (u32 j = b; j < NS; j += MAXK) {
+            s_sb[j] = A.sd[S0 + j].sb;
+            s_fe[j] = A.sd[S0 + j].sb + A.s_nfull[S0 + j];
+        }
+    }
     u32 c = 0;
+#pragma unroll 16
     for (u32 j = 0; j < NS; ++j) c += A.s_count[(u64)(S0 + j) * MAXK + b];
     // exclusive scan over the 256 buckets
     u32 incl = c;
@@ -53,18 +65,18 @@ __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
     A.dblk[(u64)t * (MAXK + 1) + b] = d;
     if (b == 0) A.dblk[(u64)t * (MAXK + 1) + MAXK] = tp.nblocks;
     // full blocks inside [d, dn): every stripe holds full blocks [sb, sb+F) then empty ones
+    auto fs_of = [&](u32 j) { return staged ? s_sb[j] : A.sd[S0 + j].sb; };
+    auto fe_of = [&](u32 j) { return staged ? s_fe[j] : A.sd[S0 + j].sb + A.s_nfull[S0 + j]; };
     u32 nf = 0;
     for (u32 j = 0; j < NS; ++j) {
-        const StripeDesc sd = A.sd[S0 + j];
-        const u32 fs = sd.sb, fe = sd.sb + A.s_nfull[S0 + j];
+        const u32 fs = fs_of(j), fe = fe_of(j);
         const u32 lo2 = fs > d ? fs : d, hi2 = fe < dn ? fe : dn;
         if (hi2 > lo2) nf += hi2 - lo2;
     }
     // Appendix A: holes (empty blocks) inside [d, d+nf) must be filled
     u32 fullpre = 0;
     for (u32 j = 0; j < NS; ++j) {
-        const StripeDesc sd = A.sd[S0 + j];
-        const u32 fs = sd.sb, fe = sd.sb + A.s_nfull[S0 + j];
+        const u32 fs = fs_of(j), fe = fe_of(j);
         const u32 lo2 = fs > d ? fs : d, hi2 = fe < d + nf ? fe : d + nf;
         if (hi2 > lo2) fullpre += hi2 - lo2;
     }
@@ -92,16 +104,49 @@ __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
     if (lane == 0) A.done[(u64)t * (MAXK / 32) + w] = bal;
     if (b == 0) {
         A.ovf_owner[t] = -1;
-        // per-task stripe prefixes of full / empty block counts (for k_moves)
-        u32 pf = 0, pe = 0;
-        for (u32 j = 0; j < NS; ++j) {
+    }
+    // per-task stripe prefixes of full / empty block counts (for k_moves): block-wide scans
+    // over the stripes, 256 at a time
+    __shared__ u32 s_wf[MAXK / 32], s_we[MAXK / 32];
+    u32 pf = 0, pe = 0;
+    for (u32 base = 0; base < NS; base += MAXK) {
+        const u32 j = base + b;
+        u32 F = 0, Em = 0;
+        if (j < NS) {
             const StripeDesc sd = A.sd[S0 + j];
-            const u32 F = A.s_nfull[S0 + j];
-            A.prefF[S0 + j] = pf;
-            A.prefE[S0 + j] = pe;
-            pf += F;
-            pe += (sd.se - sd.sb) - F;
+            F = A.s_nfull[S0 + j];
+            Em = (sd.se - sd.sb) - F;
         }
+        u32 iF = F, iE = Em;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 yF = __shfl_up_sync(0xffffffffu, iF, o), yE = __shfl_up_sync(0xffffffffu, iE, o);
+            if (lane >= (u32)o) {
+                iF += yF;
+                iE += yE;
+            }
+        }
+        __syncthreads();
+        if (lane == 31) {
+            s_wf[w] = iF;
+            s_we[w] = iE;
+        }
+        __syncthreads();
+        u32 oF = 0, oE = 0, tF = 0, tE = 0;
+        for (u32 ww = 0; ww < MAXK / 32; ++ww) {
+            if (ww < w) {
+                oF += s_wf[ww];
+                oE += s_we[ww];
+            }
+            tF += s_wf[ww];
+            tE += s_we[ww];
+        }
+        if (j < NS) {
+            A.prefF[S0 + j] = pf + oF + iF - F;
+            A.prefE[S0 + j] = pe + oE + iE - Em;
+        }
+        pf += tF;
+        pe += tE;
     }
 }
 
@@ -120,6 +165,10 @@ __device__ __forceinline__ u32 last_le(u32 n, u64 x, F key) {
 template <class TR>
 __global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
     constexpr int B = TR::B;
+    // the task's per-stripe block counts and the per-bucket move ranges, staged in shared
+    // memory: the searches below are then shared-memory lookups
+    __shared__ u32 s_sb[K2P_MAXST], s_se[K2P_MAXST], s_F[K2P_MAXST], s_pE[K2P_MAXST], s_pF[K2P_MAXST];
+    __shared__ u32 s_mov[MAXK + 1], s_d[MAXK + 1], s_nf[MAXK];
     const u32 t = blockIdx.y;
     const u32 lane = threadIdx.x & 31;
     const u32 wib = threadIdx.x >> 5;
@@ -127,32 +176,52 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
     const u32 S0 = tp.stripe_begin, NS = tp.nstripes;
     const u32* mov = A.mov + (u64)t * (MAXK + 1);
     const u32 M = mov[MAXK];
+    if (M == 0 || blockIdx.x * (blockDim.x >> 5) >= M) return;
+    const bool staged = NS <= (u32)K2P_MAXST;
+    for (u32 i = threadIdx.x; i <= (u32)MAXK; i += blockDim.x) {
+        s_mov[i] = mov[i];
+        s_d[i] = A.dblk[(u64)t * (MAXK + 1) + i];
+        if (i < (u32)MAXK) s_nf[i] = A.nfb[(u64)t * MAXK + i];
+    }
+    if (staged) {
+        for (u32 j = threadIdx.x; j < NS; j += blockDim.x) {
+            const StripeDesc sd = A.sd[S0 + j];
+            s_sb[j] = sd.sb;
+            s_se[j] = sd.se;
+            s_F[j] = A.s_nfull[S0 + j];
+            s_pE[j] = A.prefE[S0 + j];
+            s_pF[j] = A.prefF[S0 + j];
+        }
+    }
+    __syncthreads();
+    auto sb_of = [&](u32 j) { return staged ? s_sb[j] : A.sd[S0 + j].sb; };
+    auto se_of = [&](u32 j) { return staged ? s_se[j] : A.sd[S0 + j].se; };
+    auto F_of = [&](u32 j) { return staged ? s_F[j] : A.s_nfull[S0 + j]; };
+    auto pE_of = [&](u32 j) { return staged ? s_pE[j] : A.prefE[S0 + j]; };
+    auto pF_of = [&](u32 j) { return staged ? s_pF[j] : A.prefF[S0 + j]; };
     const u32 nwarps = gridDim.x * (blockDim.x >> 5);
     char* base = reinterpret_cast<char*>(A.data) + tp.g * TR::S;
     for (u32 m = blockIdx.x * (blockDim.x >> 5) + wib; m < M; m += nwarps) {
         u64 src = 0, dst = 0;
         if (lane == 0) {
-            const u32 b = last_le(MAXK, m, [&](u32 i) { return (u64)mov[i]; });
-            const u32 k = m - mov[b];
-            const u32 d = A.dblk[(u64)t * (MAXK + 1) + b];
-            const u32 nf = A.nfb[(u64)t * MAXK + b];
+            const u32 b = last_le(MAXK, m, [&](u32 i) { return (u64)s_mov[i]; });
+            const u32 k = m - s_mov[b];
+            const u32 d = s_d[b];
+            const u32 nf = s_nf[b];
             // k-th empty block at or after d
-            const u32 jd = last_le(NS, d, [&](u32 i) { return (u64)A.sd[S0 + i].sb; });
-            const StripeDesc sdd = A.sd[S0 + jd];
-            const u32 Fd = A.s_nfull[S0 + jd];
-            const u32 se_d = d < sdd.se ? d : sdd.se;
-            const u32 eb = A.prefE[S0 + jd] + (se_d > sdd.sb + Fd ? se_d - (sdd.sb + Fd) : 0u) + k;
-            const u32 je = last_le(NS, eb, [&](u32 i) { return (u64)A.prefE[S0 + i]; });
-            const StripeDesc sde = A.sd[S0 + je];
-            dst = sde.sb + A.s_nfull[S0 + je] + (eb - A.prefE[S0 + je]);
+            const u32 jd = last_le(NS, d, [&](u32 i) { return (u64)sb_of(i); });
+            const u32 sbd = sb_of(jd), Fd = F_of(jd), sed = se_of(jd);
+            const u32 se_d = d < sed ? d : sed;
+            const u32 eb = pE_of(jd) + (se_d > sbd + Fd ? se_d - (sbd + Fd) : 0u) + k;
+            const u32 je = last_le(NS, eb, [&](u32 i) { return (u64)pE_of(i); });
+            dst = sb_of(je) + F_of(je) + (eb - pE_of(je));
             // k-th full block at or after d + nf
             const u32 x = d + nf;
-            const u32 jx = last_le(NS, x, [&](u32 i) { return (u64)A.sd[S0 + i].sb; });
-            const StripeDesc sdx = A.sd[S0 + jx];
-            const u32 Fx = A.s_nfull[S0 + jx];
-            const u32 fb = A.prefF[S0 + jx] + (x - sdx.sb < Fx ? x - sdx.sb : Fx) + k;
-            const u32 jf = last_le(NS, fb, [&](u32 i) { return (u64)A.prefF[S0 + i]; });
-            src = A.sd[S0 + jf].sb + (fb - A.prefF[S0 + jf]);
+            const u32 jx = last_le(NS, x, [&](u32 i) { return (u64)sb_of(i); });
+            const u32 sbx = sb_of(jx), Fx = F_of(jx);
+            const u32 fb = pF_of(jx) + (x - sbx < Fx ? x - sbx : Fx) + k;
+            const u32 jf = last_le(NS, fb, [&](u32 i) { return (u64)pF_of(i); });
+            src = sb_of(jf) + (fb - pF_of(jf));
         }
         src = __shfl_sync(0xffffffffu, src, 0);
         dst = __shfl_sync(0xffffffffu, dst, 0);

@@ -8,6 +8,7 @@
 // front of the array: same splitters, no writes to the input.
 #pragma once
 #include "common.cuh"
+#include "k_base.cuh"
 
 namespace ips4o {
 
@@ -48,6 +49,13 @@ __device__ void build_tree_block(const u64* s_dist, u32 nd, u32 eq, u64* g_tree,
     }
 }
 
+// the sample's keys as a base-case element type (order-preserving u64 images)
+struct TKey {
+    typedef u64 V;
+    __device__ __forceinline__ static bool less(V a, V b) { return a < b; }
+    __host__ __device__ __forceinline__ static V pad() { return ~0ull; }
+};
+
 template <class TR, int SAMPLE>
 __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
     typedef typename TR::V V;
@@ -77,7 +85,9 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
     const u64 acap = (n + 1) / k;
     if ((u64)alpha > acap) alpha = (u32)(acap > 0 ? acap : 1);
     const u32 m = alpha * k - 1;
-    // stratified random sample without replacement: one element per stratum
+    // stratified random sample without replacement: one element per stratum; sorted in
+    // shared memory by the block merge sort of the base case (register networks of
+    // SAMPLE/K1_THREADS keys per thread + merge-path passes), padded with the largest key
     for (u32 j = threadIdx.x; j < (u32)SAMPLE; j += blockDim.x) {
         u64 key = ~0ull;
         if (j < m) {
@@ -86,34 +96,19 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
             u64 r = mix64(A.seed ^ mix64(lo * 0x9E3779B97F4A7C15ull + j));
             key = TR::key(data[a + r % (b - a)], tp->part);
         }
-        keys[j] = key;
+        keys[padidx(j)] = key;
     }
     __syncthreads();
-    // bitonic sort of the sampled keys in shared memory
-    for (u32 kk = 2; kk <= (u32)SAMPLE; kk <<= 1) {
-        for (u32 jj = kk >> 1; jj > 0; jj >>= 1) {
-            for (u32 p = threadIdx.x; p < (u32)SAMPLE / 2; p += blockDim.x) {
-                u32 i = 2 * p - (p & (jj - 1));
-                u32 x = i + jj;
-                bool up = (i & kk) == 0;
-                u64 a = keys[i], b = keys[x];
-                if ((a > b) == up) {
-                    keys[i] = b;
-                    keys[x] = a;
-                }
-            }
-            __syncthreads();
-        }
-    }
+    block_sort_smem<TKey, K1_THREADS, SAMPLE / K1_THREADS>(keys, (u32)SAMPLE);
     // equidistant picks s_i = S[i*alpha - 1]; duplicates?
     if (threadIdx.x == 0) s_flag = 0;
     __syncthreads();
     for (u32 i = 1 + threadIdx.x; i + 1 < k; i += blockDim.x)
-        if (keys[i * alpha - 1] == keys[(i + 1) * alpha - 1]) s_flag = 1;
+        if (keys[padidx(i * alpha - 1)] == keys[padidx((i + 1) * alpha - 1)]) s_flag = 1;
     __syncthreads();
     u32 eq = s_flag;
     if (!eq) {
-        for (u32 i = threadIdx.x; i + 1 < k; i += blockDim.x) dist[i] = keys[(i + 1) * alpha - 1];
+        for (u32 i = threadIdx.x; i + 1 < k; i += blockDim.x) dist[i] = keys[padidx((i + 1) * alpha - 1)];
         if (threadIdx.x == 0) s_nd = k - 1;
     } else {
         // Equality buckets.  Take k/2-1 equidistant picks so
@@ -123,7 +118,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
         if (threadIdx.x == 0) {
             u32 nd = 0;
             for (u32 i = 1; i < k2; ++i) {
-                u64 v = keys[i * a2 - 1];
+                u64 v = keys[padidx(i * a2 - 1)];
                 if (nd == 0 || dist[nd - 1] != v) dist[nd++] = v;
             }
             s_nd = nd;
