@@ -398,15 +398,22 @@ static LevelArgs level_args(void* data, u32 T, u32 S, int emit, u64 seed) {
     return A;
 }
 
+// Stripe length of a level: about 3 stripes per SM over the level's Ntot elements (at
+// least MIN_STRIPE), a whole number of blocks.
+template <class TR>
+static u64 stripe_len(u64 Ntot) {
+    const u64 target = std::max<u64>(1, std::min<u64>(MAXS, 3ull * g_ws.num_sms));
+    u64 L = std::max<u64>((Ntot + target - 1) / target, MIN_STRIPE);
+    return (L + TR::B - 1) / TR::B * TR::B;
+}
+// number of stripes plan_batch creates for a task of `size` elements (an upper bound: the
+// task's aligned main part is at most size)
+static u32 stripes_for(u64 size, u64 L) { return (u32)std::max<u64>(1, (size + L / 2) / L); }
+
 // Plan the stripes of a batch of tasks (host) into g_ws.h_tp / h_sd / h_order.
 template <class TR>
-static void plan_batch(const TaskDesc* tasks, u32 T, uintptr_t base_addr, u32* S_out) {
+static void plan_batch(const TaskDesc* tasks, u32 T, uintptr_t base_addr, u64 L, u32* S_out) {
     constexpr int B = TR::B;
-    u64 N = 0;
-    for (u32 i = 0; i < T; ++i) N += tasks[i].hi - tasks[i].lo;
-    const u64 target = std::max<u64>(1, std::min<u64>(MAXS, 3ull * g_ws.num_sms));
-    u64 L = std::max<u64>((N + target - 1) / target, MIN_STRIPE);
-    L = (L + B - 1) / B * B;
     u32 S = 0;
     for (u32 i = 0; i < T; ++i) {
         const u64 lo = tasks[i].lo, hi = tasks[i].hi;
@@ -444,15 +451,6 @@ static void plan_batch(const TaskDesc* tasks, u32 T, uintptr_t base_addr, u32* S
         return (g_ws.h_sd[a].end - g_ws.h_sd[a].begin) > (g_ws.h_sd[b].end - g_ws.h_sd[b].begin);
     });
     *S_out = S;
-}
-
-// number of stripes plan_batch will create for a task, for batching decisions
-template <class TR>
-static u32 stripes_for(u64 size, u64 N) {
-    const u64 target = std::max<u64>(1, std::min<u64>(MAXS, 3ull * g_ws.num_sms));
-    u64 L = std::max<u64>((N + target - 1) / target, MIN_STRIPE);
-    L = (L + TR::B - 1) / TR::B * TR::B;
-    return (u32)std::max<u64>(1, (size + L / 2) / L) + 1;
 }
 
 // One distribution level over T <= MAXT tasks (already planned into h_tp/h_sd).
@@ -623,19 +621,20 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
                   [](const TaskDesc& a, const TaskDesc& b) { return a.hi - a.lo > b.hi - b.lo; });
         u64 Ntot = 0;
         for (auto& t : cur) Ntot += t.hi - t.lo;
+        const u64 Lst = stripe_len<TR>(Ntot);
         size_t i0 = 0;
         while (i0 < cur.size()) {
             size_t i1 = i0;
             u32 sacc = 0;
             while (i1 < cur.size() && i1 - i0 < MAXT) {
-                u32 s = stripes_for<TR>(cur[i1].hi - cur[i1].lo, Ntot);
+                u32 s = stripes_for(cur[i1].hi - cur[i1].lo, Lst);
                 if (sacc + s > MAXS && i1 > i0) break;
                 sacc += s;
                 ++i1;
             }
             const u32 T = (u32)(i1 - i0);
             u32 S = 0;
-            plan_batch<TR>(&cur[i0], T, (uintptr_t)data, &S);
+            plan_batch<TR>(&cur[i0], T, (uintptr_t)data, Lst, &S);
             if (S > MAXS) {
                 snprintf(g_errbuf, sizeof g_errbuf, "stripe planning overflow");
                 return IPS4O_EINTERNAL;
@@ -745,7 +744,7 @@ static int debug_partition_impl(void* d, u64 n, const void* h_spl, u32 nspl, int
     CK(cudaMemcpyAsync(g_ws.dsplit, keys.data(), 8ull * nspl, cudaMemcpyHostToDevice, st));
     TaskDesc td{0, n, 0u, 0u};
     u32 S = 0;
-    plan_batch<TR>(&td, 1, (uintptr_t)d, &S);
+    plan_batch<TR>(&td, 1, (uintptr_t)d, stripe_len<TR>(n), &S);
     rc = run_level<TR>(d, 1, S, st, true, nspl, (u32)eq, 0, 1);
     if (rc) return rc;
     g_stats.levels = 1;
