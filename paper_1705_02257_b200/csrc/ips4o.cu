@@ -266,6 +266,18 @@ static cudaError_t set_base_attr1() {
     return cudaFuncSetAttribute(k_base_merge<TR, TH, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)BaseClass<TR, TH, 16>::smem);
 }
+// cell base-case configurations of the size classes <= 2048 and <= 4096 (threads,
+// elements per thread); the <= 8192 class uses (512, 16)
+#ifndef IPS4O_CELL_SMALL
+#define IPS4O_CELL_SMALL 1
+#endif
+// 8-byte types: 16 elements per thread in small CTAs (more leaves in flight per SM);
+// 16-byte types: 8 per thread (register budget)
+template <class TR> struct CellCfg {
+    static constexpr bool small = IPS4O_CELL_SMALL && TR::S == 8;
+    static constexpr int NT0 = small ? 128 : 256, E0 = small ? 16 : 8;
+    static constexpr int NT1 = small ? 256 : 512, E1 = small ? 16 : 8;
+};
 template <class TR, int NT, int E>
 static cudaError_t set_cell_attr() {
     return cudaFuncSetAttribute(k_base_cell<TR, NT, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -274,8 +286,8 @@ static cudaError_t set_cell_attr() {
 template <class TR>
 static cudaError_t set_base_attrs() {
     cudaError_t e = set_base_attr1<TR, (TR::CAP >= 16384 ? 1024 : 512)>();
-    if (e == cudaSuccess) e = set_cell_attr<TR, 256, 8>();
-    if (e == cudaSuccess) e = set_cell_attr<TR, 512, 8>();
+    if (e == cudaSuccess) e = set_cell_attr<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>();
+    if (e == cudaSuccess) e = set_cell_attr<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>();
     if (e == cudaSuccess) e = set_cell_attr<TR, 512, 16>();
     return e;
 }
@@ -580,8 +592,8 @@ static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStrea
         // the class-3 count lives on the device: the cell kernels append their fallbacks
         memcpy(g_ws.h_ctr + CTR_BASE0 + 3, counts + 3, 4);
         CK(cudaMemcpyAsync(g_ws.ctr + CTR_BASE0 + 3, g_ws.h_ctr + CTR_BASE0 + 3, 4, cudaMemcpyHostToDevice, st));
-        int rc = run_cell_class<TR, 256, 8>(data, counts[0], d_queues, st);
-        if (!rc) rc = run_cell_class<TR, 512, 8>(data, counts[1], d_queues + QCAP, st);
+        int rc = run_cell_class<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>(data, counts[0], d_queues, st);
+        if (!rc) rc = run_cell_class<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>(data, counts[1], d_queues + QCAP, st);
         if (!rc) rc = run_cell_class<TR, 512, 16>(data, counts[2], d_queues + 2 * QCAP, st);
         if (rc) return rc;
         constexpr int TH = TR::CAP >= 16384 ? 1024 : 512;

@@ -209,7 +209,7 @@ __device__ __forceinline__ u32 cpad(u32 c) { return c + 4u * (c / E); }
 constexpr u32 CELL_FIX_BUDGET = 4096;  // insertion-sort moves per leaf and thread before falling back
 
 template <class TR, int NT, int E>
-__global__ void __launch_bounds__(NT, (sizeof(typename TR::V) * NT * E <= 65536 ? 2 : 1))
+__global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(typename TR::V) * NT * E <= 65536 ? 2 : 1)))
     k_base_cell(const TaskDesc* tasks, u32 ntasks, void* vdata, TaskDesc* fb_queue, u32* fb_count, u32 fb_cap) {
     typedef typename TR::V V;
     typedef CellBase<TR, NT, E> CB;
