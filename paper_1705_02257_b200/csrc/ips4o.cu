@@ -87,7 +87,7 @@ struct Workspace {
     TaskDesc* h_q;
     u64* h_bnd;
     u32* h_tdone;
-    u32 k2_blocks = 0, k3_blocks = 0;
+    u32 k2_blocks = 0, k3_blocks = 0, k3t_blocks = 0;
     int k2_type = -1;
 };
 static Workspace g_ws;
@@ -303,6 +303,15 @@ template <class TR> struct K2Cfg1 { static constexpr int NT = 1024, E = 16 / TR:
 template <class TR> struct K2Cfg0 { static constexpr int NT = 256, E = 16 / TR::S * 4, MINB = 2; };
 template <class TR> struct K2Cfg1 { static constexpr int NT = 512, E = 16 / TR::S * 2, MINB = 2; };
 #endif
+// IPS4O_K3=regs selects the register-buffer permutation for the 8/16-byte types (tuning)
+static int k3_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("IPS4O_K3");
+        v = (e && e[0] == 'r') ? 1 : 0;
+    }
+    return v;
+}
 static int k2_variant() {
     static int v = -1;
     if (v < 0) {
@@ -356,12 +365,17 @@ static int prepare_kernels(void) {
     if (k2_variant() == 1) CK((k2_setup<TR, K2Cfg1<TR>>(&occ2)));
     else CK((k2_setup<TR, K2Cfg0<TR>>(&occ2)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_permute<TR>, K3_THREADS, 0));
-    if (occ2 < 1 || occ3 < 1) {
-        snprintf(g_errbuf, sizeof g_errbuf, "occupancy query returned %d/%d", occ2, occ3);
+    int occ3t = 0;
+    CK(cudaFuncSetAttribute(k_permute_tma<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)K3TSmem<TR>::total));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3t, k_permute_tma<TR>, K3T_THREADS, K3TSmem<TR>::total));
+    if (occ2 < 1 || occ3 < 1 || occ3t < 1) {
+        snprintf(g_errbuf, sizeof g_errbuf, "occupancy query returned %d/%d/%d", occ2, occ3, occ3t);
         return IPS4O_ECUDA;
     }
     g_ws.k2_blocks = (u32)(occ2 * g_ws.num_sms);
     g_ws.k3_blocks = (u32)(occ3 * g_ws.num_sms);
+    g_ws.k3t_blocks = (u32)(occ3t * g_ws.num_sms);
     g_ws.k2_type = TR::TYPE;
     return IPS4O_OK;
     }
@@ -518,7 +532,14 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
         (void)t0;
     }
 #endif
-    LAUNCH(KK_PERMUTE, (k_permute<TR><<<g_ws.k3_blocks, K3_THREADS, 0, st>>>(A)));
+    if constexpr (TR::S == 100) {
+        LAUNCH(KK_PERMUTE, (k_permute<TR><<<g_ws.k3_blocks, K3_THREADS, 0, st>>>(A)));
+    } else {
+        if (k3_variant() == 0)
+            LAUNCH(KK_PERMUTE, (k_permute_tma<TR><<<g_ws.k3t_blocks, K3T_THREADS, K3TSmem<TR>::total, st>>>(A)));
+        else
+            LAUNCH(KK_PERMUTE, (k_permute<TR><<<g_ws.k3_blocks, K3_THREADS, 0, st>>>(A)));
+    }
 #ifdef IPS4O_K3_TIMELINE
     {
         static unsigned int h[4096];

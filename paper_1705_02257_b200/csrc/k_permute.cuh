@@ -495,4 +495,175 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A) {
     }
 }
 
+
+// ------------------------------------------------------------------ permutation, TMA version
+//
+// The same protocol with the swap buffers in shared memory (the paper's per-thread swap
+// buffers) and the blocks moved by TMA bulk copies: every lane of a warp
+// runs its own chain (K3T_CHAINS per warp), so a chain waits only for its own atomic and
+// its own block load, and the loads of up to K3T_CHAINS chains per warp are in flight
+// together without occupying registers.  Chain states:
+//   FREE      take a block from the primary bucket (readers++, then r <- r-1) and load it;
+//   TAKING    the taken block is arriving (mbarrier): release the reader count, classify;
+//   HELD      claim the destination slot (w <- w+1): an unprocessed block there is loaded
+//             (SWAPPING), an empty one is written once the bucket's readers are gone (WAITW);
+//   SWAPPING  the displaced block is arriving: if it already belongs to the destination it
+//             stays (skip), else ours is written over it and the displaced one is carried on.
+// Used for the 8/16-byte types (block grid 16-byte aligned); records use k_permute.
+constexpr int K3T_WARPS = 4;                    // warps per CTA
+constexpr int K3T_CHAINS = 16;                  // chains (lanes) per warp
+constexpr int K3T_THREADS = 32 * K3T_WARPS;
+enum { CH_FREE = 0, CH_TAKING = 1, CH_HELD = 2, CH_SWAPPING = 3, CH_WAITW = 4, CH_DEAD = 5 };
+
+template <class TR>
+struct K3TSmem {
+    static constexpr u32 BB = TR::B * TR::S;
+    static constexpr size_t buf_bytes = (size_t)K3T_WARPS * K3T_CHAINS * 2 * BB;
+    static constexpr size_t total = buf_bytes;
+};
+
+__device__ __forceinline__ bool mbar_test(u64* mbar, u32 parity) {
+    u32 ok;
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok)
+                 : "r"((u32)__cvta_generic_to_shared(mbar)), "r"(parity)
+                 : "memory");
+    return ok != 0;
+}
+
+template <class TR>
+__global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A) {
+    typedef K3TSmem<TR> SM;
+    constexpr u32 BB = SM::BB;
+    extern __shared__ __align__(128) unsigned char smk3[];
+    __shared__ u64 s_tree[MAXK], s_spl[MAXK];
+    __shared__ __align__(8) u64 s_mbar[K3T_WARPS * K3T_CHAINS];
+    __shared__ u32 s_next;
+    const u32 tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
+    const u32 T = A.ntasks;
+    char* const data = reinterpret_cast<char*>(A.data);
+    const bool chain = lane < (u32)K3T_CHAINS;
+    const u32 cid = wi * K3T_CHAINS + lane;  // chain index in the CTA
+    char* const mybuf = reinterpret_cast<char*>(smk3) + (size_t)(chain ? cid : 0) * 2 * BB;
+    u64* const mymbar = &s_mbar[chain ? cid : 0];
+    if (chain) mbar_init(mymbar, 1);
+    mbar_fence_init();
+    __syncthreads();
+    u32 phase = 0;  // parity of this chain's next mbarrier completion
+    u32 t = (u32)((u64)blockIdx.x * T / gridDim.x);
+    const u32 tnwords = (T + 31) / 32;
+
+    for (;;) {
+        if (tid < 32) {
+            const u32 nt = next_clear_bit(A.tdone, tnwords, t, lane);
+            if (lane == 0) s_next = nt;
+        }
+        __syncthreads();
+        const u32 nt = s_next;
+        if (nt == 0xFFFFFFFFu || nt >= T) break;
+        t = nt;
+        if (tid < (u32)MAXK) {
+            s_tree[tid] = A.tree[(u64)t * MAXK + tid];
+            s_spl[tid] = A.spl[(u64)t * MAXK + tid];
+        }
+        for (u32 i = tid + K3T_THREADS; i < (u32)MAXK; i += K3T_THREADS) {
+            s_tree[i] = A.tree[(u64)t * MAXK + i];
+            s_spl[i] = A.spl[(u64)t * MAXK + i];
+        }
+        __syncthreads();
+        const TaskParam tp = A.tp[t];
+        u32* done = A.done + (u64)t * (MAXK / 32);
+        char* tbase = data + tp.g * TR::S;
+        auto classify_buf = [&](const char* b) {
+            typename TR::V v;
+            memcpy(&v, b, sizeof(v));
+            return classify_key(TR::key(v, tp.part), s_tree, s_spl, tp.logk, tp.kprime, tp.eq);
+        };
+
+        u32 st = chain ? CH_FREE : CH_DEAD;
+        u32 pb = (u32)(((u64)blockIdx.x * (K3T_WARPS * K3T_CHAINS) + cid) * 97u % tp.K);
+        u32 xb = 0;       // buffer holding our block (the other one receives loads)
+        u32 dest = 0, slot = 0;
+        while (__any_sync(0xffffffffu, st != CH_DEAD)) {
+            bool progressed = false;
+            // ---- atomics: takes (FREE) and claims (HELD), one round trip for all chains
+            if (st == CH_FREE) {
+                const u32 b = next_open_bucket(done, pb, tp.K);
+                if (b == 0xFFFFFFFFu) {
+                    st = CH_DEAD;
+                } else {
+                    pb = b;
+                    const u32 r0 = atomicAdd(ctl_readers(A.wr, t, pb), 1u);
+                    const u64 old = atomicAdd((unsigned long long*)ctl_wr(A.wr, t, pb), ~0ull + (u64)(r0 >> 31));
+                    const int ow = (int)(u32)(old >> 32), orr = (int)((u32)old - RBIAS);
+                    if (orr < ow) {
+                        atomicSub(ctl_readers(A.wr, t, pb), 1u);
+                        atomicOr(&done[pb >> 5], 1u << (pb & 31));
+                    } else {
+                        bulk_wait_read0();  // our earlier stores have read this buffer
+                        fence_proxy_async_smem();
+                        bulk_g2s(mybuf + xb * BB, tbase + (u64)orr * BB, BB, mymbar);
+                        st = CH_TAKING;
+                    }
+                    progressed = true;
+                }
+            } else if (st == CH_HELD) {
+                const u64 old = atomicAdd((unsigned long long*)ctl_wr(A.wr, t, dest), 1ull << 32);
+                const int ow = (int)(u32)(old >> 32), orr = (int)((u32)old - RBIAS);
+                slot = (u32)ow;
+                if (ow <= orr) {
+                    bulk_wait_read0();
+                    fence_proxy_async_smem();
+                    bulk_g2s(mybuf + (xb ^ 1) * BB, tbase + (u64)ow * BB, BB, mymbar);
+                    st = CH_SWAPPING;
+                } else {
+                    st = CH_WAITW;  // empty block: written once the bucket has no readers
+                }
+                progressed = true;
+            }
+            if (st == CH_WAITW && *(volatile u32*)ctl_readers(A.wr, t, dest) == 0u) {
+                // no reader left at the crossing: write into the empty block
+                // (past the task end: the overflow block).  (Never spin here:
+                // the reader may be a chain of this warp.)
+                char* dst;
+                if (tp.g + (u64)(slot + 1) * TR::B > tp.hi) {
+                    dst = reinterpret_cast<char*>(A.ovf) + (u64)t * BB;
+                    A.ovf_owner[t] = (int)dest;
+                } else {
+                    dst = tbase + (u64)slot * BB;
+                }
+                bulk_s2g(dst, mybuf + xb * BB, BB);
+                bulk_commit();
+                st = CH_FREE;
+                progressed = true;
+            }
+            // ---- arrived blocks
+            if ((st == CH_TAKING || st == CH_SWAPPING) && mbar_test(mymbar, phase)) {
+                phase ^= 1u;
+                if (st == CH_TAKING) {
+                    atomicSub(ctl_readers(A.wr, t, pb), 1u);  // the block has been read
+                    dest = classify_buf(mybuf + xb * BB);
+                    st = CH_HELD;
+                } else {
+                    const u32 od = classify_buf(mybuf + (xb ^ 1) * BB);
+                    if (od != dest) {
+                        bulk_s2g(tbase + (u64)slot * BB, mybuf + xb * BB, BB);
+                        bulk_commit();
+                        xb ^= 1u;
+                        dest = od;
+                    }  // else: already in place, skip it and keep ours
+                    st = CH_HELD;
+                }
+                progressed = true;
+            }
+            if (!__any_sync(0xffffffffu, progressed)) __nanosleep(32);
+        }
+        __syncthreads();
+        if (tid == 0) atomicOr(&A.tdone[t >> 5], 1u << (t & 31));
+    }
+    bulk_wait0();  // every block store is complete before the kernel ends
+}
+
 }  // namespace ips4o
