@@ -14,7 +14,11 @@ LIB = os.path.join(HERE, "libips4o.so")
 VARIANTS = {"bb256": ["-DIPS4O_BLOCK_BYTES=256"],
             "k3s2": ["-DIPS4O_K3_SLOTS=2"], "k3s8": ["-DIPS4O_K3_SLOTS=8"],
             "k3s4m3": ["-DIPS4O_K3_MINB=3"], "k3s2m8": ["-DIPS4O_K3_SLOTS=2", "-DIPS4O_K3_MINB=8"],
-            "k3tl": ["-DIPS4O_K3_TIMELINE"], "cellbig": ["-DIPS4O_CELL_SMALL=0"]}
+            "k3tl": ["-DIPS4O_K3_TIMELINE"], "cellbig": ["-DIPS4O_CELL_SMALL=0"],
+            "k3t_2x32": ["-DIPS4O_K3T_WARPS=2", "-DIPS4O_K3T_CHAINS=32"],
+            "k3t_8x8": ["-DIPS4O_K3T_WARPS=8", "-DIPS4O_K3T_CHAINS=8"],
+            "k3t_3x16": ["-DIPS4O_K3T_WARPS=3", "-DIPS4O_K3T_CHAINS=16"],
+            "k3t_4x24": ["-DIPS4O_K3T_WARPS=4", "-DIPS4O_K3T_CHAINS=24"]}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

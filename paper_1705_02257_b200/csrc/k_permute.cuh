@@ -510,8 +510,14 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A) {
 //   SWAPPING  the displaced block is arriving: if it already belongs to the destination it
 //             stays (skip), else ours is written over it and the displaced one is carried on.
 // Used for the 8/16-byte types (block grid 16-byte aligned); records use k_permute.
-constexpr int K3T_WARPS = 4;                    // warps per CTA
-constexpr int K3T_CHAINS = 16;                  // chains (lanes) per warp
+#ifndef IPS4O_K3T_WARPS
+#define IPS4O_K3T_WARPS 4
+#endif
+#ifndef IPS4O_K3T_CHAINS
+#define IPS4O_K3T_CHAINS 16
+#endif
+constexpr int K3T_WARPS = IPS4O_K3T_WARPS;      // warps per CTA
+constexpr int K3T_CHAINS = IPS4O_K3T_CHAINS;    // chains (lanes) per warp
 constexpr int K3T_THREADS = 32 * K3T_WARPS;
 enum { CH_FREE = 0, CH_TAKING = 1, CH_HELD = 2, CH_SWAPPING = 3, CH_WAITW = 4, CH_DEAD = 5 };
 
