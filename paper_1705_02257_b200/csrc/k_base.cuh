@@ -337,14 +337,22 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
             // their own cell, with no cell boundaries to track.
             const u32 rs = myrun[0].x;
             const u32 re = (tid + 1) * E < ncell ? cnt[cpad<E>((tid + 1) * E)] : n;
-            for (u32 i = rs + 1; i < re; ++i) {
-                const V x = X[i];
-                u32 q = i;
-                while (q > rs && TR::less(x, X[q - 1])) {
-                    X[q] = X[q - 1];
-                    --q;
+            if (rs < re) {
+                V prev = X[rs];  // the largest element of [rs, i)
+                for (u32 i = rs + 1; i < re; ++i) {
+                    const V x = X[i];
+                    if (!TR::less(x, prev)) {
+                        prev = x;
+                        continue;
+                    }
+                    X[i] = prev;
+                    u32 q = i - 1;
+                    while (q > rs && TR::less(x, X[q - 1])) {
+                        X[q] = X[q - 1];
+                        --q;
+                    }
+                    X[q] = x;
                 }
-                if (q != i) X[q] = x;
             }
         }
         __syncthreads();
