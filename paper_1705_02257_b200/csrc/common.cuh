@@ -14,7 +14,13 @@ constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer (SURVEY 
 // Each bucket's permutation control pair: the packed (w, r) word, then its reader count.
 // (Spreading the pairs over 256-byte lines -- one L2 slice each -- measured no faster.)
 constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
-constexpr int TREE_COPIES = 8;       // replicated splitter tree in K2 (lanes l, l+8 of a half-warp share a copy)
+#ifndef IPS4O_K2_STAGES
+#define IPS4O_K2_STAGES 1
+#endif
+constexpr int K2_STAGES = IPS4O_K2_STAGES;   // tiles staged ahead in K2 (TMA)
+// replicated splitter tree in K2: 16 copies (conflict-free lookups) when shared memory
+// allows, else 8 (lanes l, l+8 of a half-warp share a copy)
+constexpr int TREE_COPIES = K2_STAGES == 1 ? 16 : 8;
 constexpr u32 TREE_NODE_BYTES = 8 * TREE_COPIES;
 constexpr u32 INV_BUCKET = 0xFFFFu;  // "no element" marker in classification registers
 constexpr int K3_THREADS = 256;      // block permutation CTA

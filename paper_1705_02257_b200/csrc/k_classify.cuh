@@ -29,7 +29,7 @@ struct K2Smem {
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
     static constexpr size_t arr_bytes = 5 * MAXK * 4;
     static constexpr size_t rtree_bytes = (size_t)MAXK * TREE_COPIES * 8;
-    static constexpr size_t stage_bytes = (size_t)2 * NT * (16 / TR::S * 4) * TR::S;  // 2 tiles
+    static constexpr size_t stage_bytes = (size_t)K2_STAGES * NT * (16 / TR::S * 4) * TR::S;  // staged tiles
     static constexpr size_t total = buf_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes + stage_bytes;
 };
 
@@ -432,18 +432,29 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             constexpr u32 ALL = (E >= 32) ? 0xFFFFFFFFu : ((1u << E) - 1u);
             constexpr u32 TB = TILE * sizeof(V);
             if (tid == 0) {
-                for (u64 k = 0; k < 2 && k < nft; ++k) bulk_g2s(stage + k * TILE, data + mb + k * TILE, TB, &s_mbar[k]);
+                for (u64 k = 0; k < (u64)K2_STAGES && k < nft; ++k)
+                    bulk_g2s(stage + k * TILE, data + mb + k * TILE, TB, &s_mbar[k]);
             }
             for (u64 ti = 0; ti < nft; ++ti) {
-                const u32 st = (u32)(ti & 1);
+                const u32 st = K2_STAGES == 2 ? (u32)(ti & 1) : 0u;
                 mbar_wait(&s_mbar[st], (phase >> st) & 1u);
                 phase ^= 1u << st;
                 const uint4* sp = reinterpret_cast<const uint4*>(stage + st * TILE);
 #pragma unroll
                 for (int i = 0; i < E / TR::VEC; ++i) cur[i] = sp[i * NT + tid];
-                // (the tile's first barrier follows every thread's reads of the stage; the
-                // refill of this stage for tile ti+2 is issued after it, inside k2_tile)
-                const V* refill = ti + 2 < nft ? data + mb + (ti + 2) * TILE : nullptr;
+                // two stages: the tile's first barrier follows every thread's reads of the
+                // stage, and the refill for tile ti+2 is issued after it, inside k2_tile; one
+                // stage: an extra barrier here, then the load of tile ti+1
+                const V* refill = nullptr;
+                if (K2_STAGES == 2) {
+                    refill = ti + 2 < nft ? data + mb + (ti + 2) * TILE : nullptr;
+                } else {
+                    __syncthreads();
+                    if (tid == 0 && ti + 1 < nft) {
+                        fence_proxy_async_smem();
+                        bulk_g2s(stage, data + mb + (ti + 1) * TILE, TB, &s_mbar[0]);
+                    }
+                }
                 if (tp.logk == 8)
                     k2_tile<TR, NT, E, 8>(data, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                           slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
