@@ -455,7 +455,11 @@ static void plan_batch(const TaskDesc* tasks, u32 T, uintptr_t base_addr, u64 L,
         tp.part = tasks[i].part;
         const u64 main = hi - g;
         u64 ns = std::max<u64>(1, (main + L / 2) / L);
-        u64 Lt = ((main + ns - 1) / ns + B - 1) / B * B;
+        // the task's last stripe is a quarter of the others: with the stripes handed out
+        // longest first, the short ones fill the persistent K2 CTAs' last round
+        u64 Lt = ns > 1 ? (u64)std::ceil((double)main / ((double)ns - 0.75)) : main;
+        Lt = (Lt + B - 1) / B * B;
+        if (ns > 1 && (ns - 1) * Lt >= main) Lt = ((main + ns - 1) / ns + B - 1) / B * B;
         ns = std::max<u64>(1, (main + Lt - 1) / Lt);
         tp.stripe_begin = S;
         tp.nstripes = (u32)ns;
