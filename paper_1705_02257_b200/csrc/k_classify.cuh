@@ -252,14 +252,15 @@ struct K2Defer {
     u32 mask;
 };
 
-template <class TR, int NT, int E, int LOGK>
+template <class TR, int NT, int E, int LOGK, bool AGG>
 __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const uint4 (&raw)[E / TR::VEC],
                                         u32 valid, bool final_tile, u64 mb, u32 cap,
                                         typename TR::V* buf, u32* nbl,
                                         const u64* tree, const u64* spl, u32* fill, u32* cnt,
                                         u32* slotb, u32* nfl, u32* s_nflushed, u32 logk,
                                         u32 kprime, u32 eq, const typename TR::V* refill,
-                                        typename TR::V* refill_stage, u64* refill_mbar, K2Defer<TR, E>& df) {
+                                        typename TR::V* refill_stage, u64* refill_mbar, K2Defer<TR, E>& df,
+                                        bool& agg) {
     typedef typename TR::V V;
     constexpr int B = TR::B;
     const u32 tid = threadIdx.x;
@@ -276,9 +277,24 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         for (int e = 0; e < E; ++e) key[e] = TR::key(v[e], 0);
         k2_bucket_keys<E, LOGK>(key, valid, tree, spl, logk, kprime, eq, bk);
     }
+    // (skewed tiles -- sorted runs, equal keys: the previous tile put more than 1/8 of its
+    // elements into one bucket -- check each slot for a warp whose 32 elements share a
+    // bucket; such a warp takes its 32 positions with one atomic instead of 32 serialised)
+    const u32 lane = tid & 31;
 #pragma unroll
-    for (int j = 0; j < E; ++j)
-        if (bk[j] != INV_BUCKET) pos[j] = atomicAdd(&cnt[bk[j]], 1u);
+    for (int j = 0; j < E; ++j) {
+        bool done = false;
+        if (AGG) {
+            const u32 b0 = __shfl_sync(0xffffffffu, bk[j], 0);
+            if (__all_sync(0xffffffffu, bk[j] == b0) && b0 != INV_BUCKET) {
+                u32 base = 0;
+                if (lane == 0) base = atomicAdd(&cnt[b0], 32u);
+                pos[j] = __shfl_sync(0xffffffffu, base, 0) + lane;
+                done = true;
+            }
+        }
+        if (!done && bk[j] != INV_BUCKET) pos[j] = atomicAdd(&cnt[bk[j]], 1u);
+    }
     __syncthreads();
     if (refill && tid == 0) {
         // every thread has read the stage: load the tile two ahead into it (WAR across the
@@ -290,10 +306,12 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     //    this tile and their flush slots.  cnt[b] counts the bucket's stream from the first
     //    element of its buffer (the atomics above returned buffer-relative positions); it is
     //    rebased past the blocks flushed now, nbl[b] counts the flushed blocks.
+    bool hot = false;
     if (tid < (u32)MAXK) {
         bulk_wait_read0();
         const u32 b = tid;
         const u32 run = cnt[b];  // buffered (incl. deferred) + new elements
+        hot = run - fill[b] > (u32)(NT * E / 8);
         u32 nf = run / B, slot = 0;
         if (nf) {
             if (final_tile) {
@@ -315,7 +333,8 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         fill[b] = run - nf * B;
         nbl[b] += nf;
     }
-    __syncthreads();
+    if (AGG || LOGK == 8) agg = __syncthreads_or(hot);
+    else __syncthreads();
     // 4. place: the previous tile's deferred elements, then this tile's: first block ->
     //    smem buffer, later complete blocks -> straight to the stripe, the start of the
     //    next block -> deferred
@@ -422,6 +441,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
         const u64 me = sd.end;
         K2Defer<TR, E> df;
         df.mask = 0;
+        bool agg = false;  // skewed tiles: aggregate the atomics of uniform warps
         const u32 cap = me > mb ? (u32)((me - mb) / B) : 0u;
         if (mb < me) {
             // full tiles: staged in shared memory by TMA bulk loads two tiles ahead (a tile
@@ -455,21 +475,21 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
                         bulk_g2s(stage, data + mb + (ti + 1) * TILE, TB, &s_mbar[0]);
                     }
                 }
-                if (tp.logk == 8)
-                    k2_tile<TR, NT, E, 8>(data, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
-                                          slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
-                                          refill, stage + st * TILE, &s_mbar[st], df);
+                if (tp.logk == 8 && !agg)
+                    k2_tile<TR, NT, E, 8, false>(data, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                                                 slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
+                                                 refill, stage + st * TILE, &s_mbar[st], df, agg);
                 else
-                    k2_tile<TR, NT, E, 0>(data, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
-                                          slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
-                                          refill, stage + st * TILE, &s_mbar[st], df);
+                    k2_tile<TR, NT, E, 0, true>(data, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                                                slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
+                                                refill, stage + st * TILE, &s_mbar[st], df, agg);
             }
             const u64 tb = mb + nft * TILE;
             if (tb < me) {
                 const u32 vt = k2_load<TR, NT, E>(data, tb, (u32)(me - tb), cur);
-                k2_tile<TR, NT, E, 0>(data, cur, vt, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                k2_tile<TR, NT, E, 0, true>(data, cur, vt, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                       slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
-                                      nullptr, nullptr, nullptr, df);
+                                      nullptr, nullptr, nullptr, df, agg);
             }
         }
         if (sd.first && tp.lo < tp.g) {
@@ -478,8 +498,8 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             const u64 hend = tp.g < tp.hi ? tp.g : tp.hi;
             uint4 hv[E / TR::VEC];
             const u32 hval = k2_load<TR, NT, E>(data, tp.lo, (u32)(hend - tp.lo), hv);
-            k2_tile<TR, NT, E, 0>(data, hv, hval, true, mb, cap, buf, nbl, rtree, spl, fill, cnt, slotb, nfl,
-                           &s_nflushed, tp.logk, tp.kprime, tp.eq, nullptr, nullptr, nullptr, df);
+            k2_tile<TR, NT, E, 0, true>(data, hv, hval, true, mb, cap, buf, nbl, rtree, spl, fill, cnt, slotb, nfl,
+                           &s_nflushed, tp.logk, tp.kprime, tp.eq, nullptr, nullptr, nullptr, df, agg);
         }
         k2_drain<TR, E>(buf, df);
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area
