@@ -95,11 +95,15 @@ __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
     for (u32 ww = 0; ww < w; ++ww) woff += s_wsum[ww];
     A.mov[(u64)t * (MAXK + 1) + b] = woff + incl - moves;
     if (b == MAXK - 1) A.mov[(u64)t * (MAXK + 1) + MAXK] = woff + incl;
-    // w_i = d_i, r_i = d_i + nf_i - 1 (block indices; r biased)
-    *ctl_wr(A.wr, t, b) = ((u64)d << 32) | (u64)(u32)(d + nf - 1u + RBIAS);
+    // w_i = d_i, r_i = d_i + nf_i - 1 (block indices; r biased).  A task whose
+    // elements all fell into this one bucket (equal keys) has, after the Appendix-A moves,
+    // only blocks of this bucket in [d, d+nf): every block is in place, w_i = d_i + nf_i.
+    const bool all_here = (u64)c == tp.hi - tp.lo;
+    const u32 w0 = all_here ? d + nf : d;
+    *ctl_wr(A.wr, t, b) = ((u64)w0 << 32) | (u64)(u32)(d + nf - 1u + RBIAS);
     *ctl_readers(A.wr, t, b) = 0;
     A.cflag[(u64)t * MAXK + b] = 0;
-    const u32 dn_bit = (b >= tp.K || nf == 0) ? 1u : 0u;
+    const u32 dn_bit = (b >= tp.K || nf == 0 || all_here) ? 1u : 0u;
     const u32 bal = __ballot_sync(0xffffffffu, dn_bit);
     if (lane == 0) A.done[(u64)t * (MAXK / 32) + w] = bal;
     if (b == 0) {
