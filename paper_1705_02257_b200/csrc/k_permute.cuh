@@ -40,8 +40,9 @@ __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
         }
     }
     u32 c = 0;
-#pragma unroll 16
+#pragma unroll 32
     for (u32 j = 0; j < NS; ++j) c += A.s_count[(u64)(S0 + j) * MAXK + b];
+    __syncthreads();  // staged stripe ranges
     // exclusive scan over the 256 buckets
     u32 incl = c;
 #pragma unroll
@@ -67,16 +68,30 @@ __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
     // full blocks inside [d, dn): every stripe holds full blocks [sb, sb+F) then empty ones
     auto fs_of = [&](u32 j) { return staged ? s_sb[j] : A.sd[S0 + j].sb; };
     auto fe_of = [&](u32 j) { return staged ? s_fe[j] : A.sd[S0 + j].sb + A.s_nfull[S0 + j]; };
+    // stripes are in block order: only those from the one containing d onwards overlap
+    // [d, dn) (a level-1 bucket spans a few of the ~444 stripes)
+    u32 j0 = 0;
+    {
+        u32 lo2 = 0, hi2 = NS;  // last stripe with sb <= d
+        while (hi2 - lo2 > 1) {
+            const u32 mid = (lo2 + hi2) >> 1;
+            if (fs_of(mid) <= d) lo2 = mid;
+            else hi2 = mid;
+        }
+        j0 = lo2;
+    }
     u32 nf = 0;
-    for (u32 j = 0; j < NS; ++j) {
+    for (u32 j = j0; j < NS; ++j) {
         const u32 fs = fs_of(j), fe = fe_of(j);
+        if (fs >= dn) break;
         const u32 lo2 = fs > d ? fs : d, hi2 = fe < dn ? fe : dn;
         if (hi2 > lo2) nf += hi2 - lo2;
     }
     // Appendix A: holes (empty blocks) inside [d, d+nf) must be filled
     u32 fullpre = 0;
-    for (u32 j = 0; j < NS; ++j) {
+    for (u32 j = j0; j < NS; ++j) {
         const u32 fs = fs_of(j), fe = fe_of(j);
+        if (fs >= d + nf) break;
         const u32 lo2 = fs > d ? fs : d, hi2 = fe < d + nf ? fe : d + nf;
         if (hi2 > lo2) fullpre += hi2 - lo2;
     }

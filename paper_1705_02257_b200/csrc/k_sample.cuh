@@ -14,7 +14,7 @@ namespace ips4o {
 
 constexpr int K1_THREADS = 1024;
 constexpr int K1_SAMPLE = 4096;        // sample capacity for ordinary tasks (32 KB smem)
-constexpr int K1_SAMPLE_BIG = 16384;   // for tasks of >= 2^22 elements (dynamic smem, 128 KB)
+constexpr int K1_SAMPLE_BIG = 8192;    // for tasks of >= 2^22 elements (dynamic smem, 64 KB)
 constexpr u64 K1_BIG_TASK = 1ull << 22;
 
 // Builds the padded splitter array spl[1..k'-1] and the BFS tree from nd distinct sorted
