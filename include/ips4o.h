@@ -85,6 +85,18 @@ int ips4o_sort(void* d_data, uint64_t n, int elem_type, void* stream);
  * reused across calls and released by ips4o_release_workspace(). */
 int ips4o_sort_host(void* h_data, uint64_t n, int elem_type, void* stream);
 
+/* Key-value sort of structure-of-arrays data: d_keys[0..n) (uint64 if
+ * key_type == IPS4O_U64, IEEE double if IPS4O_F64; no NaN / -0.0) are sorted ascending
+ * and d_vals[0..n) (uint64) travel with their keys; unstable.  Both arrays are device
+ * memory of the current device owned by the caller.  The pairs are gathered into a
+ * library-owned 16·n-byte staging array of {key image, value} records (f64 keys as their
+ * order-preserving uint64 image), sorted in place there by the IPS4O_PAIR_U64 path, and
+ * scattered back: this entry point is NOT in place -- it needs 16·n bytes beyond
+ * ips4o_aux_bytes(n, IPS4O_PAIR_U64), released by ips4o_release_workspace().
+ * Returns IPS4O_OK, IPS4O_EINVAL (bad key_type, null pointer with n > 0), IPS4O_EALIGN
+ * (pointers not 8-byte aligned), IPS4O_ENOMEM, or a status of ips4o_sort. */
+int ips4o_sort_kv(uint64_t* d_keys, uint64_t* d_vals, uint64_t n, int key_type, void* stream);
+
 /* Upper bound, in bytes, of the device workspace ips4o_sort(n, elem_type) uses
  * (Theorem 2: O(k b t) buffers; here t = stripes/CTAs). */
 size_t ips4o_aux_bytes(uint64_t n, int elem_type);

@@ -23,7 +23,7 @@ NUM_KERNEL_KINDS = 8
 
 # every symbol include/ips4o.h declares
 EXPORTS = (
-    "ips4o_sort", "ips4o_sort_host", "ips4o_aux_bytes", "ips4o_last_stats", "ips4o_error_string",
+    "ips4o_sort", "ips4o_sort_host", "ips4o_sort_kv", "ips4o_aux_bytes", "ips4o_last_stats", "ips4o_error_string",
     "ips4o_release_workspace", "ips4o_profile_enable", "ips4o_profile_read",
     "ips4o_kernel_kind_name", "ips4o_debug_classify", "ips4o_debug_partition_once",
 )
@@ -63,6 +63,7 @@ def lib():
         vp, u64, u32, i32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int
         L.ips4o_sort.argtypes = [vp, u64, i32, vp]
         L.ips4o_sort_host.argtypes = [vp, u64, i32, vp]
+        L.ips4o_sort_kv.argtypes = [vp, vp, u64, i32, vp]
         L.ips4o_aux_bytes.argtypes = [u64, i32]
         L.ips4o_aux_bytes.restype = ctypes.c_size_t
         L.ips4o_last_stats.argtypes = [ctypes.POINTER(Stats)]
@@ -76,7 +77,7 @@ def lib():
         L.ips4o_debug_classify.argtypes = [vp, u64, i32, vp, u32, i32, vp, vp]
         L.ips4o_debug_partition_once.argtypes = [vp, u64, i32, vp, u32, i32,
                                                  ctypes.POINTER(u64), ctypes.POINTER(u32), vp]
-        for f in ("ips4o_sort", "ips4o_sort_host", "ips4o_last_stats", "ips4o_release_workspace",
+        for f in ("ips4o_sort", "ips4o_sort_host", "ips4o_sort_kv", "ips4o_last_stats", "ips4o_release_workspace",
                   "ips4o_profile_enable", "ips4o_profile_read", "ips4o_debug_classify",
                   "ips4o_debug_partition_once"):
             getattr(L, f).restype = i32
@@ -94,6 +95,26 @@ def _check(rc: int, what: str):
 
 def ips4o_sort(d_ptr: int, n: int, elem_type: int, stream: int = 0) -> None:
     _check(lib().ips4o_sort(ctypes.c_void_p(d_ptr), n, elem_type, ctypes.c_void_p(stream)), "ips4o_sort")
+
+
+def ips4o_sort_kv(keys_ptr: int, vals_ptr: int, n: int, key_type: int, stream: int = 0) -> None:
+    _check(lib().ips4o_sort_kv(ctypes.c_void_p(keys_ptr), ctypes.c_void_p(vals_ptr), n, key_type,
+                               ctypes.c_void_p(stream)), "ips4o_sort_kv")
+
+
+def sort_kv_(keys, vals):
+    """Sort CUDA tensors keys (uint64 or float64) and vals (64-bit) by key, in their own
+    storage (16*n bytes of library staging, see include/ips4o.h); unstable."""
+    import torch
+    if not (keys.is_cuda and vals.is_cuda) or keys.shape != vals.shape or keys.dim() != 1:
+        raise Ips4oError("sort_kv_ expects two 1-D CUDA tensors of the same length")
+    if not (keys.is_contiguous() and vals.is_contiguous()) or vals.element_size() != 8:
+        raise Ips4oError("sort_kv_ expects contiguous tensors and 8-byte values")
+    kt = IPS4O_F64 if keys.dtype == torch.float64 else IPS4O_U64
+    if kt == IPS4O_U64 and keys.element_size() != 8:
+        raise Ips4oError("sort_kv_ keys must be 64-bit")
+    ips4o_sort_kv(keys.data_ptr(), vals.data_ptr(), keys.shape[0], kt,
+                  torch.cuda.current_stream(keys.device).cuda_stream)
 
 
 def ips4o_sort_host(h_ptr: int, n: int, elem_type: int, stream: int = 0) -> None:

@@ -852,6 +852,78 @@ int ips4o_sort_host(void* h_data, uint64_t n, int elem_type, void* stream) {
     return IPS4O_OK;
 }
 
+}  // extern "C"
+
+namespace ips4o {
+// SoA <-> staging records {key image, value}; f64 keys through the order-preserving map
+// (and back: the map is a bijection on the non-NaN, non -0.0 doubles)
+__global__ void k_kv_gather(const u64* keys, const u64* vals, ulonglong2* out, u64 n, int f64) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 k = keys[i];
+        out[i] = make_ulonglong2(f64 ? TF64::key(k) : k, vals[i]);
+    }
+}
+__global__ void k_kv_scatter(const ulonglong2* in, u64* keys, u64* vals, u64 n, int f64) {
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const ulonglong2 p = in[i];
+        keys[i] = f64 ? ((p.x >> 63) ? (p.x & 0x7FFFFFFFFFFFFFFFull) : ~p.x) : p.x;
+        vals[i] = p.y;
+    }
+}
+static void* g_kv_stage = nullptr;
+static size_t g_kv_bytes = 0;
+static int g_kv_dev = -1;
+}  // namespace ips4o
+
+extern "C" {
+
+int ips4o_sort_kv(uint64_t* d_keys, uint64_t* d_vals, uint64_t n, int key_type, void* stream) {
+    if (key_type != IPS4O_U64 && key_type != IPS4O_F64) {
+        snprintf(g_errbuf, sizeof g_errbuf, "sort_kv: key type must be u64 or f64");
+        return IPS4O_EINVAL;
+    }
+    if (n > 0 && (!d_keys || !d_vals)) {
+        snprintf(g_errbuf, sizeof g_errbuf, "sort_kv: null pointer");
+        return IPS4O_EINVAL;
+    }
+    if (n >= (1ull << 40)) return IPS4O_EINVAL;
+    if ((((uintptr_t)d_keys) | ((uintptr_t)d_vals)) & 7u) return IPS4O_EALIGN;
+    if (n <= 1) return IPS4O_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        const size_t need = (size_t)n * 16;
+        if (g_kv_stage && (g_kv_bytes < need || g_kv_dev != dev)) {
+            cudaFree(g_kv_stage);
+            g_kv_stage = nullptr;
+        }
+        if (!g_kv_stage) {
+            if (cudaMalloc(&g_kv_stage, need) != cudaSuccess) {
+                cudaGetLastError();
+                snprintf(g_errbuf, sizeof g_errbuf, "sort_kv: staging allocation of %zu bytes failed", need);
+                return IPS4O_ENOMEM;
+            }
+            g_kv_bytes = need;
+            g_kv_dev = dev;
+        }
+        const u32 grid = (u32)std::min<u64>((n + 255) / 256, 4096);
+        k_kv_gather<<<grid, 256, 0, st>>>((const u64*)d_keys, (const u64*)d_vals, (ulonglong2*)g_kv_stage, n, key_type == IPS4O_F64);
+        CK(cudaGetLastError());
+    }
+    int rc = ips4o_sort(g_kv_stage, n, IPS4O_PAIR_U64, stream);
+    if (rc) return rc;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        const u32 grid = (u32)std::min<u64>((n + 255) / 256, 4096);
+        k_kv_scatter<<<grid, 256, 0, st>>>((const ulonglong2*)g_kv_stage, (u64*)d_keys, (u64*)d_vals, n, key_type == IPS4O_F64);
+        CK(cudaGetLastError());
+        g_stats.elem_type = (uint32_t)key_type;
+    }
+    return IPS4O_OK;
+}
+
 size_t ips4o_aux_bytes(uint64_t n, int elem_type) {
     const int s = type_size(elem_type);
     if (!s) return 0;
@@ -878,6 +950,9 @@ const char* ips4o_error_string(int status) {
 
 int ips4o_release_workspace(void) {
     std::lock_guard<std::mutex> lk(g_mu);
+    if (g_kv_stage) cudaFree(g_kv_stage);
+    g_kv_stage = nullptr;
+    g_kv_bytes = 0;
     if (g_ws.dev) cudaFree(g_ws.dev);
     g_ws.dev = nullptr;
     g_ws.dev_bytes = 0;

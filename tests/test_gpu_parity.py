@@ -275,6 +275,31 @@ def test_stats_and_aux_bytes():
     assert st["levels"] >= 2
 
 
+@pytest.mark.parametrize("key_type", [W.ELEM_U64, W.ELEM_F64])
+def test_sort_kv_vs_oracle(key_type):
+    """Structure-of-arrays key-value sort: keys bit-exact vs the oracle's key sort, every
+    (key, value) pair preserved."""
+    for n in (1, 2, 1000, 70_001, 1_000_003):
+        rng = np.random.default_rng(n)
+        if key_type == W.ELEM_U64:
+            k = W.u64_uniform(n, 5) >> np.uint64(40)   # duplicates
+        else:
+            k = W.f64_exponential(n, 5) * np.where(rng.random(n) < 0.5, -1.0, 1.0)
+        v = rng.integers(0, 2**63, size=n, dtype=np.int64).astype(np.uint64)
+        dk = to_dev(k, key_type)
+        dv = torch.from_numpy(v.view(np.int64)).cuda()
+        ips4o.sort_kv_(dk, dv)
+        torch.cuda.synchronize()
+        gk = to_host(dk, key_type)
+        gv = dv.cpu().numpy().view(np.uint64)
+        assert np.array_equal(gk, oracle.sort(k))
+        kb = k.view(np.uint64) if key_type == W.ELEM_F64 else k
+        gkb = gk.view(np.uint64) if key_type == W.ELEM_F64 else gk
+        a = np.sort(np.stack([kb, v], 1).view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k", "v"])
+        b = np.sort(np.stack([gkb, gv], 1).view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k", "v"])
+        assert np.array_equal(a, b)
+
+
 def test_sort_host_entry_point():
     a = W.u64_uniform(1 << 20, 11)
     h = a.copy()
