@@ -331,12 +331,24 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
         __syncthreads();
         // 4. insertion sort inside the cells of this thread's run; nothing
         //    to do when every cell is a single key value
-        if (mul && tid * E < ncell) {
-            // The run's positions [rs, re) hold its cells in cell order, and the cell map is
-            // monotone: an insertion sort of the whole run by key moves elements only inside
-            // their own cell, with no cell boundaries to track.
-            const u32 rs = myrun[0].x;
-            const u32 re = (tid + 1) * E < ncell ? cnt[cpad<E>((tid + 1) * E)] : n;
+        if (mul) {
+            // Thread t takes the cells that start in positions [t*n/NT, (t+1)*n/NT) (equal
+            // shares of elements); [rs, re) holds them in cell order, and the cell map is
+            // monotone: an insertion sort of the whole range by key moves elements only
+            // inside their own cell.
+            auto cell_at = [&](u32 i) { return (u32)__umul64hi(TR::key(X[i]) - kmin, mul); };
+            auto first_start = [&](u32 p) {  // first cell start at or after position p
+                if (p == 0 || p >= n) return p < n ? p : n;
+                u32 cprev = cell_at(p - 1);
+                while (p < n) {
+                    const u32 c = cell_at(p);
+                    if (c != cprev) break;
+                    ++p;
+                }
+                return p;
+            };
+            const u32 rs = first_start((u32)(((u64)tid * n) / NT));
+            const u32 re = first_start((u32)(((u64)(tid + 1) * n) / NT));
             if (rs < re) {
                 V prev = X[rs];  // the largest element of [rs, i)
                 for (u32 i = rs + 1; i < re; ++i) {
