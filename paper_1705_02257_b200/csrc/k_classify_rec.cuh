@@ -12,14 +12,16 @@
 
 namespace ips4o {
 
+constexpr int K2REC_RPT = 2;  // records per thread and tile
+
 template <int NT>
 struct K2RecSmem {
     static constexpr int NW = NT / 32;
     static constexpr size_t buf_bytes = (size_t)MAXK * TRec::B * 100;
-    static constexpr size_t stage_bytes = (size_t)NT * 100;
-    static constexpr size_t wcnt_bytes = (size_t)NW * MAXK * 2;
+    static constexpr size_t stage_bytes = (size_t)NT * K2REC_RPT * 100 + 16;
+    static constexpr size_t wcnt_bytes = 0;
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
-    static constexpr size_t arr_bytes = 4 * MAXK * 4;
+    static constexpr size_t arr_bytes = 5 * MAXK * 4;
     static constexpr size_t rtree_bytes = (size_t)MAXK * TREE_COPIES * 8;
     static constexpr size_t total = buf_bytes + stage_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes;
 };
@@ -38,13 +40,21 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
     extern __shared__ __align__(128) unsigned char smem[];
     u32* buf = reinterpret_cast<u32*>(smem);                                   // [256][B][25]
     u32* stage = reinterpret_cast<u32*>(smem + SM::buf_bytes);                 // [NT][25]
-    unsigned short* wcnt = reinterpret_cast<unsigned short*>(smem + SM::buf_bytes + SM::stage_bytes);
     u64* tree = reinterpret_cast<u64*>(smem + SM::buf_bytes + SM::stage_bytes + SM::wcnt_bytes);
     u64* spl = tree + MAXK;
     u32* fill = reinterpret_cast<u32*>(spl + MAXK);
     u32* cnt = fill + MAXK;
     u32* slotb = cnt + MAXK;
     u32* nfl = slotb + MAXK;
+    u32* nbl = nfl + MAXK;
+    constexpr int RPT = K2REC_RPT;
+    __shared__ __align__(8) u64 s_mbar;
+    u32 sphase = 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_mbar, 1);
+        mbar_fence_init();
+    }
+    constexpr u32 RT = NT * RPT;  // records per tile
     u64* rtree = reinterpret_cast<u64*>(smem + SM::buf_bytes + SM::stage_bytes + SM::wcnt_bytes + SM::tree_bytes +
                                         SM::arr_bytes);
     __shared__ u32 s_stripe, s_nflushed, s_wsum[NW];
@@ -67,65 +77,83 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
             spl[b] = A.spl[(u64)sd.task * MAXK + b];
             fill[b] = 0;
             cnt[b] = 0;
-            for (int ww = 0; ww < NW; ++ww) wcnt[ww * MAXK + b] = 0;
+            nbl[b] = 0;
         }
         rtree_fill(rtree, A.tree + (u64)sd.task * MAXK, tid, NT);
         if (tid == 0) s_nflushed = 0;
         __syncthreads();
         const u64 mb = sd.begin, me = sd.end;  // g == lo for records: no head region
-        for (u64 tb = mb; tb < me; tb += NT) {
-            const u32 len = (u32)((me - tb) < NT ? (me - tb) : NT);
-            // stage the tile (coalesced 4-byte words)
-            const u32* src = gw + tb * RW;
-            for (u32 i = tid; i < len * RW; i += NT) stage[i] = src[i];
-            __syncthreads();
-            const bool valid = tid < len;
-            const u32* my = stage + tid * RW;
-            u64 key[1];
-            key[0] = valid ? (tp.part ? TRec::lo_of(my[2]) : TRec::hi_of(my[0], my[1])) : 0ull;
-            u32 bk[1], peers[1];
-            const bool full = __all_sync(0xffffffffu, valid);
-            if (tp.logk == 8)
-                k2_classify_keys<1, 8>(key, valid ? 1u : 0u, full, rtree, spl, tp.logk, tp.kprime, tp.eq, bk, peers);
-            else
-                k2_classify_keys<1, 0>(key, valid ? 1u : 0u, full, rtree, spl, tp.logk, tp.kprime, tp.eq, bk, peers);
-            // warp-aggregated ranking
-            const u32 b = bk[0];
-            const u32 leader = __ffs(peers[0]) - 1;
-            u32 base = 0;
-            if (lane == leader && b != INV_BUCKET) {
-                base = wcnt[w * MAXK + b];
-                wcnt[w * MAXK + b] = (unsigned short)(base + __popc(peers[0]));
+        for (u64 tb = mb; tb < me; tb += (u64)RT) {
+            const u32 len = (u32)((me - tb) < RT ? (me - tb) : RT);
+            // stage the tile: the 16-byte aligned body of its bytes by one TMA bulk copy
+            // (mbarrier completion), the < 16 bytes before / after it by plain loads; record
+            // r of the tile then starts at stage word dw + 25 r
+            const uintptr_t p0 = (uintptr_t)(gw + tb * RW), p1 = p0 + (uintptr_t)len * 100u;
+            const uintptr_t a0 = (p0 + 15) & ~(uintptr_t)15, a1 = p1 & ~(uintptr_t)15;
+            const uintptr_t w0 = p0 & ~(uintptr_t)15;  // stage byte 0
+            const u32 dw = (u32)((p0 - w0) / 4);
+            if (tid == 0) {
+                if (a1 > a0) bulk_g2s(reinterpret_cast<char*>(stage) + (a0 - w0), reinterpret_cast<const void*>(a0),
+                                      (u32)(a1 - a0), &s_mbar);
+                else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((u32)__cvta_generic_to_shared(&s_mbar)) : "memory");
             }
-            base = __shfl_sync(0xffffffffu, base, leader);
-            u32 pos = base + __popc(peers[0] & lanemask_lt());
+            {
+                // head words [p0, min(a0, p1)) and tail words [max(a1, a0), p1)
+                const u32 nh = (u32)(((a0 < p1 ? a0 : p1) - p0) / 4);
+                const uintptr_t t0 = a1 > a0 ? a1 : (a0 < p1 ? a0 : p1);
+                const u32 nt = (u32)((p1 - t0) / 4);
+                if (tid < nh) stage[dw + tid] = reinterpret_cast<const u32*>(p0)[tid];
+                if (tid >= 32 && tid - 32 < nt) stage[(t0 - w0) / 4 + (tid - 32)] = reinterpret_cast<const u32*>(t0)[tid - 32];
+            }
+            mbar_wait(&s_mbar, sphase);
+            sphase ^= 1u;
             __syncthreads();
+            // classify this thread's records (branchless descent) and rank
+            // them in their buckets' buffer streams by shared-memory atomics (any order
+            // inside a bucket)
+            u64 key[RPT];
+            u32 valid = 0;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                const u32 ir = tid + r * NT;
+                const u32* my = stage + dw + ir * RW;
+                const bool ok = ir < len;
+                key[r] = ok ? (tp.part ? TRec::lo_of(my[2]) : TRec::hi_of(my[0], my[1])) : 0ull;
+                valid |= (ok ? 1u : 0u) << r;
+            }
+            u32 bk[RPT], pos[RPT];
+            if (tp.logk == 8) k2_bucket_keys<RPT, 8>(key, valid, rtree, spl, tp.logk, tp.kprime, tp.eq, bk);
+            else k2_bucket_keys<RPT, 0>(key, valid, rtree, spl, tp.logk, tp.kprime, tp.eq, bk);
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+                if (bk[r] != INV_BUCKET) pos[r] = atomicAdd(&cnt[bk[r]], 1u);
+            __syncthreads();
+            // per bucket: completed blocks, flush slots; rebase the buffer-relative counts
             for (u32 bb = tid; bb < (u32)MAXK; bb += NT) {
-                const u32 f = fill[bb];
-                u32 run = f;
-                for (int ww = 0; ww < NW; ++ww) {
-                    u32 c = wcnt[ww * MAXK + bb];
-                    wcnt[ww * MAXK + bb] = (unsigned short)run;
-                    run += c;
-                }
+                const u32 run = cnt[bb];
                 const u32 nf = run / B;
                 nfl[bb] = nf;
                 slotb[bb] = nf ? atomicAdd(&s_nflushed, nf) : 0u;
-                cnt[bb] += run - f;
+                cnt[bb] = run - nf * B;
                 fill[bb] = run - nf * B;
+                nbl[bb] += nf;
             }
             __syncthreads();
-            bool defer = false;
-            if (b != INV_BUCKET) {
-                const u32 p = (u32)wcnt[w * MAXK + b] + pos;
+            u32 defer = 0;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                const u32 b = bk[r];
+                if (b == INV_BUCKET) continue;
+                const u32* my = stage + dw + (tid + r * NT) * RW;
+                const u32 p = pos[r];
                 const u32 q = p / B, off = p % B, nf = nfl[b];
                 if (q == 0) {
                     copy_rec(buf + (b * B + off) * RW, my);
                 } else if (q < nf) {
                     copy_rec(gw + (mb + (u64)(slotb[b] + q) * B + off) * RW, my);
                 } else {
-                    pos = p - nf * B;
-                    defer = true;
+                    pos[r] = p - nf * B;
+                    defer |= 1u << r;
                 }
             }
             __syncthreads();
@@ -138,10 +166,11 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
                 }
             }
             __syncthreads();
-            if (defer) copy_rec(buf + (b * B + pos) * RW, my);
-            for (u32 bb = tid; bb < (u32)MAXK; bb += NT)
-                for (int ww = 0; ww < NW; ++ww) wcnt[ww * MAXK + bb] = 0;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+                if (defer & (1u << r)) copy_rec(buf + (bk[r] * B + pos[r]) * RW, stage + dw + (tid + r * NT) * RW);
             __syncthreads();
+            if (tid == 0) fence_proxy_async_smem();  // generic reads of the stage before the next TMA write
         }
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area
         u32 f = tid < (u32)MAXK ? fill[tid] : 0u;
@@ -162,7 +191,7 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
         if (tid == 0) s_spbase = atomicAdd((unsigned long long*)A.spill_ctr, (unsigned long long)total);
         __syncthreads();
         if (tid < (u32)MAXK) {
-            A.s_count[(u64)sidx * MAXK + tid] = cnt[tid];
+            A.s_count[(u64)sidx * MAXK + tid] = nbl[tid] * (u32)B + cnt[tid];
             A.s_fill[(u64)sidx * MAXK + tid] = f;
             A.s_spoff[(u64)sidx * MAXK + tid] = excl;
             slotb[tid] = excl;
