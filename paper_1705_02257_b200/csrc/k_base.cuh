@@ -140,21 +140,63 @@ struct TRecItem {
 constexpr int KREC_THREADS = 256, KREC_ITEMS = 4;  // CAP = 1024 records
 struct RecBase {
     static constexpr size_t items_bytes = (size_t)padidx(KREC_THREADS * KREC_ITEMS) * 16 + 16;
-    static constexpr size_t smem = items_bytes + (size_t)KREC_THREADS * KREC_ITEMS * 100;
+    static constexpr u32 rec_words = KREC_THREADS * KREC_ITEMS * 25 + 8;  // + alignment slack
+    static constexpr size_t smem = items_bytes + (size_t)2 * rec_words * 4;  // two leaves
 };
+
+// Records of one leaf arrive in shared memory by a TMA bulk copy of the 16-byte aligned body
+// (the < 16 bytes before / after it by plain loads), one leaf ahead: the copy of leaf t+1
+// overlaps the sort of leaf t.  Returns the word offset of the leaf's first record.
+__device__ __forceinline__ u32 rec_fetch(const TaskDesc& td, const u32* gw, u32* buf, u64* mbar, bool edges_now) {
+    const uintptr_t p0 = (uintptr_t)(gw + td.lo * 25), p1 = (uintptr_t)(gw + td.hi * 25);
+    const uintptr_t a0 = (p0 + 15) & ~(uintptr_t)15, a1 = p1 & ~(uintptr_t)15, w0 = p0 & ~(uintptr_t)15;
+    if (edges_now) {
+        if (a1 > a0) bulk_g2s(reinterpret_cast<char*>(buf) + (a0 - w0), reinterpret_cast<const void*>(a0),
+                              (u32)(a1 - a0), mbar);
+        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((u32)__cvta_generic_to_shared(mbar)) : "memory");
+    }
+    return (u32)((p0 - w0) / 4);
+}
 
 __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks, u32 ntasks, void* vdata) {
     extern __shared__ __align__(16) unsigned char smem5[];
     ulonglong2* it = reinterpret_cast<ulonglong2*>(smem5);
-    u32* srec = reinterpret_cast<u32*>(smem5 + RecBase::items_bytes);
+    u32* const sbuf = reinterpret_cast<u32*>(smem5 + RecBase::items_bytes);
     u32* gw = reinterpret_cast<u32*>(vdata);
     const u32 tid = threadIdx.x;
+    __shared__ __align__(8) u64 s_mbar[2];
+    if (tid == 0) {
+        mbar_init(&s_mbar[0], 1);
+        mbar_init(&s_mbar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    u32 phase = 0, cur = 0;
+    if (blockIdx.x < ntasks && tid == 0) rec_fetch(tasks[blockIdx.x], gw, sbuf, &s_mbar[0], true);
     for (u32 ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
         const TaskDesc td = tasks[ti];
         const u32 n = (u32)(td.hi - td.lo);
         const u32 n16 = (n + KREC_ITEMS - 1) / KREC_ITEMS * KREC_ITEMS;
         u32* g = gw + td.lo * 25;
-        for (u32 i = tid; i < n * 25; i += KREC_THREADS) srec[i] = g[i];
+        u32* srec0 = sbuf + cur * RecBase::rec_words;
+        if (tid == 0 && ti + gridDim.x < ntasks) {
+            fence_proxy_async_smem();
+            rec_fetch(tasks[ti + gridDim.x], gw, sbuf + (cur ^ 1) * RecBase::rec_words, &s_mbar[cur ^ 1], true);
+        }
+        const u32 dw = rec_fetch(td, gw, srec0, nullptr, false);
+        u32* srec = srec0 + dw;
+        {
+            // this leaf's head / tail words outside the aligned body
+            const uintptr_t p0 = (uintptr_t)g, p1 = (uintptr_t)(g + n * 25);
+            const uintptr_t a0 = (p0 + 15) & ~(uintptr_t)15, a1 = p1 & ~(uintptr_t)15;
+            const u32 nh = (u32)(((a0 < p1 ? a0 : p1) - p0) / 4);
+            const uintptr_t t0 = a1 > a0 ? a1 : (a0 < p1 ? a0 : p1);
+            const u32 nt = (u32)((p1 - t0) / 4);
+            if (tid < nh) srec[tid] = g[tid];
+            if (tid >= 32 && tid - 32 < nt) srec[(t0 - p0) / 4 + (tid - 32)] = reinterpret_cast<const u32*>(t0)[tid - 32];
+        }
+        mbar_wait(&s_mbar[cur], (phase >> cur) & 1u);
+        phase ^= 1u << cur;
         __syncthreads();
         for (u32 i = tid; i < n16; i += KREC_THREADS) {
             ulonglong2 x = TRecItem::pad();
@@ -173,6 +215,7 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
             g[i] = srec[src * 25 + wd];
         }
         __syncthreads();
+        cur ^= 1u;
     }
 }
 
