@@ -620,6 +620,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A) {
                     st = CH_DEAD;
                 } else {
                     pb = b;
+                    K3_TL_EVENT(1);
                     const u32 r0 = atomicAdd(ctl_readers(A.wr, t, pb), 1u);
                     const u64 old = atomicAdd((unsigned long long*)ctl_wr(A.wr, t, pb), ~0ull + (u64)(r0 >> 31));
                     const int ow = (int)(u32)(old >> 32), orr = (int)((u32)old - RBIAS);
@@ -635,6 +636,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A) {
                     progressed = true;
                 }
             } else if (st == CH_HELD) {
+                K3_TL_EVENT(0);
                 const u64 old = atomicAdd((unsigned long long*)ctl_wr(A.wr, t, dest), 1ull << 32);
                 const int ow = (int)(u32)(old >> 32), orr = (int)((u32)old - RBIAS);
                 slot = (u32)ow;
