@@ -347,12 +347,17 @@ static int prepare_kernels(void) {
         CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(padidx(K1_SAMPLE) * 8 + 16)));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_permute<TR>, K3_THREADS, 0));
-        if (occ2 < 1 || occ3 < 1) {
-            snprintf(g_errbuf, sizeof g_errbuf, "occupancy query returned %d/%d", occ2, occ3);
+        int occ3t = 0;
+        CK(cudaFuncSetAttribute(k_permute_tma<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)K3TSmem<TR>::total));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3t, k_permute_tma<TR>, K3T_THREADS, K3TSmem<TR>::total));
+        if (occ2 < 1 || occ3 < 1 || occ3t < 1) {
+            snprintf(g_errbuf, sizeof g_errbuf, "occupancy query returned %d/%d/%d", occ2, occ3, occ3t);
             return IPS4O_ECUDA;
         }
         g_ws.k2_blocks = (u32)(occ2 * g_ws.num_sms);
         g_ws.k3_blocks = (u32)(occ3 * g_ws.num_sms);
+        g_ws.k3t_blocks = (u32)(occ3t * g_ws.num_sms);
         g_ws.k2_type = TR::TYPE;
         return IPS4O_OK;
     } else {
@@ -443,9 +448,8 @@ static void plan_batch(const TaskDesc* tasks, u32 T, uintptr_t base_addr, u64 L,
     u32 S = 0;
     for (u32 i = 0; i < T; ++i) {
         const u64 lo = tasks[i].lo, hi = tasks[i].hi;
-        u64 g = lo;  // records: the block grid starts at lo (4-byte copies, no TMA)
-        if (TR::S != 100)
-            while (((base_addr + g * TR::S) & 15u) != 0 && g < hi) ++g;
+        u64 g = lo;  // block grid origin: the first 16-byte aligned element (TMA block moves)
+        while (((base_addr + g * TR::S) & 15u) != 0 && g < hi) ++g;
         TaskParam& tp = g_ws.h_tp[i];
         memset(&tp, 0, sizeof tp);
         tp.lo = lo;
@@ -536,9 +540,7 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
         (void)t0;
     }
 #endif
-    if constexpr (TR::S == 100) {
-        LAUNCH(KK_PERMUTE, (k_permute<TR><<<g_ws.k3_blocks, K3_THREADS, 0, st>>>(A)));
-    } else {
+    {
         if (k3_variant() == 0)
             LAUNCH(KK_PERMUTE, (k_permute_tma<TR><<<g_ws.k3t_blocks, K3T_THREADS, K3TSmem<TR>::total, st>>>(A)));
         else

@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
     u32* nfl = slotb + MAXK;
     u32* nbl = nfl + MAXK;
     constexpr int RPT = K2REC_RPT;
+    constexpr int RS = RPT;  // record slots per thread
+    __shared__ u32 s_head[3 * 25], s_hb[3];
     __shared__ __align__(8) u64 s_mbar;
     u32 sphase = 0;
     if (threadIdx.x == 0) {
@@ -82,9 +84,17 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
         rtree_fill(rtree, A.tree + (u64)sd.task * MAXK, tid, NT);
         if (tid == 0) s_nflushed = 0;
         __syncthreads();
-        const u64 mb = sd.begin, me = sd.end;  // g == lo for records: no head region
+        // the block grid starts at g, the first 16-byte aligned record >= lo (TMA block
+        // moves); the < 4 head records [lo, g) of a task's first stripe are classified after
+        // its tiles and go straight to the spill with the partial buffers (they never
+        // complete a block, so no flush can outrun the read frontier)
+        const u64 mb = sd.begin > tp.g ? sd.begin : tp.g, me = sd.end;
+        const u32 nhead = sd.first ? (u32)(tp.g - tp.lo) : 0u;
+        if (tid < nhead * RW) s_head[tid] = gw[tp.lo * RW + tid];
+        if (tid < 3) s_hb[tid] = INV_BUCKET;
         for (u64 tb = mb; tb < me; tb += (u64)RT) {
             const u32 len = (u32)((me - tb) < RT ? (me - tb) : RT);
+            constexpr bool with_head = false;
             // stage the tile: the 16-byte aligned body of its bytes by one TMA bulk copy
             // (mbarrier completion), the < 16 bytes before / after it by plain loads; record
             // r of the tile then starts at stage word dw + 25 r
@@ -111,21 +121,24 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
             // classify this thread's records (branchless descent) and rank
             // them in their buckets' buffer streams by shared-memory atomics (any order
             // inside a bucket)
-            u64 key[RPT];
+            // slot RS-1 of threads tid < nhead holds a head record in the first tile
+            auto rec_ptr = [&](int r) -> const u32* {
+                return r < RPT ? stage + dw + (tid + r * NT) * RW : s_head + tid * RW;
+            };
+            u64 key[RS];
             u32 valid = 0;
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-                const u32 ir = tid + r * NT;
-                const u32* my = stage + dw + ir * RW;
-                const bool ok = ir < len;
+            for (int r = 0; r < RS; ++r) {
+                const u32* my = rec_ptr(r);
+                const bool ok = r < RPT ? tid + r * NT < len : (with_head && tid < nhead);
                 key[r] = ok ? (tp.part ? TRec::lo_of(my[2]) : TRec::hi_of(my[0], my[1])) : 0ull;
                 valid |= (ok ? 1u : 0u) << r;
             }
-            u32 bk[RPT], pos[RPT];
-            if (tp.logk == 8) k2_bucket_keys<RPT, 8>(key, valid, rtree, spl, tp.logk, tp.kprime, tp.eq, bk);
-            else k2_bucket_keys<RPT, 0>(key, valid, rtree, spl, tp.logk, tp.kprime, tp.eq, bk);
+            u32 bk[RS], pos[RS];
+            if (tp.logk == 8) k2_bucket_keys<RS, 8>(key, valid, rtree, spl, tp.logk, tp.kprime, tp.eq, bk);
+            else k2_bucket_keys<RS, 0>(key, valid, rtree, spl, tp.logk, tp.kprime, tp.eq, bk);
 #pragma unroll
-            for (int r = 0; r < RPT; ++r)
+            for (int r = 0; r < RS; ++r)
                 if (bk[r] != INV_BUCKET) pos[r] = atomicAdd(&cnt[bk[r]], 1u);
             __syncthreads();
             // per bucket: completed blocks, flush slots; rebase the buffer-relative counts
@@ -141,10 +154,10 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
             __syncthreads();
             u32 defer = 0;
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) {
+            for (int r = 0; r < RS; ++r) {
                 const u32 b = bk[r];
                 if (b == INV_BUCKET) continue;
-                const u32* my = stage + dw + (tid + r * NT) * RW;
+                const u32* my = rec_ptr(r);
                 const u32 p = pos[r];
                 const u32 q = p / B, off = p % B, nf = nfl[b];
                 if (q == 0) {
@@ -167,13 +180,26 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
             }
             __syncthreads();
 #pragma unroll
-            for (int r = 0; r < RPT; ++r)
-                if (defer & (1u << r)) copy_rec(buf + (bk[r] * B + pos[r]) * RW, stage + dw + (tid + r * NT) * RW);
+            for (int r = 0; r < RS; ++r)
+                if (defer & (1u << r)) copy_rec(buf + (bk[r] * B + pos[r]) * RW, rec_ptr(r));
             __syncthreads();
             if (tid == 0) fence_proxy_async_smem();  // generic reads of the stage before the next TMA write
         }
+        // head records: classified now, spilled with the bucket's partial buffer
+        if (tid < nhead) {
+            const u32* my = s_head + tid * RW;
+            u64 hk[1] = {tp.part ? TRec::lo_of(my[2]) : TRec::hi_of(my[0], my[1])};
+            u32 hb[1];
+            if (tp.logk == 8) k2_bucket_keys<1, 8>(hk, 1u, rtree, spl, tp.logk, tp.kprime, tp.eq, hb);
+            else k2_bucket_keys<1, 0>(hk, 1u, rtree, spl, tp.logk, tp.kprime, tp.eq, hb);
+            s_hb[tid] = hb[0];
+        }
+        __syncthreads();
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area
-        u32 f = tid < (u32)MAXK ? fill[tid] : 0u;
+        u32 nh_b = 0;  // head records of this bucket
+        if (tid < (u32)MAXK)
+            for (u32 i = 0; i < 3; ++i) nh_b += s_hb[i] == tid ? 1u : 0u;
+        u32 f = tid < (u32)MAXK ? fill[tid] + nh_b : 0u;
         u32 incl = f;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -191,7 +217,7 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
         if (tid == 0) s_spbase = atomicAdd((unsigned long long*)A.spill_ctr, (unsigned long long)total);
         __syncthreads();
         if (tid < (u32)MAXK) {
-            A.s_count[(u64)sidx * MAXK + tid] = nbl[tid] * (u32)B + cnt[tid];
+            A.s_count[(u64)sidx * MAXK + tid] = nbl[tid] * (u32)B + cnt[tid] + nh_b;
             A.s_fill[(u64)sidx * MAXK + tid] = f;
             A.s_spoff[(u64)sidx * MAXK + tid] = excl;
             slotb[tid] = excl;
@@ -207,6 +233,12 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
             for (u32 bb = w; bb < (u32)MAXK; bb += NW) {
                 const u32 fb = fill[bb], ob = slotb[bb];
                 for (u32 i = lane; i < fb * RW; i += 32) sp[ob * RW + i] = buf[bb * B * RW + i];
+                u32 o2 = ob + fb;  // then the bucket's head records
+                for (u32 h = 0; h < 3; ++h) {
+                    if (s_hb[h] != bb) continue;
+                    for (u32 i = lane; i < RW; i += 32) sp[o2 * RW + i] = s_head[h * RW + i];
+                    ++o2;
+                }
             }
         }
         __syncthreads();
