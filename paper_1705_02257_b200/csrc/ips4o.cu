@@ -297,7 +297,7 @@ static cudaError_t set_base_attrs() {
 #if IPS4O_BLOCK_BYTES == 512
 // 256 buffers of 512 B = 128 KB of shared memory: one CTA per SM
 template <class TR> struct K2Cfg0 { static constexpr int NT = 512, E = 16 / TR::S * 4, MINB = 1; };
-template <class TR> struct K2Cfg1 { static constexpr int NT = 1024, E = 16 / TR::S * 2, MINB = 1; };
+template <class TR> struct K2Cfg1 { static constexpr int NT = 384, E = 16 / TR::S * 6, MINB = 1; };
 #else
 // 256 buffers of 256 B = 64 KB: two CTAs per SM
 template <class TR> struct K2Cfg0 { static constexpr int NT = 256, E = 16 / TR::S * 4, MINB = 2; };
@@ -324,10 +324,10 @@ template <class TR, class C>
 static cudaError_t k2_setup(int* occ) {
     cudaError_t e = cudaFuncSetAttribute(k_classify<TR, C::NT, C::E, C::MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)K2Smem<TR, C::NT>::total);
+                                         (int)K2Smem<TR, C::NT, C::E>::total);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_classify<TR, C::NT, C::E, C::MINB>, C::NT,
-                                                         K2Smem<TR, C::NT>::total);
+                                                         K2Smem<TR, C::NT, C::E>::total);
 }
 
 constexpr int K2REC_THREADS = 256;
@@ -511,10 +511,10 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
         LAUNCH(KK_CLASSIFY, (k_classify_rec<K2REC_THREADS><<<g2, K2REC_THREADS, K2RecSmem<K2REC_THREADS>::total, st>>>(A)));
     } else if (k2_variant() == 1) {
         typedef K2Cfg1<TR> C;
-        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E, C::MINB><<<g2, C::NT, K2Smem<TR, C::NT>::total, st>>>(A)));
+        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E, C::MINB><<<g2, C::NT, K2Smem<TR, C::NT, C::E>::total, st>>>(A)));
     } else {
         typedef K2Cfg0<TR> C;
-        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E, C::MINB><<<g2, C::NT, K2Smem<TR, C::NT>::total, st>>>(A)));
+        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E, C::MINB><<<g2, C::NT, K2Smem<TR, C::NT, C::E>::total, st>>>(A)));
     }
     LAUNCH(KK_PREPARE, (k_prepare<TR><<<T, MAXK, 0, st>>>(A)));
     const u32 gx = std::max<u32>(1, (2 * g_ws.num_sms + T - 1) / T);

@@ -19,7 +19,7 @@
 
 namespace ips4o {
 
-template <class TR, int NT>
+template <class TR, int NT, int E>
 struct K2Smem {
     typedef typename TR::V V;
     static constexpr int B = TR::B;
@@ -29,7 +29,7 @@ struct K2Smem {
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
     static constexpr size_t arr_bytes = 5 * MAXK * 4;
     static constexpr size_t rtree_bytes = (size_t)MAXK * TREE_COPIES * 8;
-    static constexpr size_t stage_bytes = (size_t)K2_STAGES * NT * (16 / TR::S * 4) * TR::S;  // staged tiles
+    static constexpr size_t stage_bytes = (size_t)K2_STAGES * NT * E * TR::S;  // staged tiles
     static constexpr size_t total = buf_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes + stage_bytes;
 };
 
@@ -389,7 +389,7 @@ __device__ __forceinline__ void k2_drain(typename TR::V* buf, K2Defer<TR, E>& df
 template <class TR, int NT, int E, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
     typedef typename TR::V V;
-    typedef K2Smem<TR, NT> SM;
+    typedef K2Smem<TR, NT, E> SM;
     constexpr int B = TR::B;
     constexpr u32 TILE = NT * E;
     extern __shared__ __align__(128) unsigned char smem[];
