@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
     extern __shared__ __align__(16) unsigned char smc[];
     V* X = reinterpret_cast<V*>(smc);
     u32* cnt = reinterpret_cast<u32*>(smc + CB::x_bytes);
-    __shared__ u64 s_range[2], s_mul;
+    __shared__ u64 s_range[2];
     __shared__ u32 s_flag, s_wsum[NW];
     V* data = reinterpret_cast<V*>(vdata);
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -310,9 +310,9 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
         if (span == 0) continue;  // all keys equal: already sorted (no write)
         // cell(key) = floor((key - kmin) * ncell / (span + 1)) as the high half of a 64x64
         // product with a per-leaf multiplier: monotone, onto [0, ncell)
-        if (tid == 0) s_mul = span < ncell ? 0ull : (u64)(((unsigned __int128)ncell << 64) / ((unsigned __int128)span + 1));
-        __syncthreads();
-        const u64 mul = s_mul;
+        // (every thread computes it: mul = floor((2^64-1)/(span+1)) * ncell keeps
+        // span * mul < ncell * 2^64, so cells stay in [0, ncell))
+        const u64 mul = span < ncell ? 0ull : (span == ~0ull ? (u64)ncell : (~0ull / (span + 1)) * ncell);
         // 2. cell and rank inside the cell
         u32 cr[E];  // cell | rank << 16
 #pragma unroll
