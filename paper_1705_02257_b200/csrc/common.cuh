@@ -14,6 +14,9 @@ constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer (SURVEY 
 // Each bucket's permutation control pair: the packed (w, r) word, then its reader count.
 // (Spreading the pairs over 256-byte lines -- one L2 slice each -- measured no faster.)
 constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
+#ifndef IPS4O_K2_WFLUSH  // K2 flushes buffer blocks by TMA bulk stores (0) or warp copies (1, measured slower)
+#define IPS4O_K2_WFLUSH 0
+#endif
 #ifndef IPS4O_K2_STAGES
 #define IPS4O_K2_STAGES 1
 #endif

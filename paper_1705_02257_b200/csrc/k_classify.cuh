@@ -308,7 +308,7 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     //    rebased past the blocks flushed now, nbl[b] counts the flushed blocks.
     bool hot = false;
     if (tid < (u32)MAXK) {
-        bulk_wait_read0();
+        if (!IPS4O_K2_WFLUSH) bulk_wait_read0();
         const u32 b = tid;
         const u32 run = cnt[b];  // buffered (incl. deferred) + new elements
         hot = run - fill[b] > (u32)(NT * E / 8);
@@ -363,6 +363,32 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         }
     }
     df.mask = defer;
+#if IPS4O_K2_WFLUSH
+    __syncthreads();
+    // 5. flush complete buffer blocks: warp w copies the blocks of buckets w, w + NT/32, ...
+    //    (one 16-byte vector per lane and block, two blocks in flight); the next tile's
+    //    barriers order these reads before the buffers are refilled
+    {
+        constexpr u32 NWP = NT / 32, NV = B * sizeof(V) / 16;
+        static_assert(NV <= 32, "a block is one vector per lane");
+        const u32 w = tid >> 5;
+        const u32 bl = w + NWP * lane;
+        u32 m = __ballot_sync(0xffffffffu, bl < (u32)MAXK && nfl[bl] != 0u);
+        while (m) {
+            const u32 b0 = w + NWP * (u32)(__ffs(m) - 1);
+            m &= m - 1;
+            const bool two = m != 0u;
+            const u32 b1 = two ? w + NWP * (u32)(__ffs(m) - 1) : b0;
+            if (two) m &= m - 1;
+            if (lane < NV) {
+                const uint4 x0 = reinterpret_cast<const uint4*>(buf + b0 * B)[lane];
+                const uint4 x1 = reinterpret_cast<const uint4*>(buf + b1 * B)[lane];
+                reinterpret_cast<uint4*>(data + mb + (u64)slotb[b0] * B)[lane] = x0;
+                if (two) reinterpret_cast<uint4*>(data + mb + (u64)slotb[b1] * B)[lane] = x1;
+            }
+        }
+    }
+#else
     fence_proxy_async_smem();
     __syncthreads();
     // 5. flush complete buffer blocks with TMA bulk copies (their reads are awaited at the
@@ -371,6 +397,7 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         bulk_s2g(data + mb + (u64)slotb[tid] * B, buf + tid * B, B * sizeof(V));
         bulk_commit();
     }
+#endif
 }
 
 // End of a stripe: the last flushes have read their buffers; deferred elements join the
