@@ -372,41 +372,61 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
             if (idx < n) X[cnt[cpad<E>(cr[j] & 0xFFFFu)] + (cr[j] >> 16)] = v[j];
         }
         __syncthreads();
-        // 4. insertion sort inside the cells of this thread's run; nothing
-        //    to do when every cell is a single key value
+        // 4. order the cells of this thread's run that hold several elements (PAPER.md:403
+        //    finishes small subproblems by insertion sort): cells of 2-4 elements by a
+        //    4-element sorting network over the cell padded with the largest key (pads never
+        //    move: a comparator swaps only on strictly smaller keys), larger ones by insertion
+        //    sort.  Singleton cells need nothing; nothing at all when every cell is a single
+        //    key value.
         if (mul) {
-            // Thread t takes the cells that start in positions [t*n/NT, (t+1)*n/NT) (equal
-            // shares of elements); [rs, re) holds them in cell order, and the cell map is
-            // monotone: an insertion sort of the whole range by key moves elements only
-            // inside their own cell.
-            auto cell_at = [&](u32 i) { return (u32)__umul64hi(TR::key(X[i]) - kmin, mul); };
-            auto first_start = [&](u32 p) {  // first cell start at or after position p
-                if (p == 0 || p >= n) return p < n ? p : n;
-                u32 cprev = cell_at(p - 1);
-                while (p < n) {
-                    const u32 c = cell_at(p);
-                    if (c != cprev) break;
-                    ++p;
-                }
-                return p;
-            };
-            const u32 rs = first_start((u32)(((u64)tid * n) / NT));
-            const u32 re = first_start((u32)(((u64)(tid + 1) * n) / NT));
-            if (rs < re) {
-                V prev = X[rs];  // the largest element of [rs, i)
-                for (u32 i = rs + 1; i < re; ++i) {
-                    const V x = X[i];
-                    if (!TR::less(x, prev)) {
-                        prev = x;
-                        continue;
+            u32 bs[E + 1];
+#pragma unroll
+            for (int k = 0; k < E / 4; ++k) {
+                const uint4 q = myrun[k];
+                bs[4 * k] = q.x;
+                bs[4 * k + 1] = q.y;
+                bs[4 * k + 2] = q.z;
+                bs[4 * k + 3] = q.w;
+            }
+            bs[E] = tid + 1 < (u32)NT ? cnt[cpad<E>((tid + 1) * E)] : n;
+            u32 mask = 0;
+#pragma unroll
+            for (int k = 0; k < E; ++k) mask |= (bs[k + 1] - bs[k] > 1u ? 1u : 0u) << k;
+            const u32 enext = bs[E];
+            while (mask) {
+                const u32 k = (u32)__ffs(mask) - 1u;
+                mask &= mask - 1u;
+                const u32 b = cnt[cpad<E>(tid * E + k)];
+                const u32 e = k + 1 < (u32)E ? cnt[cpad<E>(tid * E + k + 1)] : enext;
+                if (e - b <= 4u) {
+                    const V pd = TR::pad();
+                    V x0 = X[b], x1 = X[b + 1];
+                    V x2 = e - b > 2u ? X[b + 2] : pd, x3 = e - b > 3u ? X[b + 3] : pd;
+                    auto cas = [](V& lo, V& hi) {
+                        const bool sw = TR::less(hi, lo);
+                        const V t = sw ? hi : lo;
+                        hi = sw ? lo : hi;
+                        lo = t;
+                    };
+                    cas(x0, x1);
+                    cas(x2, x3);
+                    cas(x0, x2);
+                    cas(x1, x3);
+                    cas(x1, x2);
+                    X[b] = x0;
+                    X[b + 1] = x1;
+                    if (e - b > 2u) X[b + 2] = x2;
+                    if (e - b > 3u) X[b + 3] = x3;
+                } else {
+                    for (u32 i = b + 1; i < e; ++i) {
+                        const V x = X[i];
+                        u32 q = i;
+                        while (q > b && TR::less(x, X[q - 1])) {
+                            X[q] = X[q - 1];
+                            --q;
+                        }
+                        X[q] = x;
                     }
-                    X[i] = prev;
-                    u32 q = i - 1;
-                    while (q > rs && TR::less(x, X[q - 1])) {
-                        X[q] = X[q - 1];
-                        --q;
-                    }
-                    X[q] = x;
                 }
             }
         }
