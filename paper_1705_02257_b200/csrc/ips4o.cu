@@ -22,6 +22,7 @@ namespace ips4o {
 
 constexpr u32 MAXT = 512;          // tasks per level batch
 constexpr u32 MAXS = 512;          // stripes per level batch
+static_assert(MAXS <= (u32)K4_MAXSTRIPES && MAXS <= (u32)K2P_MAXST, "per-task stripe tables in shared memory");
 constexpr u32 QCAP = MAXT * MAXK;  // queue capacity (tasks)
 constexpr u64 MIN_STRIPE = 65536;  // elements
 
@@ -563,8 +564,8 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
     }
 #endif
     if (T * MAXK >= 32u * g_ws.num_sms) {
-        // many buckets: one warp each
-        const u32 nw = T * MAXK, want = (nw + K4_WARPS - 1) / K4_WARPS;
+        // many buckets: one warp per group of K4_GROUP buckets
+        const u32 nw = T * MAXK / K4_GROUP, want = (nw + K4_WARPS - 1) / K4_WARPS;
         LAUNCH(KK_CLEANUP, (k_cleanup<TR><<<std::min<u32>(want, 8u * g_ws.num_sms), K4_THREADS, 0, st>>>(A)));
     } else {
         LAUNCH(KK_CLEANUP, (k_cleanup_cta<TR><<<T * MAXK, K4_THREADS, 0, st>>>(A)));
@@ -623,6 +624,23 @@ static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStrea
         if (!rc) rc = run_cell_class<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>(data, counts[1], d_queues + QCAP, st);
         if (!rc) rc = run_cell_class<TR, 512, 16>(data, counts[2], d_queues + 2 * QCAP, st);
         if (rc) return rc;
+#ifdef IPS4O_BASE_PROF
+        {
+            static unsigned long long h[2][8], z[2][8];
+            cudaStreamSynchronize(st);
+            cudaMemcpyFromSymbol(h, g_base_prof, sizeof h);
+            cudaMemcpyToSymbol(g_base_prof, z, sizeof z);
+            static const char* nm[8] = {"wb+top", "load+mm", "range", "rank", "sum", "scan+chk", "scatter", "fix"};
+            for (int c = 0; c < 2; ++c) {
+                unsigned long long t = 0;
+                for (int i = 0; i < 8; ++i) t += h[c][i];
+                if (!t) continue;
+                fprintf(stderr, "base prof class %s:", c ? "NT>=512" : "NT<512");
+                for (int i = 0; i < 8; ++i) fprintf(stderr, " %s %.1f%%", nm[i], 100.0 * h[c][i] / t);
+                fprintf(stderr, "\n");
+            }
+        }
+#endif
         constexpr int TH = TR::CAP >= 16384 ? 1024 : 512;
         typedef BaseClass<TR, TH, 16> BC;
         const u32 grid = std::max<u32>(1u, std::min<u32>(counts[3] + 64u, 2u * g_ws.num_sms));

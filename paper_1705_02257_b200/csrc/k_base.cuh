@@ -240,6 +240,31 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
 // whose cells would need too much insertion work (keys clustered far below the resolution
 // of the cells, e.g. heavy duplicates) is handed to the merge-sort kernel (fallback queue)
 // untouched.
+// Phase profile of the cell base case (tuning builds only): thread 0 of each CTA adds the
+// clock64 intervals between the leaf's barriers; the host prints the shares per class.
+#ifdef IPS4O_BASE_PROF
+__device__ unsigned long long g_base_prof[2][8];
+#define BASE_PROF_INIT()                                          \
+    unsigned long long bp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};      \
+    unsigned long long bp_last = clock64()
+#define BASE_PROF_MARK(i)                                         \
+    do {                                                          \
+        if (threadIdx.x == 0) {                                   \
+            const unsigned long long c_ = clock64();              \
+            bp_acc[i] += c_ - bp_last;                            \
+            bp_last = c_;                                         \
+        }                                                         \
+    } while (0)
+#define BASE_PROF_FLUSH(cls)                                                               \
+    do {                                                                                   \
+        if (threadIdx.x == 0)                                                              \
+            for (int i_ = 0; i_ < 8; ++i_) atomicAdd(&g_base_prof[cls][i_], bp_acc[i_]);  \
+    } while (0)
+#else
+#define BASE_PROF_INIT() do {} while (0)
+#define BASE_PROF_MARK(i) do {} while (0)
+#define BASE_PROF_FLUSH(cls) do {} while (0)
+#endif
 template <class TR, int NT, int E>
 struct CellBase {
     static constexpr u32 TILE = NT * E;                  // a power of two
@@ -266,6 +291,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
     V* data = reinterpret_cast<V*>(vdata);
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     uint4* myrun = reinterpret_cast<uint4*>(cnt + cpad<E>(tid * E));  // this thread's E counters
+    BASE_PROF_INIT();
     for (u32 ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
         const TaskDesc td = tasks[ti];
         const u32 n = (u32)(td.hi - td.lo);
@@ -273,6 +299,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
         const u32 cb = n > 1 ? 32u - (u32)__clz(n - 1) : 1u;  // 2^cb >= n cells
         const u32 ncell = 1u << cb;
         __syncthreads();  // the previous leaf is finished
+        BASE_PROF_MARK(0);
         if (tid == 0) {
             s_range[0] = ~0ull;
             s_range[1] = 0ull;
@@ -300,11 +327,13 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
             kmax = b > kmax ? b : kmax;
         }
         __syncthreads();
+        BASE_PROF_MARK(1);
         if (lane == 0 && w * 32 < n) {
             atomicMin(&s_range[0], kmin);
             atomicMax(&s_range[1], kmax);
         }
         __syncthreads();
+        BASE_PROF_MARK(2);
         kmin = s_range[0];
         const u64 span = s_range[1] - kmin;
         if (span == 0) continue;  // all keys equal: already sorted (no write)
@@ -325,6 +354,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
             }
         }
         __syncthreads();
+        BASE_PROF_MARK(3);
         // 3. exclusive scan of the counts (own run of E cells, 128-bit accesses)
         u32 sum = 0;
 #pragma unroll
@@ -340,6 +370,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
         }
         if (lane == 31) s_wsum[w] = incl;
         __syncthreads();
+        BASE_PROF_MARK(4);
         u32 base = incl - sum;
         for (u32 ww = 0; ww < w; ++ww) base += s_wsum[ww];
         u32 bigwork = 0;  // insertion work of this run's cells (~m^2 / 4 for large cells)
@@ -358,6 +389,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
         }
         if (bigwork && mul) atomicAdd(&s_flag, bigwork);
         __syncthreads();
+        BASE_PROF_MARK(5);
         if (s_flag > CELL_FIX_BUDGET) {
             // clustered keys (heavy duplicates in few cells): leave the leaf to the merge sort
             if (tid == 0) {
@@ -372,6 +404,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
             if (idx < n) X[cnt[cpad<E>(cr[j] & 0xFFFFu)] + (cr[j] >> 16)] = v[j];
         }
         __syncthreads();
+        BASE_PROF_MARK(6);
         // 4. order the cells of this thread's run that hold several elements (PAPER.md:403
         //    finishes small subproblems by insertion sort): cells of 2-4 elements by a
         //    4-element sorting network over the cell padded with the largest key (pads never
@@ -431,9 +464,11 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
             }
         }
         __syncthreads();
+        BASE_PROF_MARK(7);
         // 5. write back
         for (u32 i = tid; i < n; i += NT) g[i] = X[i];
     }
+    BASE_PROF_FLUSH(NT >= 512 ? 1 : 0);
 }
 
 template <class TR, int THREADS, int ITEMS>

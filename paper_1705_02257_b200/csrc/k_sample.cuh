@@ -91,10 +91,12 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
     for (u32 j = threadIdx.x; j < (u32)SAMPLE; j += blockDim.x) {
         u64 key = ~0ull;
         if (j < m) {
-            u64 a = lo + (u64)((unsigned __int128)n * j / m);
-            u64 b = lo + (u64)((unsigned __int128)n * (j + 1) / m);
-            u64 r = mix64(A.seed ^ mix64(lo * 0x9E3779B97F4A7C15ull + j));
-            key = TR::key(data[a + r % (b - a)], tp->part);
+            // stratum [a, b) of the task (n * (j+1) < 2^64 for n < 2^50); the offset inside
+            // it is the high half of a 64x64-bit product (no division)
+            const u64 a = lo + n * j / m;
+            const u64 b = lo + n * (j + 1) / m;
+            const u64 r = mix64(A.seed ^ mix64(lo * 0x9E3779B97F4A7C15ull + j));
+            key = TR::key(data[a + __umul64hi(r, b - a)], tp->part);
         }
         keys[padidx(j)] = key;
     }
