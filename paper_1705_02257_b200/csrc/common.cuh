@@ -165,6 +165,7 @@ struct LevelArgs {
     u64* bnd;         // [T][257] element-exact bucket starts e_0..e_256
     u32* dblk;        // [T][257] delimiters d_i (block index, rounded up)
     u32* nfb;         // [T][256] full blocks of bucket i
+    u32* btot;        // [T][256] bucket sizes: zeroed by K1, each K2 stripe adds its counts
     u32* mov;         // [T][257] prefix of Appendix-A moves over buckets
     u64* wr;          // [T][256] control lines: word 0 packed (w:32 | r+RBIAS:32) block
                       // pointers, word 1 (low half) the bucket's reader count

@@ -71,7 +71,7 @@ struct Workspace {
     u32 *s_count, *s_fill, *s_spoff, *s_nfull, *prefF, *prefE;
     u64* s_spbase;
     u64* bnd;
-    u32 *dblk, *nfb, *mov, *done, *cflag, *tdone;
+    u32 *dblk, *nfb, *mov, *done, *cflag, *tdone, *btot;
     u64* wr;
     void* ovf;
     int* ovf_owner;
@@ -116,7 +116,7 @@ static size_t fixed_bytes() {
     add(MAXS * 8 + MAXS * 4 * 3);              // s_spbase, s_nfull, prefF, prefE
     add((size_t)MAXT * (MAXK + 1) * 8);        // bnd
     add((size_t)MAXT * (MAXK + 1) * 4 * 2);    // dblk, mov
-    add((size_t)MAXT * MAXK * 4 * 2);          // nfb, cflag
+    add((size_t)MAXT * MAXK * 4 * 3);          // nfb, cflag, btot
     add((size_t)MAXT * (MAXK / 32) * 4);       // done
     add(MAXT / 32 * 4);                        // tdone
     add((size_t)MAXT * MAXK * 8 * CTL_STRIDE);  // wr control lines
@@ -187,9 +187,10 @@ static int ensure_ws(u64 n, int esize) {
     char* dm = take((size_t)MAXT * (MAXK + 1) * 4 * 2);
     g_ws.dblk = (u32*)dm;
     g_ws.mov = g_ws.dblk + (size_t)MAXT * (MAXK + 1);
-    char* nr = take((size_t)MAXT * MAXK * 4 * 2);
+    char* nr = take((size_t)MAXT * MAXK * 4 * 3);
     g_ws.nfb = (u32*)nr;
     g_ws.cflag = g_ws.nfb + (size_t)MAXT * MAXK;
+    g_ws.btot = g_ws.cflag + (size_t)MAXT * MAXK;
     g_ws.done = (u32*)take((size_t)MAXT * (MAXK / 32) * 4);
     g_ws.tdone = (u32*)take(MAXT / 32 * 4);
     g_ws.wr = (u64*)take((size_t)MAXT * MAXK * 8 * CTL_STRIDE);
@@ -411,6 +412,7 @@ static LevelArgs level_args(void* data, u32 T, u32 S, int emit, u64 seed) {
     A.bnd = g_ws.bnd;
     A.dblk = g_ws.dblk;
     A.nfb = g_ws.nfb;
+    A.btot = g_ws.btot;
     A.mov = g_ws.mov;
     A.wr = g_ws.wr;
     A.done = g_ws.done;

@@ -217,7 +217,9 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
         if (tid == 0) s_spbase = atomicAdd((unsigned long long*)A.spill_ctr, (unsigned long long)total);
         __syncthreads();
         if (tid < (u32)MAXK) {
-            A.s_count[(u64)sidx * MAXK + tid] = nbl[tid] * (u32)B + cnt[tid] + nh_b;
+            const u32 cb = nbl[tid] * (u32)B + cnt[tid] + nh_b;
+            A.s_count[(u64)sidx * MAXK + tid] = cb;
+            if (cb) atomicAdd(&A.btot[(u64)sd.task * MAXK + tid], cb);
             A.s_fill[(u64)sidx * MAXK + tid] = f;
             A.s_spoff[(u64)sidx * MAXK + tid] = excl;
             slotb[tid] = excl;

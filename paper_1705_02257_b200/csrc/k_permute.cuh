@@ -1,6 +1,6 @@
 // k_permute.cuh -- K3: delimiters, empty-block movement and the block permutation.
 //
-// k_prepare (one CTA per task): prefix sum of the stripes' bucket counts -> element-exact
+// k_prepare (one CTA per task): bucket sizes (summed by K2's stripes) -> element-exact
 //   bucket starts e_i; delimiters d_i = e_i rounded up to the block grid;
 //   full-block counts per bucket; initial (w_i, r_i).
 // k_moves: Appendix A -- make every bucket read "full blocks, then
@@ -39,9 +39,7 @@ __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
             s_fe[j] = A.sd[S0 + j].sb + A.s_nfull[S0 + j];
         }
     }
-    u32 c = 0;
-#pragma unroll 32
-    for (u32 j = 0; j < NS; ++j) c += A.s_count[(u64)(S0 + j) * MAXK + b];
+    const u32 c = A.btot[(u64)t * MAXK + b];  // summed by K2 over the task's stripes
     __syncthreads();  // staged stripe ranges
     // exclusive scan over the 256 buckets
     u32 incl = c;
@@ -195,7 +193,7 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
     const u32 S0 = tp.stripe_begin, NS = tp.nstripes;
     const u32* mov = A.mov + (u64)t * (MAXK + 1);
     const u32 M = mov[MAXK];
-    if (M == 0 || blockIdx.x * (blockDim.x >> 5) >= M) return;
+    if (M == 0 || blockIdx.x * (blockDim.x >> 5) * 32u >= M) return;
     const bool staged = NS <= (u32)K2P_MAXST;
     for (u32 i = threadIdx.x; i <= (u32)MAXK; i += blockDim.x) {
         s_mov[i] = mov[i];
@@ -220,9 +218,13 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
     auto pF_of = [&](u32 j) { return staged ? s_pF[j] : A.prefF[S0 + j]; };
     const u32 nwarps = gridDim.x * (blockDim.x >> 5);
     char* base = reinterpret_cast<char*>(A.data) + tp.g * TR::S;
-    for (u32 m = blockIdx.x * (blockDim.x >> 5) + wib; m < M; m += nwarps) {
-        u64 src = 0, dst = 0;
-        if (lane == 0) {
+    // every lane locates one move (five binary searches), then the warp copies the 32
+    // blocks two at a time (the moves are independent: sources are full blocks, targets
+    // empty ones)
+    for (u32 m0 = (blockIdx.x * (blockDim.x >> 5) + wib) * 32u; m0 < M; m0 += nwarps * 32u) {
+        const u32 m = m0 + lane;
+        u32 src = 0, dst = 0;
+        if (m < M) {
             const u32 b = last_le(MAXK, m, [&](u32 i) { return (u64)s_mov[i]; });
             const u32 k = m - s_mov[b];
             const u32 d = s_d[b];
@@ -242,10 +244,17 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
             const u32 jf = last_le(NS, fb, [&](u32 i) { return (u64)pF_of(i); });
             src = sb_of(jf) + (fb - pF_of(jf));
         }
-        src = __shfl_sync(0xffffffffu, src, 0);
-        dst = __shfl_sync(0xffffffffu, dst, 0);
-        const BlockRegs v = BlockIO<TR>::load(base + src * (B * TR::S), lane);
-        BlockIO<TR>::store(base + dst * (B * TR::S), lane, v);
+        const u32 cnt = M - m0 < 32u ? M - m0 : 32u;
+        for (u32 i = 0; i < cnt; i += 2) {
+            const bool two = i + 1 < cnt;
+            const u32 s0 = __shfl_sync(0xffffffffu, src, i), d0 = __shfl_sync(0xffffffffu, dst, i);
+            const u32 s1 = __shfl_sync(0xffffffffu, src, two ? i + 1 : i), d1 = __shfl_sync(0xffffffffu, dst, two ? i + 1 : i);
+            const BlockRegs v0 = BlockIO<TR>::load(base + (u64)s0 * (B * TR::S), lane);
+            BlockRegs v1;
+            if (two) v1 = BlockIO<TR>::load(base + (u64)s1 * (B * TR::S), lane);
+            BlockIO<TR>::store(base + (u64)d0 * (B * TR::S), lane, v0);
+            if (two) BlockIO<TR>::store(base + (u64)d1 * (B * TR::S), lane, v1);
+        }
     }
 }
 

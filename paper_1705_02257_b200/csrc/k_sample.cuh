@@ -21,7 +21,7 @@ constexpr u64 K1_BIG_TASK = 1ull << 22;
 // splitters held in s_dist[0..nd).  k' = next power of two >= nd+1; padding repeats the
 // largest splitter.  Writes the task's classifier fields.
 __device__ void build_tree_block(const u64* s_dist, u32 nd, u32 eq, u64* g_tree, u64* g_spl,
-                                 TaskParam* tp) {
+                                 TaskParam* tp, u32* btot) {
     u32 kp = 2;
     while (kp < nd + 1) kp <<= 1;
     u32 logk = 0;
@@ -41,6 +41,7 @@ __device__ void build_tree_block(const u64* s_dist, u32 nd, u32 eq, u64* g_tree,
         }
         g_tree[j] = v;
     }
+    for (u32 i = threadIdx.x; i < (u32)MAXK; i += blockDim.x) btot[i] = 0u;
     if (threadIdx.x == 0) {
         tp->kprime = kp;
         tp->logk = logk;
@@ -88,18 +89,25 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
     // stratified random sample without replacement: one element per stratum; sorted in
     // shared memory by the block merge sort of the base case (register networks of
     // SAMPLE/K1_THREADS keys per thread + merge-path passes), padded with the largest key
-    for (u32 j = threadIdx.x; j < (u32)SAMPLE; j += blockDim.x) {
-        u64 key = ~0ull;
+    // (all of a thread's random reads are issued before any is used: each one is a TLB and
+    // DRAM miss somewhere in the array)
+    constexpr int PER = SAMPLE / K1_THREADS;
+    u64 sk[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const u32 j = q * K1_THREADS + threadIdx.x;
+        sk[q] = ~0ull;
         if (j < m) {
             // stratum [a, b) of the task (n * (j+1) < 2^64 for n < 2^50); the offset inside
             // it is the high half of a 64x64-bit product (no division)
             const u64 a = lo + n * j / m;
             const u64 b = lo + n * (j + 1) / m;
             const u64 r = mix64(A.seed ^ mix64(lo * 0x9E3779B97F4A7C15ull + j));
-            key = TR::key(data[a + __umul64hi(r, b - a)], tp->part);
+            sk[q] = TR::key(data[a + __umul64hi(r, b - a)], tp->part);
         }
-        keys[padidx(j)] = key;
     }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) keys[padidx(q * K1_THREADS + threadIdx.x)] = sk[q];
     __syncthreads();
     block_sort_smem<TKey, K1_THREADS, SAMPLE / K1_THREADS>(keys, (u32)SAMPLE);
     // equidistant picks s_i = S[i*alpha - 1]; duplicates?
@@ -127,7 +135,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
         }
     }
     __syncthreads();
-    build_tree_block(dist, s_nd, eq, A.tree + (u64)t * MAXK, A.spl + (u64)t * MAXK, tp);
+    build_tree_block(dist, s_nd, eq, A.tree + (u64)t * MAXK, A.spl + (u64)t * MAXK, tp, A.btot + (u64)t * MAXK);
     if (threadIdx.x == 0 && eq) atomicAdd(&A.ctr[CTR_EQ], 1u);
 }
 
@@ -136,7 +144,7 @@ __global__ void k_tree_from_splitters(LevelArgs A, const u64* splitters, u32 nsp
     __shared__ u64 dist[MAXK];
     for (u32 i = threadIdx.x; i < nspl; i += blockDim.x) dist[i] = splitters[i];
     __syncthreads();
-    build_tree_block(dist, nspl, eq, A.tree, A.spl, const_cast<TaskParam*>(A.tp));
+    build_tree_block(dist, nspl, eq, A.tree, A.spl, const_cast<TaskParam*>(A.tp), A.btot);
 }
 
 }  // namespace ips4o
