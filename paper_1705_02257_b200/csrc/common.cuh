@@ -231,10 +231,13 @@ struct BlockIO {
                 r.w[i] = idx < BB / 4 ? *(volatile const u32*)(blk + 4 * idx) : 0u;
             }
         } else {
-            asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
-                         : "l"(blk + 16 * lane)
-                         : "memory");
+            static_assert(BB % 16 == 0 && BB <= 512, "a block is at most one vector per lane");
+            r.w[0] = r.w[1] = r.w[2] = r.w[3] = 0u;
+            if (16 * lane < BB)
+                asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3])
+                             : "l"(blk + 16 * lane)
+                             : "memory");
         }
         return r;
     }
@@ -246,9 +249,10 @@ struct BlockIO {
                 if (idx < BB / 4) *(volatile u32*)(blk + 4 * idx) = r.w[i];
             }
         } else {
-            asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(blk + 16 * lane), "r"(r.w[0]),
-                         "r"(r.w[1]), "r"(r.w[2]), "r"(r.w[3])
-                         : "memory");
+            if (16 * lane < BB)
+                asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(blk + 16 * lane), "r"(r.w[0]),
+                             "r"(r.w[1]), "r"(r.w[2]), "r"(r.w[3])
+                             : "memory");
         }
     }
     // key part `part` of the block's first element (warp-collective)
