@@ -14,6 +14,9 @@ constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer (SURVEY 
 // Each bucket's permutation control pair: the packed (w, r) word, then its reader count.
 // (Spreading the pairs over 256-byte lines -- one L2 slice each -- measured no faster.)
 constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
+#ifndef IPS4O_K2_LUT  // K2 classifies through the bucket-hint table (1) or the splitter tree only (0)
+#define IPS4O_K2_LUT 1
+#endif
 #ifndef IPS4O_K2_WFLUSH  // K2 flushes buffer blocks by TMA bulk stores (0) or warp copies (1, measured slower)
 #define IPS4O_K2_WFLUSH 0
 #endif
@@ -119,7 +122,16 @@ struct TaskParam {
     u32 kprime, logk, eq, K;      // classifier (written by k_sample or the debug path)
     u32 stripe_begin, nstripes;   // this task's stripes in the stripe table (contiguous)
     u32 part;                     // key part (TRec); 0 otherwise
+    u32 lut_sh;                   // bucket-hint table: cell of key = (key - lut_lo) >> lut_sh
+    u64 lut_lo;                   //   (written with the classifier)
 };
+
+// Bucket-hint table of a task (K2's classification, written with the classifier): the key
+// range [s_1, inf) is cut into LUT_N cells of 2^lut_sh keys from lut_lo = s_1 (keys below s_1
+// use entry LUT_N).  Entry c = A | d << 8: A = #{padded splitters <= the cell's first key},
+// d = #{padded splitters inside the cell}.  The leaf a key reaches in the splitter tree is
+// A + #{j in 1..d : s_{A+j} <= key} (PAPER.md:137-142 computes the same count).
+constexpr u32 LUT_LOG = 12, LUT_N = 1u << LUT_LOG, LUT_STRIDE = LUT_N + 8;  // u16 entries
 
 // A stripe: [begin, end) elements of one task.  Its whole blocks [sb, se) (relative to
 // the task's g) receive the flushed blocks at the front.
@@ -166,6 +178,7 @@ struct LevelArgs {
     u32* dblk;        // [T][257] delimiters d_i (block index, rounded up)
     u32* nfb;         // [T][256] full blocks of bucket i
     u32* btot;        // [T][256] bucket sizes: zeroed by K1, each K2 stripe adds its counts
+    unsigned short* lut;  // [T][LUT_STRIDE] bucket-hint tables
     u32* mov;         // [T][257] prefix of Appendix-A moves over buckets
     u64* wr;          // [T][256] control lines: word 0 packed (w:32 | r+RBIAS:32) block
                       // pointers, word 1 (low half) the bucket's reader count

@@ -72,6 +72,7 @@ struct Workspace {
     u64* s_spbase;
     u64* bnd;
     u32 *dblk, *nfb, *mov, *done, *cflag, *tdone, *btot;
+    unsigned short* lut;
     u64* wr;
     void* ovf;
     int* ovf_owner;
@@ -117,6 +118,7 @@ static size_t fixed_bytes() {
     add((size_t)MAXT * (MAXK + 1) * 8);        // bnd
     add((size_t)MAXT * (MAXK + 1) * 4 * 2);    // dblk, mov
     add((size_t)MAXT * MAXK * 4 * 3);          // nfb, cflag, btot
+    add((size_t)MAXT * LUT_STRIDE * 2);        // bucket-hint tables
     add((size_t)MAXT * (MAXK / 32) * 4);       // done
     add(MAXT / 32 * 4);                        // tdone
     add((size_t)MAXT * MAXK * 8 * CTL_STRIDE);  // wr control lines
@@ -191,6 +193,7 @@ static int ensure_ws(u64 n, int esize) {
     g_ws.nfb = (u32*)nr;
     g_ws.cflag = g_ws.nfb + (size_t)MAXT * MAXK;
     g_ws.btot = g_ws.cflag + (size_t)MAXT * MAXK;
+    g_ws.lut = (unsigned short*)take((size_t)MAXT * LUT_STRIDE * 2);
     g_ws.done = (u32*)take((size_t)MAXT * (MAXK / 32) * 4);
     g_ws.tdone = (u32*)take(MAXT / 32 * 4);
     g_ws.wr = (u64*)take((size_t)MAXT * MAXK * 8 * CTL_STRIDE);
@@ -413,6 +416,7 @@ static LevelArgs level_args(void* data, u32 T, u32 S, int emit, u64 seed) {
     A.dblk = g_ws.dblk;
     A.nfb = g_ws.nfb;
     A.btot = g_ws.btot;
+    A.lut = g_ws.lut;
     A.mov = g_ws.mov;
     A.wr = g_ws.wr;
     A.done = g_ws.done;

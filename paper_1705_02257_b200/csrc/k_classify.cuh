@@ -30,7 +30,9 @@ struct K2Smem {
     static constexpr size_t arr_bytes = 5 * MAXK * 4;
     static constexpr size_t rtree_bytes = (size_t)MAXK * TREE_COPIES * 8;
     static constexpr size_t stage_bytes = (size_t)K2_STAGES * NT * E * TR::S;  // staged tiles
-    static constexpr size_t total = buf_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes + stage_bytes;
+    static constexpr size_t lut_bytes = IPS4O_K2_LUT ? (size_t)LUT_STRIDE * 2 : 0;  // bucket hints
+    static constexpr size_t total =
+        buf_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes + stage_bytes + lut_bytes;
 };
 
 // Loads one tile (<= NT*E elements from tb, len valid) into raw 16-byte registers; bit e of
@@ -241,6 +243,57 @@ __device__ __forceinline__ void k2_bucket_keys(const u64 (&key)[E], u32 valid, c
     }
 }
 
+// Classification through the bucket-hint table (common.cuh): the leaf a key reaches in the
+// splitter tree (the number of padded splitters <= key, ties right) is
+// A + #{j in 1..d : s_{A+j} <= key} for the entry (A, d) of the key's cell.  Nearly every cell
+// holds at most one splitter, so one comparison settles the key; cells with several
+// splitters finish with a binary search over them (all lanes of a warp wait for it only when
+// one of them needs it).  Equality buckets as in k2_bucket_keys.
+template <int E>
+__device__ __forceinline__ void k2_bucket_keys_lut(const u64 (&key)[E], u32 valid, const unsigned short* lut,
+                                                   const u64* spl, u64 lut_lo, u32 lut_sh, u32 eq, u32 (&bk)[E]) {
+    u32 cnt[E], en[E], more = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const u64 y = (key[e] - lut_lo) >> lut_sh;
+        const u32 c = key[e] < lut_lo ? LUT_N : (y >= LUT_N ? LUT_N - 1u : (u32)y);
+        en[e] = lut[c];
+        const u32 A = en[e] & 0xFFu, d = en[e] >> 8;
+        const bool ge = d != 0u && key[e] >= spl[A < (u32)MAXK - 1u ? A + 1u : (u32)MAXK - 1u];
+        cnt[e] = A + (ge ? 1u : 0u);
+        if (ge && d > 1u) more |= 1u << e;
+    }
+    if (__any_sync(0xffffffffu, more != 0u)) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if (more & (1u << e)) {
+                // s_l <= key for l = A+1; candidates s_{l+1} .. s_{l+n}
+                u32 l = cnt[e], n = (en[e] >> 8) - 1u;
+                while (n) {
+                    const u32 h = (n + 1u) >> 1;
+                    if (key[e] >= spl[l + h]) {
+                        l += h;
+                        n -= h;
+                    } else {
+                        n = h - 1u;
+                    }
+                }
+                cnt[e] = l;
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        u32 i = cnt[e];
+        if (eq) {
+            const u32 ii = i ? i : 1u;
+            const bool isq = i >= 1u && spl[ii] >= key[e];
+            i = 2 * i - (isq ? 1u : 0u);
+        }
+        bk[e] = ((valid >> e) & 1u) ? i : INV_BUCKET;
+    }
+}
+
 // Elements of a tile that start a bucket's next buffer block while the buffer's completed
 // block is still being flushed: kept in registers and written into the buffer during the
 // next tile's placement, after the flush has read the buffer (so the TMA read latency
@@ -260,7 +313,7 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
                                         u32* slotb, u32* nfl, u32* s_nflushed, u32 logk,
                                         u32 kprime, u32 eq, const typename TR::V* refill,
                                         typename TR::V* refill_stage, u64* refill_mbar, K2Defer<TR, E>& df,
-                                        bool& agg) {
+                                        bool& agg, const unsigned short* lut, u64 lut_lo, u32 lut_sh) {
     typedef typename TR::V V;
     constexpr int B = TR::B;
     const u32 tid = threadIdx.x;
@@ -275,7 +328,11 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         u64 key[E];
 #pragma unroll
         for (int e = 0; e < E; ++e) key[e] = TR::key(v[e], 0);
+#if IPS4O_K2_LUT
+        k2_bucket_keys_lut<E>(key, valid, lut, spl, lut_lo, lut_sh, eq, bk);
+#else
         k2_bucket_keys<E, LOGK>(key, valid, tree, spl, logk, kprime, eq, bk);
+#endif
     }
     // (skewed tiles -- sorted runs, equal keys: the previous tile put more than 1/8 of its
     // elements into one bucket -- check each slot for a warp whose 32 elements share a
@@ -431,6 +488,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
     u64* rtree = reinterpret_cast<u64*>(smem + SM::buf_bytes + SM::wcnt_bytes + SM::tree_bytes + SM::arr_bytes);
     V* stage = reinterpret_cast<V*>(smem + SM::buf_bytes + SM::wcnt_bytes + SM::tree_bytes + SM::arr_bytes +
                                     SM::rtree_bytes);
+    unsigned short* lut = reinterpret_cast<unsigned short*>(reinterpret_cast<unsigned char*>(stage) + SM::stage_bytes);
     __shared__ u32 s_stripe, s_nflushed, s_wsum[NT / 32];
     __shared__ u64 s_spbase;
     __shared__ __align__(8) u64 s_mbar[2];
@@ -462,6 +520,10 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             nbl[tid] = 0;
         }
         rtree_fill(rtree, A.tree + (u64)sd.task * MAXK, tid, NT);
+        if (IPS4O_K2_LUT) {
+            const uint4* gl = reinterpret_cast<const uint4*>(A.lut + (u64)sd.task * LUT_STRIDE);
+            for (u32 i = tid; i < LUT_STRIDE * 2 / 16; i += NT) reinterpret_cast<uint4*>(lut)[i] = gl[i];
+        }
         if (tid == 0) s_nflushed = 0;
         __syncthreads();
         const u64 mb = sd.begin > tp.g ? sd.begin : tp.g;  // stripe main region start (block aligned)
@@ -505,18 +567,18 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
                 if (tp.logk == 8 && !agg)
                     k2_tile<TR, NT, E, 8, false>(data, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                                  slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
-                                                 refill, stage + st * TILE, &s_mbar[st], df, agg);
+                                                 refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);
                 else
                     k2_tile<TR, NT, E, 0, true>(data, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                                 slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
-                                                refill, stage + st * TILE, &s_mbar[st], df, agg);
+                                                refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);
             }
             const u64 tb = mb + nft * TILE;
             if (tb < me) {
                 const u32 vt = k2_load<TR, NT, E>(data, tb, (u32)(me - tb), cur);
                 k2_tile<TR, NT, E, 0, true>(data, cur, vt, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                       slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
-                                      nullptr, nullptr, nullptr, df, agg);
+                                      nullptr, nullptr, nullptr, df, agg, lut, tp.lut_lo, tp.lut_sh);
             }
         }
         if (sd.first && tp.lo < tp.g) {
@@ -526,7 +588,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             uint4 hv[E / TR::VEC];
             const u32 hval = k2_load<TR, NT, E>(data, tp.lo, (u32)(hend - tp.lo), hv);
             k2_tile<TR, NT, E, 0, true>(data, hv, hval, true, mb, cap, buf, nbl, rtree, spl, fill, cnt, slotb, nfl,
-                           &s_nflushed, tp.logk, tp.kprime, tp.eq, nullptr, nullptr, nullptr, df, agg);
+                           &s_nflushed, tp.logk, tp.kprime, tp.eq, nullptr, nullptr, nullptr, df, agg, lut, tp.lut_lo, tp.lut_sh);
         }
         k2_drain<TR, E>(buf, df);
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area

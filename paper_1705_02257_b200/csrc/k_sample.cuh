@@ -20,8 +20,49 @@ constexpr u64 K1_BIG_TASK = 1ull << 22;
 // Builds the padded splitter array spl[1..k'-1] and the BFS tree from nd distinct sorted
 // splitters held in s_dist[0..nd).  k' = next power of two >= nd+1; padding repeats the
 // largest splitter.  Writes the task's classifier fields.
+// Bucket-hint table (common.cuh, LUT_N): for every cell, A = #{padded splitters <= the
+// cell's first key} and d = #{padded splitters inside the cell}, by binary search over the
+// padded splitters s_i = s_dist[min(i, nd) - 1], i in [1, kp-1].
+__device__ void build_lut_block(const u64* s_dist, u32 nd, u32 kp, unsigned short* g_lut, TaskParam* tp) {
+    auto S = [&](u32 i) { return s_dist[(i <= nd ? i : nd) - 1]; };
+    auto C = [&](u64 v) {  // #{i in [1, kp-1] : s_i <= v}
+        u32 lo = 0, hi = kp - 1;
+        while (lo < hi) {
+            const u32 mid = (lo + hi + 1) >> 1;
+            if (S(mid) <= v) lo = mid;
+            else hi = mid - 1;
+        }
+        return lo;
+    };
+    const u64 lo = S(1), span = S(kp - 1) - lo;
+    u32 sh = 0;
+    if (span) {
+        const u32 bl = 64u - (u32)__clzll((long long)span);
+        sh = bl > LUT_LOG ? bl - LUT_LOG : 0u;  // span >> sh < LUT_N
+    }
+    for (u32 c = threadIdx.x; c < LUT_STRIDE; c += blockDim.x) {
+        u32 e = 0;  // entry LUT_N (keys below s_1) and the padding: A = d = 0
+        if (c < LUT_N) {
+            const u64 off0 = (u64)c << sh;
+            const u64 c0 = off0 > ~0ull - lo ? ~0ull : lo + off0;
+            u64 c1 = ~0ull;  // the last cell extends to the largest key
+            if (c + 1 < LUT_N) {
+                const u64 off1 = ((u64)(c + 1) << sh) - 1;
+                c1 = off1 > ~0ull - lo ? ~0ull : lo + off1;
+            }
+            const u32 A = C(c0), d = C(c1) - A;
+            e = A | d << 8;
+        }
+        g_lut[c] = (unsigned short)e;
+    }
+    if (threadIdx.x == 0) {
+        tp->lut_lo = lo;
+        tp->lut_sh = sh;
+    }
+}
+
 __device__ void build_tree_block(const u64* s_dist, u32 nd, u32 eq, u64* g_tree, u64* g_spl,
-                                 TaskParam* tp, u32* btot) {
+                                 TaskParam* tp, u32* btot, unsigned short* g_lut) {
     u32 kp = 2;
     while (kp < nd + 1) kp <<= 1;
     u32 logk = 0;
@@ -48,6 +89,7 @@ __device__ void build_tree_block(const u64* s_dist, u32 nd, u32 eq, u64* g_tree,
         tp->eq = eq;
         tp->K = eq ? 2 * kp - 1 : kp;
     }
+    build_lut_block(s_dist, nd, kp, g_lut, tp);
 }
 
 // the sample's keys as a base-case element type (order-preserving u64 images)
@@ -135,7 +177,8 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
         }
     }
     __syncthreads();
-    build_tree_block(dist, s_nd, eq, A.tree + (u64)t * MAXK, A.spl + (u64)t * MAXK, tp, A.btot + (u64)t * MAXK);
+    build_tree_block(dist, s_nd, eq, A.tree + (u64)t * MAXK, A.spl + (u64)t * MAXK, tp, A.btot + (u64)t * MAXK,
+                     A.lut + (u64)t * LUT_STRIDE);
     if (threadIdx.x == 0 && eq) atomicAdd(&A.ctr[CTR_EQ], 1u);
 }
 
@@ -144,7 +187,7 @@ __global__ void k_tree_from_splitters(LevelArgs A, const u64* splitters, u32 nsp
     __shared__ u64 dist[MAXK];
     for (u32 i = threadIdx.x; i < nspl; i += blockDim.x) dist[i] = splitters[i];
     __syncthreads();
-    build_tree_block(dist, nspl, eq, A.tree, A.spl, const_cast<TaskParam*>(A.tp), A.btot);
+    build_tree_block(dist, nspl, eq, A.tree, A.spl, const_cast<TaskParam*>(A.tp), A.btot, A.lut);
 }
 
 }  // namespace ips4o
