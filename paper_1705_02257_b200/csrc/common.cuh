@@ -20,8 +20,8 @@ constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
 #ifndef IPS4O_K2_WFLUSH  // K2 flushes buffer blocks by TMA bulk stores (0) or warp copies (1, measured slower)
 #define IPS4O_K2_WFLUSH 0
 #endif
-#ifndef IPS4O_K2_STAGES
-#define IPS4O_K2_STAGES 1
+#ifndef IPS4O_K2_STAGES  // two TMA tile stages when the tree copies are not needed
+#define IPS4O_K2_STAGES (IPS4O_K2_LUT ? 2 : 1)
 #endif
 constexpr int K2_STAGES = IPS4O_K2_STAGES;   // tiles staged ahead in K2 (TMA)
 // replicated splitter tree in K2: 16 copies (conflict-free lookups) when shared memory

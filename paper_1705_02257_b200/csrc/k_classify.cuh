@@ -28,7 +28,7 @@ struct K2Smem {
     static constexpr size_t wcnt_bytes = 0;
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
     static constexpr size_t arr_bytes = 5 * MAXK * 4;
-    static constexpr size_t rtree_bytes = (size_t)MAXK * TREE_COPIES * 8;
+    static constexpr size_t rtree_bytes = IPS4O_K2_LUT ? 0 : (size_t)MAXK * TREE_COPIES * 8;  // tree copies
     static constexpr size_t stage_bytes = (size_t)K2_STAGES * NT * E * TR::S;  // staged tiles
     static constexpr size_t lut_bytes = IPS4O_K2_LUT ? (size_t)LUT_STRIDE * 2 : 0;  // bucket hints
     static constexpr size_t total =
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
             cnt[tid] = 0;
             nbl[tid] = 0;
         }
-        rtree_fill(rtree, A.tree + (u64)sd.task * MAXK, tid, NT);
+        if (!IPS4O_K2_LUT) rtree_fill(rtree, A.tree + (u64)sd.task * MAXK, tid, NT);
         if (IPS4O_K2_LUT) {
             const uint4* gl = reinterpret_cast<const uint4*>(A.lut + (u64)sd.task * LUT_STRIDE);
             for (u32 i = tid; i < LUT_STRIDE * 2 / 16; i += NT) reinterpret_cast<uint4*>(lut)[i] = gl[i];
