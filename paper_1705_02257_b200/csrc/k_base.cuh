@@ -240,6 +240,9 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
 // whose cells would need too much insertion work (keys clustered far below the resolution
 // of the cells, e.g. heavy duplicates) is handed to the merge-sort kernel (fallback queue)
 // untouched.
+#ifndef IPS4O_BASE_TMA_WB  // write sorted leaves back by TMA bulk stores (1) or plain stores (0)
+#define IPS4O_BASE_TMA_WB 1
+#endif
 // Phase profile of the cell base case (tuning builds only): thread 0 of each CTA adds the
 // clock64 intervals between the leaf's barriers; the host prints the shares per class.
 #ifdef IPS4O_BASE_PROF
@@ -268,7 +271,7 @@ __device__ unsigned long long g_base_prof[2][8];
 template <class TR, int NT, int E>
 struct CellBase {
     static constexpr u32 TILE = NT * E;                  // a power of two
-    static constexpr size_t x_bytes = (size_t)TILE * sizeof(typename TR::V);
+    static constexpr size_t x_bytes = (size_t)TILE * sizeof(typename TR::V) + 16;  // + alignment shift
     static constexpr size_t cnt_bytes = (size_t)((E + 4) * NT + 8) * 4;
     static constexpr size_t smem = x_bytes + cnt_bytes;
 };
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
     constexpr int NW = NT / 32;
     static_assert(E % 4 == 0, "cell runs are read as 128-bit vectors");
     extern __shared__ __align__(16) unsigned char smc[];
-    V* X = reinterpret_cast<V*>(smc);
+    V* const X0 = reinterpret_cast<V*>(smc);
     u32* cnt = reinterpret_cast<u32*>(smc + CB::x_bytes);
     __shared__ u64 s_range[2];
     __shared__ u32 s_flag, s_wsum[NW];
@@ -296,6 +299,10 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
         const TaskDesc td = tasks[ti];
         const u32 n = (u32)(td.hi - td.lo);
         V* g = data + td.lo;
+        // the leaf in shared memory starts at the same offset modulo 16 bytes as in global
+        // memory, so that its aligned body leaves by one TMA bulk store
+        const u32 p = sizeof(V) == 8 ? (u32)((reinterpret_cast<uintptr_t>(g) >> 3) & 1u) : 0u;
+        V* const X = X0 + p;
         const u32 cb = n > 1 ? 32u - (u32)__clz(n - 1) : 1u;  // 2^cb >= n cells
         const u32 ncell = 1u << cb;
         __syncthreads();  // the previous leaf is finished
@@ -388,6 +395,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
             }
         }
         if (bigwork && mul) atomicAdd(&s_flag, bigwork);
+        if (IPS4O_BASE_TMA_WB && tid == 0) bulk_wait_read0();  // the previous leaf has left X
         __syncthreads();
         BASE_PROF_MARK(5);
         if (s_flag > CELL_FIX_BUDGET) {
@@ -463,11 +471,30 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
                 }
             }
         }
+#if IPS4O_BASE_TMA_WB
+        fence_proxy_async_smem();
+        __syncthreads();
+        BASE_PROF_MARK(7);
+        // 5. write back: the 16-byte aligned body by one TMA bulk store (read before the next
+        //    leaf's scatter), the element before / after it by plain stores
+        {
+            const u32 i0 = p < n ? p : n;
+            const u32 i1 = sizeof(V) == 8 ? i0 + ((n - i0) & ~1u) : n;
+            if (tid == 0 && i1 > i0) {
+                bulk_s2g(g + i0, X + i0, (i1 - i0) * (u32)sizeof(V));
+                bulk_commit();
+            }
+            if (tid == 32 && i0 > 0) g[0] = X[0];
+            if (tid == 64 && i1 < n) g[n - 1] = X[n - 1];
+        }
+#else
         __syncthreads();
         BASE_PROF_MARK(7);
         // 5. write back
         for (u32 i = tid; i < n; i += NT) g[i] = X[i];
+#endif
     }
+    if (IPS4O_BASE_TMA_WB && tid == 0) bulk_wait0();
     BASE_PROF_FLUSH(NT >= 512 ? 1 : 0);
 }
 
