@@ -255,13 +255,16 @@ __device__ __forceinline__ void k2_bucket_keys_lut(const u64 (&key)[E], u32 vali
     u32 cnt[E], en[E], more = 0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
+        // (branch-free: every key loads its cell's first splitter, used only if d > 0)
         const u64 y = (key[e] - lut_lo) >> lut_sh;
-        const u32 c = key[e] < lut_lo ? LUT_N : (y >= LUT_N ? LUT_N - 1u : (u32)y);
+        u32 c = (y >> LUT_LOG) != 0ull ? LUT_N - 1u : (u32)y;
+        c = key[e] < lut_lo ? LUT_N : c;
         en[e] = lut[c];
         const u32 A = en[e] & 0xFFu, d = en[e] >> 8;
-        const bool ge = d != 0u && key[e] >= spl[A < (u32)MAXK - 1u ? A + 1u : (u32)MAXK - 1u];
-        cnt[e] = A + (ge ? 1u : 0u);
-        if (ge && d > 1u) more |= 1u << e;
+        const u64 s1 = spl[min(A + 1u, (u32)MAXK - 1u)];
+        const u32 ge = (u32)(key[e] >= s1) & (u32)(d != 0u);
+        cnt[e] = A + ge;
+        more |= (ge & (u32)(d > 1u)) << e;
     }
     if (__any_sync(0xffffffffu, more != 0u)) {
 #pragma unroll
