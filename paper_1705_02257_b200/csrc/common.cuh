@@ -320,6 +320,10 @@ __device__ __forceinline__ void mbar_wait(u64* mbar, u32 parity) {
                  "@!p bra W;\n\t}" ::"r"(mb), "r"(parity)
                  : "memory");
 }
+// TMA bulk prefetch of [src, src+bytes) into L2 (16-byte aligned, multiple of 16)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, u32 bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

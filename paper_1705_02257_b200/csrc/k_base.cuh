@@ -295,8 +295,12 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     uint4* myrun = reinterpret_cast<uint4*>(cnt + cpad<E>(tid * E));  // this thread's E counters
     BASE_PROF_INIT();
+    // the next leaf's descriptor is read one leaf ahead, and its elements are prefetched
+    // into L2 by a TMA bulk prefetch during the current leaf (its load then hits L2)
+    TaskDesc tnext = blockIdx.x < ntasks ? tasks[blockIdx.x] : TaskDesc{0, 0, 0, 0};
     for (u32 ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
-        const TaskDesc td = tasks[ti];
+        const TaskDesc td = tnext;
+        if (ti + gridDim.x < ntasks) tnext = tasks[ti + gridDim.x];
         const u32 n = (u32)(td.hi - td.lo);
         V* g = data + td.lo;
         // the leaf in shared memory starts at the same offset modulo 16 bytes as in global
@@ -341,6 +345,11 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
         }
         __syncthreads();
         BASE_PROF_MARK(2);
+        if (tid == 0 && ti + gridDim.x < ntasks) {
+            const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + tnext.lo) & ~(uintptr_t)15;
+            const uintptr_t a1 = (reinterpret_cast<uintptr_t>(data + tnext.hi) + 15) & ~(uintptr_t)15;
+            if (a1 > a0) bulk_prefetch_l2(reinterpret_cast<const void*>(a0), (u32)(a1 - a0));
+        }
         kmin = s_range[0];
         const u64 span = s_range[1] - kmin;
         if (span == 0) continue;  // all keys equal: already sorted (no write)
