@@ -439,44 +439,64 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
                 bs[4 * k + 3] = q.w;
             }
             bs[E] = tid + 1 < (u32)NT ? cnt[cpad<E>((tid + 1) * E)] : n;
-            u32 mask = 0;
+            // cells of 2 (most multi-element cells), of 3-4 and larger ones in separate
+            // loops, so that a warp's lanes run the same code in each
+            u32 m2 = 0, m34 = 0, mbig = 0;
 #pragma unroll
-            for (int k = 0; k < E; ++k) mask |= (bs[k + 1] - bs[k] > 1u ? 1u : 0u) << k;
+            for (int k = 0; k < E; ++k) {
+                const u32 m = bs[k + 1] - bs[k];
+                m2 |= (m == 2u ? 1u : 0u) << k;
+                m34 |= (m == 3u || m == 4u ? 1u : 0u) << k;
+                mbig |= (m > 4u ? 1u : 0u) << k;
+            }
             const u32 enext = bs[E];
-            while (mask) {
-                const u32 k = (u32)__ffs(mask) - 1u;
-                mask &= mask - 1u;
+            while (m2) {
+                const u32 k = (u32)__ffs(m2) - 1u;
+                m2 &= m2 - 1u;
+                const u32 b = cnt[cpad<E>(tid * E + k)];
+                const V x0 = X[b], x1 = X[b + 1];
+                if (TR::less(x1, x0)) {
+                    X[b] = x1;
+                    X[b + 1] = x0;
+                }
+            }
+            while (m34) {
+                const u32 k = (u32)__ffs(m34) - 1u;
+                m34 &= m34 - 1u;
                 const u32 b = cnt[cpad<E>(tid * E + k)];
                 const u32 e = k + 1 < (u32)E ? cnt[cpad<E>(tid * E + k + 1)] : enext;
-                if (e - b <= 4u) {
-                    const V pd = TR::pad();
-                    V x0 = X[b], x1 = X[b + 1];
-                    V x2 = e - b > 2u ? X[b + 2] : pd, x3 = e - b > 3u ? X[b + 3] : pd;
-                    auto cas = [](V& lo, V& hi) {
-                        const bool sw = TR::less(hi, lo);
-                        const V t = sw ? hi : lo;
-                        hi = sw ? lo : hi;
-                        lo = t;
-                    };
-                    cas(x0, x1);
-                    cas(x2, x3);
-                    cas(x0, x2);
-                    cas(x1, x3);
-                    cas(x1, x2);
-                    X[b] = x0;
-                    X[b + 1] = x1;
-                    if (e - b > 2u) X[b + 2] = x2;
-                    if (e - b > 3u) X[b + 3] = x3;
-                } else {
-                    for (u32 i = b + 1; i < e; ++i) {
-                        const V x = X[i];
-                        u32 q = i;
-                        while (q > b && TR::less(x, X[q - 1])) {
-                            X[q] = X[q - 1];
-                            --q;
-                        }
-                        X[q] = x;
+                const V pd = TR::pad();
+                V x0 = X[b], x1 = X[b + 1], x2 = X[b + 2];
+                V x3 = e - b > 3u ? X[b + 3] : pd;
+                auto cas = [](V& lo, V& hi) {
+                    const bool sw = TR::less(hi, lo);
+                    const V t = sw ? hi : lo;
+                    hi = sw ? lo : hi;
+                    lo = t;
+                };
+                cas(x0, x1);
+                cas(x2, x3);
+                cas(x0, x2);
+                cas(x1, x3);
+                cas(x1, x2);
+                X[b] = x0;
+                X[b + 1] = x1;
+                X[b + 2] = x2;
+                if (e - b > 3u) X[b + 3] = x3;
+            }
+            while (mbig) {
+                const u32 k = (u32)__ffs(mbig) - 1u;
+                mbig &= mbig - 1u;
+                const u32 b = cnt[cpad<E>(tid * E + k)];
+                const u32 e = k + 1 < (u32)E ? cnt[cpad<E>(tid * E + k + 1)] : enext;
+                for (u32 i = b + 1; i < e; ++i) {
+                    const V x = X[i];
+                    u32 q = i;
+                    while (q > b && TR::less(x, X[q - 1])) {
+                        X[q] = X[q - 1];
+                        --q;
                     }
+                    X[q] = x;
                 }
             }
         }
