@@ -111,6 +111,27 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
             __threadfence();
             for (u32 gi = 0; gi < K4_GROUP; ++gi) st_release_u32(flag + b0 + gi, 1u);
         }
+        // the group's partial-buffer lengths and spill positions, one round trip: lane
+        // 8g + j holds stripe j of bucket b0 + g (tasks of at most 8 stripes -- the lower
+        // levels); g_excl = its offset among the bucket's spilled elements
+        const bool few = NS <= 8u;
+        u32 g_excl = 0, g_incl = 0;
+        u64 g_src = 0;
+        if (few) {
+            const u32 gg = lane >> 3, j = lane & 7u;
+            u32 len = 0;
+            if (j < NS && b0 + gg < tp.K) {
+                len = A.s_fill[(u64)(S0 + j) * MAXK + b0 + gg];
+                g_src = A.s_spbase[S0 + j] + A.s_spoff[(u64)(S0 + j) * MAXK + b0 + gg];
+            }
+            g_incl = len;
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                const u32 y = __shfl_up_sync(0xffffffffu, g_incl, o, 8);
+                if (j >= (u32)o) g_incl += y;
+            }
+            g_excl = g_incl - len;
+        }
         // 2. each bucket: gather its partial blocks into its empty slots, then emit it
 #pragma unroll 1
         for (u32 gi = 0; gi < K4_GROUP; ++gi) {
@@ -126,8 +147,8 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
             const u64 in_end = own_ovf ? tp.g + (u64)(tp.nblocks - 1) * B : tp.g + (u64)wfin * B;
             const u32 ovl = (in_end > db_el && in_end > e1) ? (u32)(in_end - e1) : 0u;
             // spilled partial buffers of every stripe of this task for bucket b
-            u32 sp_total = 0;
-            for (u32 base = 0; base < NS; base += 32) {
+            u32 sp_total = few ? __shfl_sync(0xffffffffu, g_incl, 8 * gi + 7) : 0u;
+            for (u32 base = 0; !few && base < NS; base += 32) {
                 const u32 j = base + lane;
                 const u32 len = j < NS ? A.s_fill[(u64)(S0 + j) * MAXK + b] : 0u;
                 u32 incl = len;
@@ -139,7 +160,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
                 if (j < NS) s_pref[j] = sp_total + incl - len;
                 sp_total += __shfl_sync(0xffffffffu, incl, 31);
             }
-            if (lane == 0) s_pref[NS] = sp_total;
+            if (lane == 0 && !few) s_pref[NS] = sp_total;
             __syncwarp();
             const u32 nsrc = ovl + sp_total + (own_ovf ? (u32)B : 0u);
             const u64 hend = db_el < e1 ? db_el : e1;
@@ -165,8 +186,26 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
             }
             __syncwarp();
             const V* ovf = reinterpret_cast<const V*>(A.ovf) + (u64)t * B;
+            if (few) {
+                // stripe of each spilled source from the lanes of this bucket's segment
+                for (u32 k0 = 0; k0 < nsrc; k0 += 32) {
+                    const u32 k = k0 + lane, kk = k - ovl;
+                    u32 lo = 0;
+                    for (u32 j = 1; j < NS; ++j)
+                        if (kk >= __shfl_sync(0xffffffffu, g_excl, 8 * gi + j)) lo = j;
+                    const u64 sbase = __shfl_sync(0xffffffffu, g_src, 8 * gi + lo);
+                    const u32 pre = __shfl_sync(0xffffffffu, g_excl, 8 * gi + lo);
+                    if (k < nsrc) {
+                        V val;
+                        if (k < ovl) val = s_ovh[k];
+                        else if (kk < sp_total) val = spill[sbase + (kk - pre)];
+                        else val = ovf[kk - sp_total];
+                        data[(u64)k < hl ? e0 + k : ts + (k - hl)] = val;
+                    }
+                }
+            }
             u32 jcur = 0;  // stripe of the previous source (sources are visited in order)
-            for (u32 k = lane; k < nsrc; k += 32) {
+            for (u32 k = few ? nsrc : lane; k < nsrc; k += 32) {
                 V val;
                 if (k < ovl) {
                     val = s_ovh[k];
@@ -228,6 +267,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A) {
     constexpr int B = TR::B;
     __shared__ V s_ovh[B];
     __shared__ u32 s_pref[K4_MAXSTRIPES + 1];
+    __shared__ u64 s_src[K4_MAXSTRIPES];  // spill position of stripe j's partial buffer for b
     __shared__ u32 s_wsum[K4_THREADS / 32];
     __shared__ u32 s_ticket;
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -276,7 +316,10 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A) {
             if (ww < w) woff += s_wsum[ww];
             tot += s_wsum[ww];
         }
-        if (j < NS) s_pref[j] = sp_total + woff + incl - len;
+        if (j < NS) {
+            s_pref[j] = sp_total + woff + incl - len;
+            s_src[j] = A.s_spbase[S0 + j] + A.s_spoff[(u64)(S0 + j) * MAXK + b];
+        }
         sp_total += tot;
         __syncthreads();
     }
@@ -306,25 +349,35 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A) {
     __syncthreads();
     const V* spill = reinterpret_cast<const V*>(A.spill);
     const V* ovf = reinterpret_cast<const V*>(A.ovf) + (u64)t * B;
-    for (u32 k = tid; k < nsrc; k += blockDim.x) {
-        V val;
-        if (k < ovl) {
-            val = s_ovh[k];
-        } else if (k - ovl < sp_total) {
+    // gather: four sources per thread in flight (each is a stripe lookup in shared memory
+    // and one dependent load)
+    auto src_of = [&](u32 k) -> V {
+        if (k < ovl) return s_ovh[k];
+        if (k - ovl < sp_total) {
             const u32 kk = k - ovl;
             u32 lo = 0, hi = NS;  // last j with s_pref[j] <= kk
             while (hi - lo > 1) {
-                u32 mid = (lo + hi) >> 1;
+                const u32 mid = (lo + hi) >> 1;
                 if (s_pref[mid] <= kk) lo = mid;
                 else hi = mid;
             }
-            const u64 at = A.s_spbase[S0 + lo] + A.s_spoff[(u64)(S0 + lo) * MAXK + b] + (kk - s_pref[lo]);
-            val = spill[at];
-        } else {
-            val = ovf[k - ovl - sp_total];
+            return spill[s_src[lo] + (kk - s_pref[lo])];
         }
-        const u64 dst = (u64)k < hl ? e0 + k : ts + (k - hl);
-        data[dst] = val;
+        return ovf[k - ovl - sp_total];
+    };
+    auto dst_of = [&](u32 k) { return (u64)k < hl ? e0 + k : ts + (k - hl); };
+    for (u32 k0 = tid; k0 < nsrc; k0 += 4 * K4_THREADS) {
+        V val[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const u32 k = k0 + q * K4_THREADS;
+            if (k < nsrc) val[q] = src_of(k);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const u32 k = k0 + q * K4_THREADS;
+            if (k < nsrc) data[dst_of(k)] = val[q];
+        }
     }
     // emit the bucket (PAPER.md:342 for equality buckets)
     if (tid == 0 && A.emit) {
