@@ -22,8 +22,10 @@ struct K2RecSmem {
     static constexpr size_t wcnt_bytes = 0;
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
     static constexpr size_t arr_bytes = 5 * MAXK * 4;
-    static constexpr size_t rtree_bytes = (size_t)MAXK * TREE_COPIES * 8;
-    static constexpr size_t total = buf_bytes + stage_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes;
+    static constexpr size_t rtree_bytes = IPS4O_K2_LUT ? 0 : (size_t)MAXK * TREE_COPIES * 8;
+    static constexpr size_t lut_bytes = IPS4O_K2_LUT ? (size_t)LUT_STRIDE * 2 : 0;  // bucket hints
+    static constexpr size_t total =
+        buf_bytes + stage_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes + lut_bytes;
 };
 
 __device__ __forceinline__ void copy_rec(u32* dst, const u32* src) {
@@ -59,6 +61,7 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
     constexpr u32 RT = NT * RPT;  // records per tile
     u64* rtree = reinterpret_cast<u64*>(smem + SM::buf_bytes + SM::stage_bytes + SM::wcnt_bytes + SM::tree_bytes +
                                         SM::arr_bytes);
+    unsigned short* lut = reinterpret_cast<unsigned short*>(reinterpret_cast<unsigned char*>(rtree) + SM::rtree_bytes);
     __shared__ u32 s_stripe, s_nflushed, s_wsum[NW];
     __shared__ u64 s_spbase;
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -81,7 +84,11 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
             cnt[b] = 0;
             nbl[b] = 0;
         }
-        rtree_fill(rtree, A.tree + (u64)sd.task * MAXK, tid, NT);
+        if (!IPS4O_K2_LUT) rtree_fill(rtree, A.tree + (u64)sd.task * MAXK, tid, NT);
+        if (IPS4O_K2_LUT) {
+            const uint4* gl = reinterpret_cast<const uint4*>(A.lut + (u64)sd.task * LUT_STRIDE);
+            for (u32 i = tid; i < LUT_STRIDE * 2 / 16; i += NT) reinterpret_cast<uint4*>(lut)[i] = gl[i];
+        }
         if (tid == 0) s_nflushed = 0;
         __syncthreads();
         // the block grid starts at g, the first 16-byte aligned record >= lo (TMA block
@@ -135,8 +142,12 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
                 valid |= (ok ? 1u : 0u) << r;
             }
             u32 bk[RS], pos[RS];
+#if IPS4O_K2_LUT
+            k2_bucket_keys_lut<RS>(key, valid, lut, spl, tp.lut_lo, tp.lut_sh, tp.eq, bk);
+#else
             if (tp.logk == 8) k2_bucket_keys<RS, 8>(key, valid, rtree, spl, tp.logk, tp.kprime, tp.eq, bk);
             else k2_bucket_keys<RS, 0>(key, valid, rtree, spl, tp.logk, tp.kprime, tp.eq, bk);
+#endif
 #pragma unroll
             for (int r = 0; r < RS; ++r)
                 if (bk[r] != INV_BUCKET) pos[r] = atomicAdd(&cnt[bk[r]], 1u);
@@ -189,10 +200,7 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
         if (tid < nhead) {
             const u32* my = s_head + tid * RW;
             u64 hk[1] = {tp.part ? TRec::lo_of(my[2]) : TRec::hi_of(my[0], my[1])};
-            u32 hb[1];
-            if (tp.logk == 8) k2_bucket_keys<1, 8>(hk, 1u, rtree, spl, tp.logk, tp.kprime, tp.eq, hb);
-            else k2_bucket_keys<1, 0>(hk, 1u, rtree, spl, tp.logk, tp.kprime, tp.eq, hb);
-            s_hb[tid] = hb[0];
+            s_hb[tid] = classify_key(hk[0], tree, spl, tp.logk, tp.kprime, tp.eq);  // (a partial warp)
         }
         __syncthreads();
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area
