@@ -304,7 +304,7 @@ __device__ __forceinline__ void k2_bucket_keys_lut(const u64 (&key)[E], u32 vali
 template <class TR, int E>
 struct K2Defer {
     typename TR::V v[E];
-    u32 off[E], bk[E];
+    u32 idx[E];  // buffer slot: bucket * B + offset
     u32 mask;
 };
 
@@ -354,6 +354,8 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
             }
         }
         if (!done && bk[j] != INV_BUCKET) pos[j] = atomicAdd(&cnt[bk[j]], 1u);
+        // bucket (< 2^16) and position (< B + tile < 2^16) in one register until placement
+        if (bk[j] != INV_BUCKET) bk[j] |= pos[j] << 16;
     }
     __syncthreads();
     if (refill && tid == 0) {
@@ -400,13 +402,13 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     //    next block -> deferred
 #pragma unroll
     for (int j = 0; j < E; ++j)
-        if (df.mask & (1u << j)) buf[df.bk[j] * B + df.off[j]] = df.v[j];
+        if (df.mask & (1u << j)) buf[df.idx[j]] = df.v[j];
     u32 defer = 0;
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-        const u32 b = bk[j];
-        if (b == INV_BUCKET) continue;
-        const u32 p = pos[j];
+        if (bk[j] == INV_BUCKET) continue;
+        const u32 b = bk[j] & 0xFFFFu;
+        const u32 p = bk[j] >> 16;
         const u32 q = p / B, off = p % B;
         if (q == 0) {
             buf[b * B + off] = v[j];
@@ -416,8 +418,7 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
                 data[mb + (u64)(slotb[b] + q) * B + off] = v[j];
             } else {
                 df.v[j] = v[j];
-                df.off[j] = p - nf * B;
-                df.bk[j] = b;
+                df.idx[j] = b * B + (p - nf * B);
                 defer |= 1u << j;
             }
         }
@@ -468,7 +469,7 @@ __device__ __forceinline__ void k2_drain(typename TR::V* buf, K2Defer<TR, E>& df
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < E; ++j)
-        if (df.mask & (1u << j)) buf[df.bk[j] * TR::B + df.off[j]] = df.v[j];
+        if (df.mask & (1u << j)) buf[df.idx[j]] = df.v[j];
     df.mask = 0;
     __syncthreads();
 }
