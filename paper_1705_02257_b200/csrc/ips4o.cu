@@ -273,6 +273,9 @@ static cudaError_t set_base_attr1() {
 }
 // cell base-case configurations of the size classes <= 2048 and <= 4096 (threads,
 // elements per thread); the <= 8192 class uses (512, 16)
+#ifndef IPS4O_CELL_BIG_NT  // threads of the base-case CTA for leaves of 4097..8192 elements
+#define IPS4O_CELL_BIG_NT 512
+#endif
 #ifndef IPS4O_CELL_SMALL
 #define IPS4O_CELL_SMALL 1
 #endif
@@ -282,6 +285,7 @@ template <class TR> struct CellCfg {
     static constexpr bool small = IPS4O_CELL_SMALL && TR::S == 8;
     static constexpr int NT0 = small ? 128 : 256, E0 = small ? 16 : 8;
     static constexpr int NT1 = small ? 256 : 512, E1 = small ? 16 : 8;
+    static constexpr int NT2 = IPS4O_CELL_BIG_NT, E2 = 8192 / IPS4O_CELL_BIG_NT;  // leaves of <= 8192
 };
 template <class TR, int NT, int E>
 static cudaError_t set_cell_attr() {
@@ -293,7 +297,7 @@ static cudaError_t set_base_attrs() {
     cudaError_t e = set_base_attr1<TR, (TR::CAP >= 16384 ? 1024 : 512)>();
     if (e == cudaSuccess) e = set_cell_attr<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>();
     if (e == cudaSuccess) e = set_cell_attr<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>();
-    if (e == cudaSuccess) e = set_cell_attr<TR, 512, 16>();
+    if (e == cudaSuccess) e = set_cell_attr<TR, CellCfg<TR>::NT2, CellCfg<TR>::E2>();
     return e;
 }
 
@@ -630,7 +634,7 @@ static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStrea
         CK(cudaMemcpyAsync(g_ws.ctr + CTR_BASE0 + 3, g_ws.h_ctr + CTR_BASE0 + 3, 4, cudaMemcpyHostToDevice, st));
         int rc = run_cell_class<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>(data, counts[0], d_queues, st);
         if (!rc) rc = run_cell_class<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>(data, counts[1], d_queues + QCAP, st);
-        if (!rc) rc = run_cell_class<TR, 512, 16>(data, counts[2], d_queues + 2 * QCAP, st);
+        if (!rc) rc = run_cell_class<TR, CellCfg<TR>::NT2, CellCfg<TR>::E2>(data, counts[2], d_queues + 2 * QCAP, st);
         if (rc) return rc;
 #ifdef IPS4O_BASE_PROF
         {
