@@ -14,6 +14,9 @@ constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer (SURVEY 
 // Each bucket's permutation control pair: the packed (w, r) word, then its reader count.
 // (Spreading the pairs over 256-byte lines -- one L2 slice each -- measured no faster.)
 constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
+#ifndef IPS4O_CELL_C1MAX  // largest leaf of the middle base-case class (8-byte types)
+#define IPS4O_CELL_C1MAX 4096
+#endif
 #ifndef IPS4O_K2_LUT  // K2 classifies through the bucket-hint table (1) or the splitter tree only (0)
 #define IPS4O_K2_LUT 1
 #endif
@@ -56,6 +59,7 @@ struct TU64 {
     typedef u64 V;
     static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 0, PARTS = 1;
     static constexpr u32 LEAF = 4096;  // target base-case size of the adaptive k
+    static constexpr u32 C1MAX = IPS4O_CELL_C1MAX;  // largest leaf of base-case class 1
     __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v; }
     __device__ __forceinline__ static bool less(V a, V b) { return a < b; }
     __host__ __device__ __forceinline__ static V pad() { return ~0ull; }
@@ -67,6 +71,7 @@ struct TF64 {
     typedef u64 V;
     static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 1, PARTS = 1;
     static constexpr u32 LEAF = 4096;
+    static constexpr u32 C1MAX = IPS4O_CELL_C1MAX;
     __host__ __device__ __forceinline__ static u64 key(V v, u32 = 0) {
         return (v >> 63) ? ~v : (v | 0x8000000000000000ull);
     }
@@ -78,6 +83,7 @@ struct TPair {
     typedef ulonglong2 V;
     static constexpr int S = 16, B = BLOCK_BYTES / 16, VEC = 1, CAP = 8192, TYPE = 2, PARTS = 1;
     static constexpr u32 LEAF = 4096;
+    static constexpr u32 C1MAX = 4096;
     __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v.x; }
     __device__ __forceinline__ static bool less(V a, V b) {
         return a.x < b.x || (a.x == b.x && a.y < b.y);
@@ -96,6 +102,7 @@ struct TRec {
     typedef Rec100 V;
     static constexpr int S = 100, B = 4, VEC = 0, CAP = 1024, TYPE = 3, PARTS = 2;
     static constexpr u32 LEAF = 512;
+    static constexpr u32 C1MAX = 4096;
     __device__ __forceinline__ static u64 hi_of(u32 w0, u32 w1) {
         return ((u64)__byte_perm(w0, 0, 0x0123) << 32) | (u64)__byte_perm(w1, 0, 0x0123);
     }
@@ -151,8 +158,8 @@ enum {
 };
 constexpr int NUM_BASE_CLASSES = 4;
 // base-case size classes: <= 2048, <= 4096, <= 8192, <= 16384 elements
-__host__ __device__ __forceinline__ u32 base_class(u64 n) {
-    return n <= 2048 ? 0u : n <= 4096 ? 1u : n <= 8192 ? 2u : 3u;
+__host__ __device__ __forceinline__ u32 base_class(u64 n, u32 c1max = 4096) {
+    return n <= 2048 ? 0u : n <= c1max ? 1u : n <= 8192 ? 2u : 3u;
 }
 enum { ERR_SPILL = 1, ERR_CONSERVE = 2, ERR_QUEUE = 4, ERR_CAPACITY = 8, ERR_PROGRESS = 16 };
 

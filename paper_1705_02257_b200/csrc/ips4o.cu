@@ -284,7 +284,7 @@ static cudaError_t set_base_attr1() {
 template <class TR> struct CellCfg {
     static constexpr bool small = IPS4O_CELL_SMALL && TR::S == 8;
     static constexpr int NT0 = small ? 128 : 256, E0 = small ? 16 : 8;
-    static constexpr int NT1 = small ? 256 : 512, E1 = small ? 16 : 8;
+    static constexpr int NT1 = small ? (int)TR::C1MAX / 16 : 512, E1 = small ? 16 : 8;
     static constexpr int NT2 = IPS4O_CELL_BIG_NT, E2 = 8192 / IPS4O_CELL_BIG_NT;  // leaves of <= 8192
 };
 template <class TR, int NT, int E>
@@ -672,7 +672,7 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
     g_stats.aux_bytes = fixed_bytes() + align_up(spill_bound_elems(n, TR::S) * TR::S, 256);
     if (n <= (u64)TR::CAP) {
         g_stats.base_elements += n;
-        const u32 c = base_class(n);
+        const u32 c = base_class(n, TR::C1MAX);
         g_ws.h_q[0] = TaskDesc{0, n, 0u, 0u};
         CK(cudaMemcpyAsync(g_ws.q_base + (size_t)c * QCAP, g_ws.h_q, sizeof(TaskDesc),
                            cudaMemcpyHostToDevice, st));

@@ -270,7 +270,8 @@ __device__ unsigned long long g_base_prof[2][8];
 #endif
 template <class TR, int NT, int E>
 struct CellBase {
-    static constexpr u32 TILE = NT * E;                  // a power of two
+    static constexpr u32 TILE = NT * E;
+    static constexpr u32 LOG_CELLS = TILE >= 8192 ? 13 : TILE >= 4096 ? 12 : TILE >= 2048 ? 11 : TILE >= 1024 ? 10 : 9;
     static constexpr size_t x_bytes = (size_t)TILE * sizeof(typename TR::V) + 16;  // + alignment shift
     static constexpr size_t cnt_bytes = (size_t)((E + 4) * NT + 8) * 4;
     static constexpr size_t smem = x_bytes + cnt_bytes;
@@ -280,7 +281,7 @@ __device__ __forceinline__ u32 cpad(u32 c) { return c + 4u * (c / E); }
 constexpr u32 CELL_FIX_BUDGET = 4096;  // insertion-sort moves per leaf and thread before falling back
 
 template <class TR, int NT, int E>
-__global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(typename TR::V) * NT * E <= 65536 ? 2 : 1)))
+__global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320 ? 3 : (sizeof(typename TR::V) * NT * E <= 65536 ? 2 : 1)))
     k_base_cell(const TaskDesc* tasks, u32 ntasks, void* vdata, TaskDesc* fb_queue, u32* fb_count, u32 fb_cap) {
     typedef typename TR::V V;
     typedef CellBase<TR, NT, E> CB;
@@ -307,7 +308,9 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : (sizeof(t
         // memory, so that its aligned body leaves by one TMA bulk store
         const u32 p = sizeof(V) == 8 ? (u32)((reinterpret_cast<uintptr_t>(g) >> 3) & 1u) : 0u;
         V* const X = X0 + p;
-        const u32 cb = n > 1 ? 32u - (u32)__clz(n - 1) : 1u;  // 2^cb >= n cells
+        // 2^cb >= n cells, at most the largest power of two <= the tile (a leaf above it,
+        // in a tile that is not a power of two, has up to 1.25 elements per cell)
+        const u32 cb = min(n > 1 ? 32u - (u32)__clz(n - 1) : 1u, CB::LOG_CELLS);
         const u32 ncell = 1u << cb;
         __syncthreads();  // the previous leaf is finished
         BASE_PROF_MARK(0);
