@@ -201,9 +201,27 @@ def cpu_baseline(dist: str, log2: int, secs_target: float = 15.0):
     oracle.sort_inplace(b)
     t = time.perf_counter() - t0
     reps = 1
+    # context: the library sort of the same sample on one core (numpy's sort, standing in
+    # for std::sort), and the host the numbers come from
+    c = a.copy()
+    t1 = time.perf_counter()
+    if et == W.ELEM_REC100:
+        np.sort(np.ascontiguousarray(c).view("S100").ravel())
+    elif et == W.ELEM_PAIR:
+        np.sort(c.view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k"])
+    else:
+        c.sort()
+    t_lib = time.perf_counter() - t1
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), "")
+    except OSError:
+        pass
     return {"value": n / t / 1e9, "unit": "Gelem/s", "cores": 1, "kind": "oracle",
             "sample": f"{dist} n=2^{log2} (seed 1), {reps} run, {t:.1f} s; oracle/ sequential IS4o "
-                      f"(PAPER.md:419), 1 thread"}
+                      f"(PAPER.md:419), 1 thread",
+            "library_sort_1core_gelems": n / t_lib / 1e9, "nproc": os.cpu_count(), "cpu_model": model}
 
 
 # ------------------------------------------------------------------ our arm
@@ -333,6 +351,9 @@ def run_ours(args):
         "sort_stats": stats,
         "clocks": clk.summary(),
         "ms_per_step_min": min(step_ms), "ms_per_step_median": statistics.median(step_ms),
+        "sorted_gbs": n * esize / per_gpu_s / 1e9,
+        "step_roofline_with_base": {"bytes": (4 * L + 2) * n * esize,
+                                    "frac_at_8TBs": (4 * L + 2) * n * esize / 8.0e12 / per_gpu_s},
     }
     if e2e:
         line["e2e"] = e2e
@@ -378,7 +399,7 @@ def verify(work, et, pristine) -> bool:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=15)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="H", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
