@@ -515,9 +515,9 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
         u64 maxn = 0;
         for (u32 i = 0; i < T; ++i) maxn = std::max<u64>(maxn, g_ws.h_tp[i].hi - g_ws.h_tp[i].lo);
         if (maxn >= K1_BIG_TASK)
-            LAUNCH(KK_SAMPLE, (k_sample<TR, K1_SAMPLE_BIG><<<T, K1_THREADS, padidx(K1_SAMPLE_BIG) * 8 + 16, st>>>(A)));
+            LAUNCH(KK_SAMPLE, (k_sample<TR, K1_SAMPLE_BIG><<<T, K1Cfg<K1_SAMPLE_BIG>::THREADS, padidx(K1_SAMPLE_BIG) * 8 + 16, st>>>(A)));
         else
-            LAUNCH(KK_SAMPLE, (k_sample<TR, K1_SAMPLE><<<T, K1_THREADS, padidx(K1_SAMPLE) * 8 + 16, st>>>(A)));
+            LAUNCH(KK_SAMPLE, (k_sample<TR, K1_SAMPLE><<<T, K1Cfg<K1_SAMPLE>::THREADS, padidx(K1_SAMPLE) * 8 + 16, st>>>(A)));
     }
     const u32 g2 = std::min<u32>(S, g_ws.k2_blocks);
     if constexpr (TR::S == 100) {

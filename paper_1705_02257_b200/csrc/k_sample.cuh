@@ -12,7 +12,8 @@
 
 namespace ips4o {
 
-constexpr int K1_THREADS = 1024;
+// threads of a K1 CTA: 16 sample keys per thread (register network of 16 + merge passes)
+template <int SAMPLE> struct K1Cfg { static constexpr int THREADS = SAMPLE / 16; };
 constexpr int K1_SAMPLE = 4096;        // sample capacity for ordinary tasks (32 KB smem)
 constexpr int K1_SAMPLE_BIG = 8192;    // for tasks of >= 2^22 elements (dynamic smem, 64 KB)
 constexpr u64 K1_BIG_TASK = 1ull << 22;
@@ -21,48 +22,61 @@ constexpr u64 K1_BIG_TASK = 1ull << 22;
 // splitters held in s_dist[0..nd).  k' = next power of two >= nd+1; padding repeats the
 // largest splitter.  Writes the task's classifier fields.
 // Bucket-hint table (common.cuh, LUT_N): for every cell, A = #{padded splitters <= the
-// cell's first key} and d = #{padded splitters inside the cell}, by binary search over the
-// padded splitters s_i = s_dist[min(i, nd) - 1], i in [1, kp-1].
-__device__ void build_lut_block(const u64* s_dist, u32 nd, u32 kp, unsigned short* g_lut, TaskParam* tp) {
+// cell's first key} and d = #{padded splitters inside the cell, above its first key}, for
+// the padded splitters s_i = s_dist[min(i, nd) - 1], i in [1, kp-1].  Every splitter is
+// counted in its cell (two 16-bit counters: equal to the cell's first key / above it), and
+// A is the exclusive prefix over the cells plus the cell's "equal" count.  scr: LUT_N words
+// of shared memory.  Block-wide; LUT_N must be a multiple of blockDim.x.
+__device__ void build_lut_block(const u64* s_dist, u32 nd, u32 kp, unsigned short* g_lut, TaskParam* tp,
+                                u32* scr) {
+    __shared__ u32 s_ws[32];
     auto S = [&](u32 i) { return s_dist[(i <= nd ? i : nd) - 1]; };
-    auto C = [&](u64 v) {  // #{i in [1, kp-1] : s_i <= v}
-        u32 lo = 0, hi = kp - 1;
-        while (lo < hi) {
-            const u32 mid = (lo + hi + 1) >> 1;
-            if (S(mid) <= v) lo = mid;
-            else hi = mid - 1;
-        }
-        return lo;
-    };
     const u64 lo = S(1), span = S(kp - 1) - lo;
     u32 sh = 0;
     if (span) {
         const u32 bl = 64u - (u32)__clzll((long long)span);
         sh = bl > LUT_LOG ? bl - LUT_LOG : 0u;  // span >> sh < LUT_N
     }
-    for (u32 c = threadIdx.x; c < LUT_STRIDE; c += blockDim.x) {
-        u32 e = 0;  // entry LUT_N (keys below s_1) and the padding: A = d = 0
-        if (c < LUT_N) {
-            const u64 off0 = (u64)c << sh;
-            const u64 c0 = off0 > ~0ull - lo ? ~0ull : lo + off0;
-            u64 c1 = ~0ull;  // the last cell extends to the largest key
-            if (c + 1 < LUT_N) {
-                const u64 off1 = ((u64)(c + 1) << sh) - 1;
-                c1 = off1 > ~0ull - lo ? ~0ull : lo + off1;
-            }
-            const u32 A = C(c0), d = C(c1) - A;
-            e = A | d << 8;
-        }
-        g_lut[c] = (unsigned short)e;
+    const u32 tid = threadIdx.x, nt = blockDim.x, per = LUT_N / nt, lane = tid & 31, w = tid >> 5;
+    for (u32 c = tid; c < LUT_N; c += nt) scr[c] = 0u;
+    __syncthreads();
+    for (u32 i = 1 + tid; i < kp; i += nt) {
+        const u64 sv = S(i);
+        const u64 y = (sv - lo) >> sh;
+        const u32 c = y >= LUT_N ? LUT_N - 1u : (u32)y;
+        atomicAdd(&scr[c], sv == lo + ((u64)c << sh) ? 0x10000u : 1u);
     }
-    if (threadIdx.x == 0) {
+    __syncthreads();
+    u32 sum = 0;
+    for (u32 k = 0; k < per; ++k) {
+        const u32 x = scr[tid * per + k];
+        sum += (x & 0xFFFFu) + (x >> 16);
+    }
+    u32 incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (u32)o) incl += y;
+    }
+    if (lane == 31) s_ws[w] = incl;
+    __syncthreads();
+    u32 run = incl - sum;
+    for (u32 ww = 0; ww < w; ++ww) run += s_ws[ww];
+    for (u32 k = 0; k < per; ++k) {
+        const u32 c = tid * per + k, x = scr[c];
+        const u32 eqc = x >> 16, gtc = x & 0xFFFFu;
+        g_lut[c] = (unsigned short)((run + eqc) | gtc << 8);
+        run += eqc + gtc;
+    }
+    for (u32 c = LUT_N + tid; c < LUT_STRIDE; c += nt) g_lut[c] = 0;  // keys below s_1; padding
+    if (tid == 0) {
         tp->lut_lo = lo;
         tp->lut_sh = sh;
     }
 }
 
 __device__ void build_tree_block(const u64* s_dist, u32 nd, u32 eq, u64* g_tree, u64* g_spl,
-                                 TaskParam* tp, u32* btot, unsigned short* g_lut) {
+                                 TaskParam* tp, u32* btot, unsigned short* g_lut, u32* scr) {
     u32 kp = 2;
     while (kp < nd + 1) kp <<= 1;
     u32 logk = 0;
@@ -89,7 +103,7 @@ __device__ void build_tree_block(const u64* s_dist, u32 nd, u32 eq, u64* g_tree,
         tp->eq = eq;
         tp->K = eq ? 2 * kp - 1 : kp;
     }
-    build_lut_block(s_dist, nd, kp, g_lut, tp);
+    build_lut_block(s_dist, nd, kp, g_lut, tp, scr);
 }
 
 // the sample's keys as a base-case element type (order-preserving u64 images)
@@ -100,7 +114,8 @@ struct TKey {
 };
 
 template <class TR, int SAMPLE>
-__global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
+__global__ void __launch_bounds__(K1Cfg<SAMPLE>::THREADS) k_sample(LevelArgs A) {
+    constexpr int K1_THREADS = K1Cfg<SAMPLE>::THREADS;
     typedef typename TR::V V;
     extern __shared__ __align__(16) unsigned char smem1[];
     u64* keys = reinterpret_cast<u64*>(smem1);
@@ -178,16 +193,17 @@ __global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A) {
     }
     __syncthreads();
     build_tree_block(dist, s_nd, eq, A.tree + (u64)t * MAXK, A.spl + (u64)t * MAXK, tp, A.btot + (u64)t * MAXK,
-                     A.lut + (u64)t * LUT_STRIDE);
+                     A.lut + (u64)t * LUT_STRIDE, reinterpret_cast<u32*>(keys));  // (the sample is done)
     if (threadIdx.x == 0 && eq) atomicAdd(&A.ctr[CTR_EQ], 1u);
 }
 
 // Debug path: classifier from splitters given by the caller (already key-transformed).
 __global__ void k_tree_from_splitters(LevelArgs A, const u64* splitters, u32 nspl, u32 eq) {
     __shared__ u64 dist[MAXK];
+    __shared__ u32 scr[LUT_N];
     for (u32 i = threadIdx.x; i < nspl; i += blockDim.x) dist[i] = splitters[i];
     __syncthreads();
-    build_tree_block(dist, nspl, eq, A.tree, A.spl, const_cast<TaskParam*>(A.tp), A.btot, A.lut);
+    build_tree_block(dist, nspl, eq, A.tree, A.spl, const_cast<TaskParam*>(A.tp), A.btot, A.lut, scr);
 }
 
 }  // namespace ips4o
