@@ -352,7 +352,8 @@ static int prepare_kernels(void) {
                                 (int)K2RecSmem<K2REC_THREADS>::total));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_classify_rec<K2REC_THREADS>, K2REC_THREADS,
                                                          K2RecSmem<K2REC_THREADS>::total));
-        CK(cudaFuncSetAttribute(k_base_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase::smem));
+        CK(cudaFuncSetAttribute(k_base_rec<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase<2>::smem));
+        CK(cudaFuncSetAttribute(k_base_rec<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase<4>::smem));
         CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(padidx(K1_SAMPLE_BIG) * 8 + 16)));
         CK(cudaFuncSetAttribute(k_sample<TR, K1_SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -617,14 +618,20 @@ static int run_cell_class(void* data, u32 count, TaskDesc* d_tasks, cudaStream_t
 template <class TR>
 static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStream_t st) {
     if constexpr (TR::S == 100) {
-        if (counts[1] || counts[2] || counts[3]) {
+        if (counts[2] || counts[3]) {
             snprintf(g_errbuf, sizeof g_errbuf, "record base task above capacity");
             return IPS4O_EINTERNAL;
         }
-        if (!counts[0]) return IPS4O_OK;
-        const u32 grid = std::min<u32>(counts[0], 4u * g_ws.num_sms);
-        LAUNCH(KK_BASE, (k_base_rec<<<grid, KREC_THREADS, RecBase::smem, st>>>(d_queues, counts[0], data)));
-        g_stats.base_tasks += counts[0];
+        if (counts[0]) {
+            const u32 grid = std::min<u32>(counts[0], 4u * g_ws.num_sms);
+            LAUNCH(KK_BASE, (k_base_rec<2><<<grid, KREC_THREADS, RecBase<2>::smem, st>>>(d_queues, counts[0], data)));
+        }
+        if (counts[1]) {
+            const u32 grid = std::min<u32>(counts[1], 4u * g_ws.num_sms);
+            LAUNCH(KK_BASE, (k_base_rec<4><<<grid, KREC_THREADS, RecBase<4>::smem, st>>>(d_queues + QCAP, counts[1],
+                                                                                         data)));
+        }
+        g_stats.base_tasks += counts[0] + counts[1];
         return IPS4O_OK;
     } else {
         if (!(counts[0] | counts[1] | counts[2] | counts[3])) return IPS4O_OK;
@@ -672,7 +679,7 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
     g_stats.aux_bytes = fixed_bytes() + align_up(spill_bound_elems(n, TR::S) * TR::S, 256);
     if (n <= (u64)TR::CAP) {
         g_stats.base_elements += n;
-        const u32 c = base_class(n, TR::C1MAX);
+        const u32 c = base_class(n, TR::C0MAX, TR::C1MAX);
         g_ws.h_q[0] = TaskDesc{0, n, 0u, 0u};
         CK(cudaMemcpyAsync(g_ws.q_base + (size_t)c * QCAP, g_ws.h_q, sizeof(TaskDesc),
                            cudaMemcpyHostToDevice, st));

@@ -137,10 +137,13 @@ struct TRecItem {
     __device__ __forceinline__ static bool less(V a, V b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
     __host__ __device__ __forceinline__ static V pad() { return make_ulonglong2(~0ull, ~0ull); }
 };
-constexpr int KREC_THREADS = 256, KREC_ITEMS = 4;  // CAP = 1024 records
+// Two size classes: leaves of <= 512 records (2 items per thread, ~110 KB of shared memory:
+// two CTAs per SM) and of <= 1024 (4 items, one CTA per SM).
+constexpr int KREC_THREADS = 256;
+template <int ITEMS>
 struct RecBase {
-    static constexpr size_t items_bytes = (size_t)padidx(KREC_THREADS * KREC_ITEMS) * 16 + 16;
-    static constexpr u32 rec_words = KREC_THREADS * KREC_ITEMS * 25 + 8;  // + alignment slack
+    static constexpr size_t items_bytes = (size_t)padidx(KREC_THREADS * ITEMS) * 16 + 16;
+    static constexpr u32 rec_words = KREC_THREADS * ITEMS * 25 + 8;  // + alignment slack
     static constexpr size_t smem = items_bytes + (size_t)2 * rec_words * 4;  // two leaves
 };
 
@@ -158,7 +161,9 @@ __device__ __forceinline__ u32 rec_fetch(const TaskDesc& td, const u32* gw, u32*
     return (u32)((p0 - w0) / 4);
 }
 
+template <int KREC_ITEMS>
 __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks, u32 ntasks, void* vdata) {
+    typedef RecBase<KREC_ITEMS> RecBase;
     extern __shared__ __align__(16) unsigned char smem5[];
     ulonglong2* it = reinterpret_cast<ulonglong2*>(smem5);
     u32* const sbuf = reinterpret_cast<u32*>(smem5 + RecBase::items_bytes);
