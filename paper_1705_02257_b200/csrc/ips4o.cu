@@ -298,6 +298,9 @@ static cudaError_t set_base_attrs() {
     if (e == cudaSuccess) e = set_cell_attr<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>();
     if (e == cudaSuccess) e = set_cell_attr<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>();
     if (e == cudaSuccess) e = set_cell_attr<TR, CellCfg<TR>::NT2, CellCfg<TR>::E2>();
+    if constexpr (TR::CAP >= 16384) {
+        if (e == cudaSuccess) e = set_cell_attr<TR, 1024, 16>();
+    }
     return e;
 }
 
@@ -660,12 +663,21 @@ static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStrea
             }
         }
 #endif
+        // class 3 (8193..16384 elements, 8-byte types) by the cell kernel with 1024 threads;
+        // the merge sort then takes only the leaves the cell kernels handed back (appended
+        // to the class-3 queue after the level's own class-3 tasks)
+        u32 mstart = 0;
+        if constexpr (TR::CAP >= 16384) {
+            rc = run_cell_class<TR, 1024, 16>(data, counts[3], d_queues + 3 * QCAP, st);
+            if (rc) return rc;
+            mstart = counts[3];
+        }
         constexpr int TH = TR::CAP >= 16384 ? 1024 : 512;
         typedef BaseClass<TR, TH, 16> BC;
-        const u32 grid = std::max<u32>(1u, std::min<u32>(counts[3] + 64u, 2u * g_ws.num_sms));
-        LAUNCH(KK_BASE, (k_base_merge<TR, TH, 16><<<grid, TH, BC::smem, st>>>(d_queues + 3 * QCAP,
+        const u32 grid = 2u * g_ws.num_sms;
+        LAUNCH(KK_BASE, (k_base_merge<TR, TH, 16><<<grid, TH, BC::smem, st>>>(d_queues + 3 * QCAP, mstart,
                                                                               g_ws.ctr + CTR_BASE0 + 3, data)));
-        g_stats.base_tasks += counts[3];
+        if (TR::CAP < 16384) g_stats.base_tasks += counts[3];
         return IPS4O_OK;
     }
 }

@@ -109,14 +109,15 @@ __device__ __forceinline__ void block_sort_smem(typename TR::V* s, u32 n) {
 }
 
 template <class TR, int THREADS, int ITEMS>
-__global__ void __launch_bounds__(THREADS) k_base_merge(const TaskDesc* tasks, const u32* d_ntasks, void* vdata) {
-    const u32 ntasks = *d_ntasks;
+__global__ void __launch_bounds__(THREADS) k_base_merge(const TaskDesc* tasks, u32 start, const u32* d_ntasks,
+                                                         void* vdata) {
+    const u32 ntasks = *d_ntasks;  // tasks [start, ntasks) (the count lives on the device)
     typedef typename TR::V V;
     extern __shared__ __align__(16) unsigned char smem5[];
     V* s = reinterpret_cast<V*>(smem5);
     V* data = reinterpret_cast<V*>(vdata);
     const u32 tid = threadIdx.x;
-    for (u32 ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
+    for (u32 ti = start + blockIdx.x; ti < ntasks; ti += gridDim.x) {
         const TaskDesc td = tasks[ti];
         const u32 n = (u32)(td.hi - td.lo);
         const u32 n16 = (n + ITEMS - 1) / ITEMS * ITEMS;
