@@ -74,7 +74,10 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
         }
         __syncthreads();
         const u32 sidx = s_stripe;
-        if (sidx == 0xFFFFFFFFu) return;
+        if (sidx == 0xFFFFFFFFu) {
+            bulk_wait0();  // the block stores are complete before the CTA exits
+            return;
+        }
         const StripeDesc sd = A.sd[sidx];
         const TaskParam tp = A.tp[sd.task];
         for (u32 b = tid; b < (u32)MAXK; b += NT) {
@@ -180,15 +183,17 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
                     defer |= 1u << r;
                 }
             }
+            fence_proxy_async_smem();  // the buffers' generic writes before the TMA reads them
             __syncthreads();
-            // flush complete buffer blocks: warp w handles buckets w, w+NW, ...
-            for (u32 bb = w; bb < (u32)MAXK; bb += NW) {
+            // flush complete buffer blocks by TMA bulk stores (400-byte blocks: 16-byte aligned
+            // in the block grid and in shared memory); read before the deferred records land
+            for (u32 bb = tid; bb < (u32)MAXK; bb += NT) {
                 if (nfl[bb]) {
-                    u32* dst = gw + (mb + (u64)slotb[bb] * B) * RW;
-                    const u32* sb = buf + bb * B * RW;
-                    for (u32 i = lane; i < B * RW; i += 32) dst[i] = sb[i];
+                    bulk_s2g(gw + (mb + (u64)slotb[bb] * B) * RW, buf + bb * B * RW, B * RW * 4);
+                    bulk_commit();
                 }
             }
+            if (tid < (u32)MAXK) bulk_wait_read0();
             __syncthreads();
 #pragma unroll
             for (int r = 0; r < RS; ++r)
