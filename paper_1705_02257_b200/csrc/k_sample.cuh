@@ -16,7 +16,10 @@ namespace ips4o {
 template <int SAMPLE> struct K1Cfg { static constexpr int THREADS = SAMPLE / 16; };
 constexpr int K1_SAMPLE = 4096;        // sample capacity for ordinary tasks (32 KB smem)
 constexpr int K1_SAMPLE_BIG = 8192;    // for tasks of >= 2^22 elements (dynamic smem, 64 KB)
-constexpr u64 K1_BIG_TASK = 1ull << 22;
+#ifndef IPS4O_K1_BIG_LOG
+#define IPS4O_K1_BIG_LOG 22
+#endif
+constexpr u64 K1_BIG_TASK = 1ull << IPS4O_K1_BIG_LOG;
 
 // Builds the padded splitter array spl[1..k'-1] and the BFS tree from nd distinct sorted
 // splitters held in s_dist[0..nd).  k' = next power of two >= nd+1; padding repeats the
