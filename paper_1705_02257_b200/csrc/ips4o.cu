@@ -24,6 +24,7 @@ constexpr u32 MAXT = 512;          // tasks per level batch
 constexpr u32 MAXS = 512;          // stripes per level batch
 static_assert(MAXS <= (u32)K4_MAXSTRIPES && MAXS <= (u32)K2P_MAXST, "per-task stripe tables in shared memory");
 constexpr u32 QCAP = MAXT * MAXK;  // queue capacity (tasks)
+constexpr u32 Q_SPEC = 512;        // next-level tasks copied back with a level's counters
 constexpr u64 MIN_STRIPE = 65536;  // elements
 
 static std::mutex g_mu;
@@ -587,6 +588,9 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
         LAUNCH(KK_CLEANUP, (k_cleanup_cta<TR><<<T * MAXK, K4_THREADS, 0, st>>>(A)));
     }
     CK(cudaMemcpyAsync(g_ws.h_ctr, g_ws.ctr, CTR_N * 4 + 16, cudaMemcpyDeviceToHost, st));
+    // the first next-level tasks come back with the counters (one sync fewer when a level
+    // emits at most Q_SPEC of them, e.g. the 256 of the top level)
+    if (emit) CK(cudaMemcpyAsync(g_ws.h_q, g_ws.q_next, Q_SPEC * sizeof(TaskDesc), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     g_stats.host_syncs++;
     if (g_ws.h_ctr[CTR_ERROR]) {
@@ -735,11 +739,11 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
             const u32 nn = g_ws.h_ctr[CTR_NEXT];
             rc = run_base<TR>(data, g_ws.h_ctr + CTR_BASE0, g_ws.q_base, st);
             if (rc) return rc;
-            if (nn) {
+            if (nn > Q_SPEC) {
                 CK(cudaMemcpyAsync(g_ws.h_q, g_ws.q_next, nn * sizeof(TaskDesc), cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
-                next.insert(next.end(), g_ws.h_q, g_ws.h_q + nn);
             }
+            if (nn) next.insert(next.end(), g_ws.h_q, g_ws.h_q + nn);
             i0 = i1;
         }
         cur.swap(next);
