@@ -17,6 +17,7 @@
 // Subproblems are binned by size class (2K/4K/8K/16K elements) by the cleanup kernel so
 // that each launch uses a CTA sized to its tasks.
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 
 namespace ips4o {
@@ -286,11 +287,25 @@ template <int E>
 __device__ __forceinline__ u32 cpad(u32 c) { return c + 4u * (c / E); }
 constexpr u32 CELL_FIX_BUDGET = 4096;  // insertion-sort moves per leaf and thread before falling back
 
+// The cell kernel works on order-preserving u64 images of f64 keys (mapped on load, mapped
+// back in shared memory before the write-back): every comparison is then a plain u64 one.
+template <class TR> struct CellWork {
+    typedef TR T;
+    __device__ __forceinline__ static typename TR::V in(typename TR::V v) { return v; }
+    __device__ __forceinline__ static typename TR::V out(typename TR::V v) { return v; }
+};
+template <> struct CellWork<TF64> {
+    typedef TU64 T;
+    __device__ __forceinline__ static u64 in(u64 v) { return TF64::key(v); }
+    __device__ __forceinline__ static u64 out(u64 k) { return (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k; }
+};
+
 template <class TR, int NT, int E>
 __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320 ? 3 : (sizeof(typename TR::V) * NT * E <= 65536 ? 2 : 1)))
     k_base_cell(const TaskDesc* tasks, u32 ntasks, void* vdata, TaskDesc* fb_queue, u32* fb_count, u32 fb_cap) {
     typedef typename TR::V V;
     typedef CellBase<TR, NT, E> CB;
+    typedef typename CellWork<TR>::T TW;
     constexpr int NW = NT / 32;
     static_assert(E % 4 == 0, "cell runs are read as 128-bit vectors");
     extern __shared__ __align__(16) unsigned char smc[];
@@ -334,8 +349,8 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320
         for (int j = 0; j < E; ++j) {
             const u32 idx = j * NT + tid;
             if (idx < n) {
-                v[j] = g[idx];
-                const u64 k = TR::key(v[j]);
+                v[j] = CellWork<TR>::in(g[idx]);
+                const u64 k = TW::key(v[j]);
                 kmin = k < kmin ? k : kmin;
                 kmax = k > kmax ? k : kmax;
             }
@@ -373,7 +388,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320
         for (int j = 0; j < E; ++j) {
             const u32 idx = j * NT + tid;
             if (idx < n) {
-                const u64 x = TR::key(v[j]) - kmin;
+                const u64 x = TW::key(v[j]) - kmin;
                 const u32 c = mul ? (u32)__umul64hi(x, mul) : (u32)x;
                 cr[j] = c | (atomicAdd(&cnt[cpad<E>(c)], 1u) << 16);
             }
@@ -464,7 +479,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320
                 m2 &= m2 - 1u;
                 const u32 b = cnt[cpad<E>(tid * E + k)];
                 const V x0 = X[b], x1 = X[b + 1];
-                if (TR::less(x1, x0)) {
+                if (TW::less(x1, x0)) {
                     X[b] = x1;
                     X[b + 1] = x0;
                 }
@@ -474,11 +489,11 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320
                 m34 &= m34 - 1u;
                 const u32 b = cnt[cpad<E>(tid * E + k)];
                 const u32 e = k + 1 < (u32)E ? cnt[cpad<E>(tid * E + k + 1)] : enext;
-                const V pd = TR::pad();
+                const V pd = TW::pad();
                 V x0 = X[b], x1 = X[b + 1], x2 = X[b + 2];
                 V x3 = e - b > 3u ? X[b + 3] : pd;
                 auto cas = [](V& lo, V& hi) {
-                    const bool sw = TR::less(hi, lo);
+                    const bool sw = TW::less(hi, lo);
                     const V t = sw ? hi : lo;
                     hi = sw ? lo : hi;
                     lo = t;
@@ -501,13 +516,17 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320
                 for (u32 i = b + 1; i < e; ++i) {
                     const V x = X[i];
                     u32 q = i;
-                    while (q > b && TR::less(x, X[q - 1])) {
+                    while (q > b && TW::less(x, X[q - 1])) {
                         X[q] = X[q - 1];
                         --q;
                     }
                     X[q] = x;
                 }
             }
+        }
+        if constexpr (!std::is_same<TW, TR>::value) {
+            __syncthreads();
+            for (u32 i = tid; i < n; i += NT) X[i] = CellWork<TR>::out(X[i]);
         }
 #if IPS4O_BASE_TMA_WB
         fence_proxy_async_smem();
