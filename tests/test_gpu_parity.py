@@ -207,8 +207,11 @@ def test_partition_once_duplicates_and_skew():
 
 # ------------------------------------------------------------ (iv) whole sorts
 
-SIZES = [0, 1, 2, 3, 17, 1000, 16383, 16384, 16385, 40_000, 131_073, 1_000_003, 3_000_017]
-SIZES_REC = [0, 1, 2, 3, 17, 1023, 1024, 1025, 5000, 70_001, 300_007]
+# (single-task sizes at every base-case class boundary: 2048/4096/8192/16384 elements,
+# 512/1024 records)
+SIZES = [0, 1, 2, 3, 17, 1000, 2048, 2049, 4096, 4097, 8192, 8193, 12_345, 16383, 16384, 16385, 40_000,
+         131_073, 1_000_003, 3_000_017]
+SIZES_REC = [0, 1, 2, 3, 17, 512, 513, 1023, 1024, 1025, 5000, 70_001, 300_007]
 
 
 @pytest.mark.parametrize("et", TYPES)
