@@ -47,6 +47,8 @@ CONFIGS = {
     "C3_almostsorted": ("almostsorted", 27, "C3: 2^27 u64 AlmostSorted"),
     "C3_reversesorted": ("reversesorted", 27, "C3: 2^27 u64 ReverseSorted"),
     "C3_zeros": ("zeros", 27, "C3: 2^27 u64 all-zero"),
+    "F3_sorted": ("sorted", 27, "f3: 2^27 u64 already sorted (PAPER.md:444 Sorted)"),
+    "F3_ones": ("ones", 27, "f3: 2^27 u64 all equal to 1 (PAPER.md:444 Ones)"),
     "C4": ("pair16", 27, "C4: 2^27 Pair16 (u64 key uniform [0,2^32), payload = index)"),
     "C5": ("rec100", 24, "C5: 2^24 100-byte records (10-byte key)"),
 }

@@ -320,7 +320,7 @@ def test_type_switching_and_reuse():
 
 FULL = [("uniform", 28), ("f64_uniform", 28), ("f64_exponential", 28), ("rootdup", 27),
         ("twodup", 27), ("eightdup", 27), ("almostsorted", 27), ("reversesorted", 27),
-        ("zeros", 27), ("pair16", 27), ("rec100", 24)]
+        ("zeros", 27), ("sorted", 27), ("ones", 27), ("pair16", 27), ("rec100", 24)]
 
 
 @pytest.mark.parametrize("dist,e", FULL)
