@@ -586,7 +586,39 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A) {
     mbar_fence_init();
     __syncthreads();
     u32 phase = 0;  // parity of this chain's next mbarrier completion
-    u32 t = (u32)((u64)blockIdx.x * T / gridDim.x);
+    // first task: CTAs spread in proportion to the tasks' block counts (the position of
+    // this CTA's share in the concatenation of the tasks' blocks), so that tasks of
+    // different sizes finish together
+    u32 t = 0;
+    if (tid < 32) {
+        u64 total = 0;
+        for (u32 q = lane; q < T; q += 32) total += A.tp[q].nblocks;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+        const u64 target = (u64)blockIdx.x * total / gridDim.x;
+        u64 acc = 0;
+        u32 found = T - 1;
+        for (u32 q0 = 0; q0 < T; q0 += 32) {
+            const u32 q = q0 + lane;
+            const u64 nb = q < T ? A.tp[q].nblocks : 0;
+            u64 incl = nb;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (u32)o) incl += y;
+            }
+            const u32 hit = __ballot_sync(0xffffffffu, q < T && acc + incl > target);
+            if (hit) {
+                found = q0 + __ffs(hit) - 1;
+                break;
+            }
+            acc += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) s_next = found;
+    }
+    __syncthreads();
+    t = s_next;
+    __syncthreads();
     const u32 tnwords = (T + 31) / 32;
 
     for (;;) {
