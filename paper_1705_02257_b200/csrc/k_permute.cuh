@@ -619,14 +619,19 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A) {
     __syncthreads();
     t = s_next;
     __syncthreads();
+    bool first = true;
     const u32 tnwords = (T + 31) / 32;
 
     for (;;) {
         if (tid < 32) {
-            const u32 nt = next_clear_bit(A.tdone, tnwords, t, lane);
+            // (after the first task, helpers start their search at spread positions, so
+            // that they do not all pile onto the task next to the one they finished)
+            const u32 from = first ? t : (u32)((t + 1u + (u64)blockIdx.x * 61u) % T);
+            const u32 nt = next_clear_bit(A.tdone, tnwords, from, lane);
             if (lane == 0) s_next = nt;
         }
         __syncthreads();
+        first = false;
         const u32 nt = s_next;
         if (nt == 0xFFFFFFFFu || nt >= T) break;
         t = nt;
