@@ -19,7 +19,7 @@ VARIANTS = {"bb256": ["-DIPS4O_BLOCK_BYTES=256"],
             "k3t_8x8": ["-DIPS4O_K3T_WARPS=8", "-DIPS4O_K3T_CHAINS=8"],
             "k3t_3x16": ["-DIPS4O_K3T_WARPS=3", "-DIPS4O_K3T_CHAINS=16"],
             "k3t_4x24": ["-DIPS4O_K3T_WARPS=4", "-DIPS4O_K3T_CHAINS=24"],
-            "k2s1": ["-DIPS4O_K2_STAGES=1"], "k2wf": ["-DIPS4O_K2_WFLUSH=1"], "baseprof": ["-DIPS4O_BASE_PROF"], "k2tree": ["-DIPS4O_K2_LUT=0"], "cell1024": ["-DIPS4O_CELL_BIG_NT=1024"], "basewb0": ["-DIPS4O_BASE_TMA_WB=0"]}
+            "k2s1": ["-DIPS4O_K2_STAGES=1"], "k2wf": ["-DIPS4O_K2_WFLUSH=1"], "baseprof": ["-DIPS4O_BASE_PROF"], "k2tree": ["-DIPS4O_K2_LUT=0"], "basess0": ["-DIPS4O_BASE_STREAMS=0"], "cell1024": ["-DIPS4O_CELL_BIG_NT=1024"], "basewb0": ["-DIPS4O_BASE_TMA_WB=0"]}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

@@ -88,6 +88,9 @@ struct Workspace {
     u32* h_order;
     u32* h_ctr;
     TaskDesc* h_q;
+    cudaStream_t side[4];             // base-case size classes run concurrently
+    cudaEvent_t ev_fork, ev_join[4];
+    bool side_ready;
     u64* h_bnd;
     u32* h_tdone;
     u32 k2_blocks = 0, k3_blocks = 0, k3t_blocks = 0;
@@ -610,6 +613,20 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
 // Base case of one level batch: size classes 0..2 (<= 2K / 4K / 8K elements) by the cell
 // kernel, class 3 (<= CAP) and any leaf the cell kernel hands back by the merge sort,
 // which reads its task count from the device (the fallback queue is appended to class 3).
+#ifndef IPS4O_BASE_STREAMS
+#define IPS4O_BASE_STREAMS 1
+#endif
+static cudaError_t side_streams_ready() {
+    if (g_ws.side_ready) return cudaSuccess;
+    for (int c = 0; c < 4; ++c) {
+        cudaError_t e = cudaStreamCreateWithFlags(&g_ws.side[c], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ws.ev_join[c], cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventCreateWithFlags(&g_ws.ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) g_ws.side_ready = true;
+    return e;
+}
 template <class TR, int NT, int E>
 static int run_cell_class(void* data, u32 count, TaskDesc* d_tasks, cudaStream_t st) {
     if (!count) return IPS4O_OK;
@@ -646,9 +663,23 @@ static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStrea
         // the class-3 count lives on the device: the cell kernels append their fallbacks
         memcpy(g_ws.h_ctr + CTR_BASE0 + 3, counts + 3, 4);
         CK(cudaMemcpyAsync(g_ws.ctr + CTR_BASE0 + 3, g_ws.h_ctr + CTR_BASE0 + 3, 4, cudaMemcpyHostToDevice, st));
-        int rc = run_cell_class<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>(data, counts[0], d_queues, st);
-        if (!rc) rc = run_cell_class<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>(data, counts[1], d_queues + QCAP, st);
-        if (!rc) rc = run_cell_class<TR, CellCfg<TR>::NT2, CellCfg<TR>::E2>(data, counts[2], d_queues + 2 * QCAP, st);
+        // the size classes touch disjoint leaves: each runs on its own side stream, so that
+        // one class's tail overlaps the others' work (fork / join through events)
+        // (serialised while the per-launch profiling events are on: they time each kernel
+        // alone)
+        cudaStream_t ss[4] = {st, st, st, st};
+        const bool conc = IPS4O_BASE_STREAMS && !g_prof.on;
+        if (conc) {
+            CK(side_streams_ready());
+            CK(cudaEventRecord(g_ws.ev_fork, st));
+            for (int c = 0; c < 4; ++c) {
+                ss[c] = g_ws.side[c];
+                CK(cudaStreamWaitEvent(ss[c], g_ws.ev_fork, 0));
+            }
+        }
+        int rc = run_cell_class<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>(data, counts[0], d_queues, ss[0]);
+        if (!rc) rc = run_cell_class<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>(data, counts[1], d_queues + QCAP, ss[1]);
+        if (!rc) rc = run_cell_class<TR, CellCfg<TR>::NT2, CellCfg<TR>::E2>(data, counts[2], d_queues + 2 * QCAP, ss[2]);
         if (rc) return rc;
 #ifdef IPS4O_BASE_PROF
         {
@@ -672,9 +703,15 @@ static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStrea
         // to the class-3 queue after the level's own class-3 tasks)
         u32 mstart = 0;
         if constexpr (TR::CAP >= 16384) {
-            rc = run_cell_class<TR, 1024, 16>(data, counts[3], d_queues + 3 * QCAP, st);
+            rc = run_cell_class<TR, 1024, 16>(data, counts[3], d_queues + 3 * QCAP, ss[3]);
             if (rc) return rc;
             mstart = counts[3];
+        }
+        if (conc) {
+            for (int c = 0; c < 4; ++c) {
+                CK(cudaEventRecord(g_ws.ev_join[c], ss[c]));
+                CK(cudaStreamWaitEvent(st, g_ws.ev_join[c], 0));
+            }
         }
         constexpr int TH = TR::CAP >= 16384 ? 1024 : 512;
         typedef BaseClass<TR, TH, 16> BC;
@@ -1012,6 +1049,14 @@ int ips4o_release_workspace(void) {
     g_ws.dev = nullptr;
     g_ws.dev_bytes = 0;
     g_ws.device = -1;
+    if (g_ws.side_ready) {
+        for (int c = 0; c < 4; ++c) {
+            cudaStreamDestroy(g_ws.side[c]);
+            cudaEventDestroy(g_ws.ev_join[c]);
+        }
+        cudaEventDestroy(g_ws.ev_fork);
+        g_ws.side_ready = false;
+    }
     return IPS4O_OK;
 }
 
