@@ -613,6 +613,9 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
 // Base case of one level batch: size classes 0..2 (<= 2K / 4K / 8K elements) by the cell
 // kernel, class 3 (<= CAP) and any leaf the cell kernel hands back by the merge sort,
 // which reads its task count from the device (the fallback queue is appended to class 3).
+#ifndef IPS4O_CELL_OVERSUB  // base-case grid: resident CTAs times this
+#define IPS4O_CELL_OVERSUB 8
+#endif
 #ifndef IPS4O_BASE_STREAMS
 #define IPS4O_BASE_STREAMS 1
 #endif
@@ -631,7 +634,13 @@ template <class TR, int NT, int E>
 static int run_cell_class(void* data, u32 count, TaskDesc* d_tasks, cudaStream_t st) {
     if (!count) return IPS4O_OK;
     typedef CellBase<TR, NT, E> CB;
-    const u32 grid = std::min<u32>(count, (2048u / NT) * 2u * g_ws.num_sms);
+    // resident CTAs x IPS4O_CELL_OVERSUB (persistent loop over the class's leaves)
+    static int occ = 0;
+    if (!occ) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_base_cell<TR, NT, E>, NT, CB::smem));
+        if (occ < 1) occ = 1;
+    }
+    const u32 grid = std::min<u32>(count, (u32)occ * IPS4O_CELL_OVERSUB * g_ws.num_sms);
     LAUNCH(KK_BASE, (k_base_cell<TR, NT, E><<<grid, NT, CB::smem, st>>>(d_tasks, count, data, g_ws.q_base + 3 * QCAP,
                                                                         g_ws.ctr + CTR_BASE0 + 3, QCAP)));
     g_stats.base_tasks += count;
