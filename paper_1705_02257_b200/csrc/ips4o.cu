@@ -20,6 +20,9 @@
 
 namespace ips4o {
 
+#ifndef IPS4O_STRIPES_PER_SM  // stripes per SM of a level (K2 balance vs per-stripe overhead)
+#define IPS4O_STRIPES_PER_SM 3
+#endif
 constexpr u32 MAXT = 512;          // tasks per level batch
 constexpr u32 MAXS = 512;          // stripes per level batch
 static_assert(MAXS <= (u32)K4_MAXSTRIPES && MAXS <= (u32)K2P_MAXST, "per-task stripe tables in shared memory");
@@ -454,7 +457,7 @@ static LevelArgs level_args(void* data, u32 T, u32 S, int emit, u64 seed) {
 // least MIN_STRIPE), a whole number of blocks.
 template <class TR>
 static u64 stripe_len(u64 Ntot) {
-    const u64 target = std::max<u64>(1, std::min<u64>(MAXS, 3ull * g_ws.num_sms));
+    const u64 target = std::max<u64>(1, std::min<u64>(MAXS, (u64)IPS4O_STRIPES_PER_SM * g_ws.num_sms));
     u64 L = std::max<u64>((Ntot + target - 1) / target, MIN_STRIPE);
     return (L + TR::B - 1) / TR::B * TR::B;
 }
