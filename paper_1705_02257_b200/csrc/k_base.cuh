@@ -163,6 +163,122 @@ __device__ __forceinline__ u32 rec_fetch(const TaskDesc& td, const u32* gw, u32*
     return (u32)((p0 - w0) / 4);
 }
 
+// Sort of a record leaf's (key part 0, key part 1 << 32 | index) items: the cell distribution
+// of the 8-byte base case on key part 0 (cells of the key range, shared-memory atomic ranks,
+// block scan, scatter, cells of several items ordered by insertion), or the merge sort when
+// part 0 does not separate the items (all equal, e.g. a part-1 task) or a cell grows large.
+// Items enter in registers (item q of thread t = index q*KREC_THREADS + t) and leave sorted
+// in it[padidx(0..n)].  Block-wide.
+template <int ITEMS>
+__device__ void rec_items_sort(ulonglong2 (&itm)[ITEMS], u32 n, ulonglong2* it, u32* cnt, u64* s_range,
+                               u32* s_flag, u32* s_wsum) {
+    const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    constexpr u32 NT = KREC_THREADS, CAPI = NT * ITEMS;
+    u64 kmin = ~0ull, kmax = 0;
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q)
+        if (q * NT + tid < n) {
+            kmin = min(kmin, itm[q].x);
+            kmax = max(kmax, itm[q].x);
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (tid == 0) {
+        s_range[0] = ~0ull;
+        s_range[1] = 0;
+        *s_flag = 0;
+    }
+    for (u32 c = tid; c < CAPI + 1; c += NT) cnt[c] = 0;
+    __syncthreads();
+    if (lane == 0 && w * 32 < n) {
+        atomicMin(reinterpret_cast<unsigned long long*>(&s_range[0]), kmin);
+        atomicMax(reinterpret_cast<unsigned long long*>(&s_range[1]), kmax);
+    }
+    __syncthreads();
+    kmin = s_range[0];
+    const u64 span = s_range[1] - kmin;
+    const u32 cb = n > 1 ? 32u - (u32)__clz(n - 1) : 1u;
+    const u32 ncell = 1u << cb;  // <= CAPI
+    const bool cells = span != 0 && n >= 64;
+    u32 cr[ITEMS];
+    if (cells) {
+        const u64 mul = span < ncell ? 0ull : (span == ~0ull ? (u64)ncell : (~0ull / (span + 1)) * ncell);
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q)
+            if (q * NT + tid < n) {
+                const u64 x = itm[q].x - kmin;
+                const u32 c = mul ? (u32)__umul64hi(x, mul) : (u32)x;
+                cr[q] = c | atomicAdd(&cnt[c], 1u) << 16;
+            }
+        __syncthreads();
+        // exclusive scan over the ncell counters: thread t owns cells [t*ITEMS, (t+1)*ITEMS)
+        u32 loc[ITEMS], sum = 0;
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q) {
+            loc[q] = cnt[tid * ITEMS + q];
+            sum += loc[q];
+            if (loc[q] > 32u) *s_flag = 1u;  // a large cell: the merge sort is cheaper
+        }
+        u32 incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (u32)o) incl += y;
+        }
+        if (lane == 31) s_wsum[w] = incl;
+        __syncthreads();
+        u32 run = incl - sum;
+        for (u32 ww = 0; ww < w; ++ww) run += s_wsum[ww];
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q) {
+            cnt[tid * ITEMS + q] = run;
+            run += loc[q];
+        }
+        if (tid == NT - 1) cnt[CAPI] = run;  // == n
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q)
+            if (q * NT + tid < n) it[padidx(cnt[cr[q] & 0xFFFFu] + (cr[q] >> 16))] = itm[q];
+        __syncthreads();
+        if (*s_flag == 0u) {
+            // order the cells of this thread's run that hold several items (also when every
+            // cell is one part-0 value: the items still differ in part 1)
+#pragma unroll
+            for (int q = 0; q < ITEMS; ++q) {
+                const u32 b = cnt[tid * ITEMS + q], e = cnt[tid * ITEMS + q + 1];
+                for (u32 i = b + 1; i < e; ++i) {
+                    const ulonglong2 x = it[padidx(i)];
+                    u32 j = i;
+                    while (j > b && TRecItem::less(x, it[padidx(j - 1)])) {
+                        it[padidx(j)] = it[padidx(j - 1)];
+                        --j;
+                    }
+                    it[padidx(j)] = x;
+                }
+            }
+        }
+        __syncthreads();
+        if (*s_flag == 0u) return;
+        // large cells: fall through to the merge sort of the (permuted) items
+        const u32 n16 = (n + ITEMS - 1) / ITEMS * ITEMS;
+        for (u32 i = n + tid; i < n16; i += NT) it[padidx(i)] = TRecItem::pad();
+        __syncthreads();
+        block_sort_smem<TRecItem, NT, ITEMS>(it, n);
+        return;
+    }
+    const u32 n16 = (n + ITEMS - 1) / ITEMS * ITEMS;
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+        const u32 i = q * NT + tid;
+        if (i < n16) it[padidx(i)] = i < n ? itm[q] : TRecItem::pad();
+    }
+    __syncthreads();
+    block_sort_smem<TRecItem, NT, ITEMS>(it, n);
+}
+
 template <int KREC_ITEMS>
 __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks, u32 ntasks, void* vdata) {
     typedef RecBase<KREC_ITEMS> RecBase;
@@ -172,6 +288,9 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
     u32* gw = reinterpret_cast<u32*>(vdata);
     const u32 tid = threadIdx.x;
     __shared__ __align__(8) u64 s_mbar[2];
+    __shared__ u32 s_cnt[KREC_THREADS * KREC_ITEMS + 1];
+    __shared__ u64 s_range[2];
+    __shared__ u32 s_flag, s_wsum[KREC_THREADS / 32];
     if (tid == 0) {
         mbar_init(&s_mbar[0], 1);
         mbar_init(&s_mbar[1], 1);
@@ -205,17 +324,20 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
         mbar_wait(&s_mbar[cur], (phase >> cur) & 1u);
         phase ^= 1u << cur;
         __syncthreads();
-        for (u32 i = tid; i < n16; i += KREC_THREADS) {
-            ulonglong2 x = TRecItem::pad();
-            if (i < n) {
-                const u32* r = srec + i * 25;
-                x.x = TRec::hi_of(r[0], r[1]);
-                x.y = (TRec::lo_of(r[2]) << 32) | i;
+        {
+            ulonglong2 itm[KREC_ITEMS];
+#pragma unroll
+            for (int q = 0; q < KREC_ITEMS; ++q) {
+                const u32 i = q * KREC_THREADS + tid;
+                itm[q] = TRecItem::pad();
+                if (i < n) {
+                    const u32* r = srec + i * 25;
+                    itm[q].x = TRec::hi_of(r[0], r[1]);
+                    itm[q].y = (TRec::lo_of(r[2]) << 32) | i;
+                }
             }
-            it[padidx(i)] = x;
+            rec_items_sort<KREC_ITEMS>(itm, n, it, s_cnt, s_range, &s_flag, s_wsum);
         }
-        __syncthreads();
-        block_sort_smem<TRecItem, KREC_THREADS, KREC_ITEMS>(it, n);
         for (u32 i = tid; i < n * 25; i += KREC_THREADS) {
             const u32 r = i / 25, wd = i - r * 25;
             const u32 src = (u32)(it[padidx(r)].y & 0xFFFFFFFFu);
