@@ -671,7 +671,6 @@ static int run_base(void* data, const u32* counts, TaskDesc* d_queues, cudaStrea
         return IPS4O_OK;
     } else {
         if (!(counts[0] | counts[1] | counts[2] | counts[3])) return IPS4O_OK;
-        if (counts[3] && TR::CAP < 16384 && false) return IPS4O_EINTERNAL;
         // the class-3 count lives on the device: the cell kernels append their fallbacks
         memcpy(g_ws.h_ctr + CTR_BASE0 + 3, counts + 3, 4);
         CK(cudaMemcpyAsync(g_ws.ctr + CTR_BASE0 + 3, g_ws.h_ctr + CTR_BASE0 + 3, 4, cudaMemcpyHostToDevice, st));

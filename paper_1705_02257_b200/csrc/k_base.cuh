@@ -350,7 +350,8 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
 
 // ---------------------------------------------------------------- cell base case
 //
-// Leaves of up to 8192 elements (8/16-byte types) are sorted by one CTA in shared memory.
+// Leaves of up to 16384 (8-byte types) / 8192 (pairs) elements are sorted by one CTA in
+// shared memory.
 // A leaf's keys already lie between two splitters, so one more distribution step needs no
 // splitters: the key range [kmin, kmax] is cut into 2^cb >= n equal cells by the
 // order-preserving map floor((key - kmin) * 2^cb / (kmax - kmin + 1)).  Then, as in the
@@ -362,9 +363,12 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
 //      and written with 128-bit accesses (the counter array has 4 pad words after each
 //      run, which also makes those accesses conflict-free) -- and the scatter of every
 //      element to base[cell] + rank;
-//   4. each thread orders the cells of its run (about one element per cell on average) by
-//      one insertion sort of the run's positions (the cells are already in order);
-//   5. coalesced write-back.
+//   4. each thread orders the cells of its run that hold several elements (about one
+//      element per cell on average): cells of 2 by one compare-exchange, of 3-4 by a
+//      4-element network, larger ones by insertion sort (the cells are already in order);
+//   5. write-back by one TMA bulk store of the leaf's 16-byte aligned body (the leaf is
+//      staged at the same offset modulo 16 as in global memory).
+// f64 leaves are sorted as their order-preserving u64 images (CellWork).
 // When every cell is a single key value (span < cells) step 4 has nothing to do.  A leaf
 // whose cells would need too much insertion work (keys clustered far below the resolution
 // of the cells, e.g. heavy duplicates) is handed to the merge-sort kernel (fallback queue)
