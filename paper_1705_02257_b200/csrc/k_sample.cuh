@@ -12,8 +12,11 @@
 
 namespace ips4o {
 
-// threads of a K1 CTA: 16 sample keys per thread (register network of 16 + merge passes)
-template <int SAMPLE> struct K1Cfg { static constexpr int THREADS = SAMPLE / 16; };
+// threads of a K1 CTA: 8 sample keys per thread (register network of 8 + merge passes)
+#ifndef IPS4O_K1_PER_THREAD
+#define IPS4O_K1_PER_THREAD 8
+#endif
+template <int SAMPLE> struct K1Cfg { static constexpr int THREADS = SAMPLE / IPS4O_K1_PER_THREAD; };
 constexpr int K1_SAMPLE = 4096;        // sample capacity for ordinary tasks (32 KB smem)
 constexpr int K1_SAMPLE_BIG = 8192;    // for tasks of >= 2^22 elements (dynamic smem, 64 KB)
 #ifndef IPS4O_K1_BIG_LOG
