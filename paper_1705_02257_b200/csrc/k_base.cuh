@@ -411,7 +411,10 @@ struct CellBase {
 };
 template <int E>
 __device__ __forceinline__ u32 cpad(u32 c) { return c + 4u * (c / E); }
-constexpr u32 CELL_FIX_BUDGET = 4096;  // insertion-sort moves per leaf and thread before falling back
+#ifndef IPS4O_CELL_FIX_BUDGET
+#define IPS4O_CELL_FIX_BUDGET 16384
+#endif
+constexpr u32 CELL_FIX_BUDGET = IPS4O_CELL_FIX_BUDGET;  // estimated insertion moves per leaf before falling back
 
 // The cell kernel works on order-preserving u64 images of f64 keys (mapped on load, mapped
 // back in shared memory before the write-back): every comparison is then a plain u64 one.
