@@ -52,7 +52,10 @@ __device__ __forceinline__ u32 emit_kind(const LevelArgs& A, const TaskParam& tp
 // same group, so it is already running or done).  The group's emitted tasks take their
 // queue slots with one atomic per queue, and the base-case element count is summed per warp:
 // tens of thousands of buckets would otherwise serialise on a few counter words.
-constexpr u32 K4_GROUP = 4;
+#ifndef IPS4O_K4_GROUP
+#define IPS4O_K4_GROUP 4
+#endif
+constexpr u32 K4_GROUP = IPS4O_K4_GROUP;
 template <class TR>
 __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
     typedef typename TR::V V;
