@@ -94,6 +94,7 @@ struct Workspace {
     cudaStream_t side[4];             // base-case size classes run concurrently
     cudaEvent_t ev_fork, ev_join[4];
     bool side_ready;
+    int side_dev;
     u64* h_bnd;
     u32* h_tdone;
     u32 k2_blocks = 0, k3_blocks = 0, k3t_blocks = 0;
@@ -623,7 +624,19 @@ static int run_level(void* data, u32 T, u32 S, cudaStream_t st, bool from_splitt
 #define IPS4O_BASE_STREAMS 1
 #endif
 static cudaError_t side_streams_ready() {
-    if (g_ws.side_ready) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e0 = cudaGetDevice(&dev);
+    if (e0 != cudaSuccess) return e0;
+    if (g_ws.side_ready && g_ws.side_dev == dev) return cudaSuccess;
+    if (g_ws.side_ready) {  // the streams belong to another device: make new ones here
+        for (int c = 0; c < 4; ++c) {
+            cudaStreamDestroy(g_ws.side[c]);
+            cudaEventDestroy(g_ws.ev_join[c]);
+        }
+        cudaEventDestroy(g_ws.ev_fork);
+        g_ws.side_ready = false;
+    }
+    g_ws.side_dev = dev;
     for (int c = 0; c < 4; ++c) {
         cudaError_t e = cudaStreamCreateWithFlags(&g_ws.side[c], cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_ws.ev_join[c], cudaEventDisableTiming);
