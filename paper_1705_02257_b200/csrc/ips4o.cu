@@ -20,6 +20,9 @@
 
 namespace ips4o {
 
+#ifndef IPS4O_LAST_STRIPE_CUT  // a task's last stripe is (1 - this) of the others
+#define IPS4O_LAST_STRIPE_CUT 0.75
+#endif
 #ifndef IPS4O_STRIPES_PER_SM  // stripes per SM of a level (K2 balance vs per-stripe overhead)
 #define IPS4O_STRIPES_PER_SM 3
 #endif
@@ -486,7 +489,7 @@ static void plan_batch(const TaskDesc* tasks, u32 T, uintptr_t base_addr, u64 L,
         u64 ns = std::max<u64>(1, (main + L / 2) / L);
         // the task's last stripe is a quarter of the others: with the stripes handed out
         // longest first, the short ones fill the persistent K2 CTAs' last round
-        u64 Lt = ns > 1 ? (u64)std::ceil((double)main / ((double)ns - 0.75)) : main;
+        u64 Lt = ns > 1 ? (u64)std::ceil((double)main / ((double)ns - IPS4O_LAST_STRIPE_CUT)) : main;
         Lt = (Lt + B - 1) / B * B;
         if (ns > 1 && (ns - 1) * Lt >= main) Lt = ((main + ns - 1) / ns + B - 1) / B * B;
         ns = std::max<u64>(1, (main + Lt - 1) / Lt);
