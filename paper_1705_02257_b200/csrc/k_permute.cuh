@@ -18,6 +18,9 @@
 
 namespace ips4o {
 
+#ifndef IPS4O_K3_IDLE_NS  // back-off of a K3 warp whose chains all wait
+#define IPS4O_K3_IDLE_NS 32
+#endif
 constexpr int K2P_MAXST = 1024;  // stripes of one task staged in shared memory by k_prepare
 
 template <class TR>
@@ -731,7 +734,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A) {
                 }
                 progressed = true;
             }
-            if (!__any_sync(0xffffffffu, progressed)) __nanosleep(32);
+            if (!__any_sync(0xffffffffu, progressed)) __nanosleep(IPS4O_K3_IDLE_NS);
         }
         __syncthreads();
         if (tid == 0) atomicOr(&A.tdone[t >> 5], 1u << (t & 31));
