@@ -24,13 +24,20 @@
  * Conventions for every entry point:
  *   - Device pointers are CUDA device memory of the current device; the caller owns it.
  *   - Work is enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy default
- *     stream).  The call may synchronise `stream` internally between recursion levels
- *     (it reads back the small per-level task list); it never synchronises other streams.
+ *     stream) and the call returns without waiting for it: the recursion is scheduled on
+ *     the device (a CUDA-graph while-loop over a device task queue), so
+ *     there is no host synchronisation inside a sort.  A sort may be captured into the
+ *     caller's CUDA graph (stream capture) once the workspace exists for that element type
+ *     and at least that n (call it once outside the capture); the captured graph then refers
+ *     to that workspace and must not run concurrently with another sort.
+ *   - Calls on different streams are ordered by the library (each call waits for the
+ *     previous one's work through an event): they share one workspace.
  *   - Argument errors return synchronously and leave the data untouched.
  *   - Device faults surface as IPS4O_ECUDA from this or a later call (CUDA convention).
  *   - The library owns a lazily grown per-device auxiliary workspace whose size is
  *     reported by ips4o_aux_bytes(); it is O(k * b * CTAs + tasks), never O(n) beyond that.
- *   - Calls are serialised by an internal mutex (one sort at a time per process).
+ *   - Host-side calls are serialised by an internal mutex.
+ *   - n < 2^36 (block indices of the permutation stay below 2^31).
  */
 #ifndef IPS4O_H
 #define IPS4O_H
@@ -50,26 +57,39 @@ typedef enum {
 
 typedef enum {
     IPS4O_OK = 0,
-    IPS4O_EINVAL = -1,   /* null pointer with n > 0, bad type, n >= 2^40, bad splitters */
+    IPS4O_EINVAL = -1,   /* null pointer with n > 0, bad type, n >= 2^36, bad splitters */
     IPS4O_EALIGN = -2,   /* data pointer not aligned to 8 B (u64/f64), 16 B (pair), 4 B (rec100) */
     IPS4O_ENOMEM = -3,   /* workspace allocation failed */
     IPS4O_ECUDA = -4,    /* CUDA launch/runtime error, see ips4o_error_string */
     IPS4O_EINTERNAL = -5 /* a device-side consistency check failed (conservation, capacity) */
 } ips4o_status;
 
-/* Statistics of the most recent ips4o_sort / ips4o_debug_partition_once call. */
+/* Statistics of the most recent ips4o_sort / ips4o_debug_partition_once call.  The
+ * device-side fields are read when ips4o_last_stats() is called: it waits for that call's
+ * work to finish (the sort itself never waits).  A call captured into a CUDA graph reports
+ * only the host-side fields (n, elem_type, aux_bytes, host_syncs). */
 typedef struct {
     uint64_t n;                 /* elements sorted */
     uint32_t elem_type;
     uint32_t levels;            /* distribution levels executed (multi-CTA tier) */
-    uint64_t distribution_tasks;/* subproblems partitioned by the distribution kernels */
-    uint64_t base_tasks;        /* subproblems finished by the base-case kernel */
+    uint64_t distribution_tasks;/* subproblems partitioned by the distribution kernels (multi-CTA tier) */
+    uint64_t base_tasks;        /* subproblems finished by the base-case kernels (shared-memory tier) */
     uint64_t equality_tasks;    /* subproblems partitioned with equality buckets */
-    uint64_t aux_bytes;         /* device workspace bytes reserved for this call */
-    uint64_t kernel_launches;   /* kernels launched by this call */
-    uint64_t host_syncs;        /* stream synchronisations performed (one per level) */
+    uint64_t aux_bytes;         /* device workspace bytes reserved while sorting (see ips4o_aux_bytes) */
+    uint64_t kernel_launches;   /* kernels launched by this call (k_init + loop iterations x body kernels) */
+    uint64_t host_syncs;        /* host synchronisations inside the sort: always 0 */
     uint64_t distributed_elements; /* sum over distribution steps of the subproblem sizes */
     uint64_t base_elements;     /* sum of the base-case subproblem sizes */
+    uint64_t batches;           /* iterations of the device-side level loop that distributed tasks */
+    uint64_t base_tasks_by_class[4]; /* base-case leaves per size class (<=2K, <=4K, <=8K, <=16K elements;
+                                        records: <=512, <=1024) */
+    uint64_t base_fallback_tasks;/* leaves the cell kernel handed to the merge sort (clustered keys) */
+    uint64_t block_moves;       /* block writes of the block permutation (swaps and placements) */
+    uint64_t empty_block_moves; /* Appendix-A moves */
+    uint64_t device_error;      /* sticky device consistency flags (0 = none; nonzero: the output is invalid) */
+    uint64_t staging_bytes;     /* device staging of ips4o_sort_host / ips4o_sort_kv (0 for ips4o_sort) */
+    uint32_t has_device_stats;  /* 1 if the device-side fields above are valid */
+    uint32_t reserved_;
 } ips4o_stats;
 
 /* ---------------------------------------------------------------- sorting */
@@ -97,8 +117,12 @@ int ips4o_sort_host(void* h_data, uint64_t n, int elem_type, void* stream);
  * (pointers not 8-byte aligned), IPS4O_ENOMEM, or a status of ips4o_sort. */
 int ips4o_sort_kv(uint64_t* d_keys, uint64_t* d_vals, uint64_t n, int key_type, void* stream);
 
-/* Upper bound, in bytes, of the device workspace ips4o_sort(n, elem_type) uses
- * (Theorem 2: O(k b t) buffers; here t = stripes/CTAs). */
+/* Bytes of the device workspace ips4o_sort(n, elem_type) allocates on a fresh workspace
+ * (Theorem 2: O(k b t) buffers with t = stripes, plus the task queues).
+ * Every term is a capacity bound of the planner: per-batch task and stripe tables
+ * (<= 512 each), base-case queues (<= n / smallest leaf of the class), level queues
+ * (<= n / (base capacity + 1)), and the partial-buffer spill (<= n/2 + K*(b-1), in practice
+ * K*(b-1) per stripe).  A larger earlier call leaves the workspace at its larger size. */
 size_t ips4o_aux_bytes(uint64_t n, int elem_type);
 
 /* Statistics of the last call (host memory). */
@@ -124,12 +148,15 @@ const char* ips4o_kernel_kind_name(int kind);
 
 /* Classification of d_in[0..n) with GIVEN splitters:
  * h_splitters is HOST memory holding nspl strictly increasing keys in the element
- * type's key format (u64: uint64; f64: double; pair: uint64 key; rec100: 10-byte
- * keys packed at a 10-byte stride).  eq enables equality buckets.  Writes the bucket
- * index of every element to d_bucket_out (device, uint32[n]), using the numbering
- * of SURVEY.md §8(c) O5.  1 <= nspl <= 255 (<= 127 with eq). */
+ * type's key format (u64: uint64; f64: double; pair: uint64 key; rec100: the big-endian
+ * uint64 of key bytes 0..7, the key part a distribution step classifies on).
+ * flags bit 0 enables equality buckets; bit 1 selects K2's production classifier (the
+ * bucket-hint table, k2_bucket_keys_lut) instead of the tree descent (classify_key).
+ * Writes the bucket index of every element to d_bucket_out (device, uint32[n]), using the
+ * numbering of SURVEY.md §8(c) O5.  1 <= nspl <= 255 (<= 127 with eq).  Returns after the
+ * stream is synchronised. */
 int ips4o_debug_classify(const void* d_in, uint64_t n, int elem_type, const void* h_splitters,
-                         uint32_t nspl, int eq, uint32_t* d_bucket_out, void* stream);
+                         uint32_t nspl, int flags, uint32_t* d_bucket_out, void* stream);
 
 /* One distribution step (local classification, block permutation, cleanup) over
  * d_data[0..n) with GIVEN splitters (same format as above), without recursion.

@@ -34,14 +34,24 @@ class Ips4oError(RuntimeError):
 
 
 class Stats(ctypes.Structure):
+    """ips4o_stats of include/ips4o.h (same field order)."""
     _fields_ = [("n", ctypes.c_uint64), ("elem_type", ctypes.c_uint32), ("levels", ctypes.c_uint32),
                 ("distribution_tasks", ctypes.c_uint64), ("base_tasks", ctypes.c_uint64),
                 ("equality_tasks", ctypes.c_uint64), ("aux_bytes", ctypes.c_uint64),
                 ("kernel_launches", ctypes.c_uint64), ("host_syncs", ctypes.c_uint64),
-                ("distributed_elements", ctypes.c_uint64), ("base_elements", ctypes.c_uint64)]
+                ("distributed_elements", ctypes.c_uint64), ("base_elements", ctypes.c_uint64),
+                ("batches", ctypes.c_uint64), ("base_tasks_by_class", ctypes.c_uint64 * 4),
+                ("base_fallback_tasks", ctypes.c_uint64), ("block_moves", ctypes.c_uint64),
+                ("empty_block_moves", ctypes.c_uint64), ("device_error", ctypes.c_uint64),
+                ("staging_bytes", ctypes.c_uint64), ("has_device_stats", ctypes.c_uint32),
+                ("reserved_", ctypes.c_uint32)]
 
     def as_dict(self):
-        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+        d = {}
+        for n, _ in self._fields_:
+            v = getattr(self, n)
+            d[n] = [int(x) for x in v] if n == "base_tasks_by_class" else int(v)
+        return d
 
 
 _lib = None
@@ -103,18 +113,24 @@ def ips4o_sort_kv(keys_ptr: int, vals_ptr: int, n: int, key_type: int, stream: i
 
 
 def sort_kv_(keys, vals):
-    """Sort CUDA tensors keys (uint64 or float64) and vals (64-bit) by key, in their own
-    storage (16*n bytes of library staging, see include/ips4o.h); unstable."""
+    """Sort CUDA tensors keys (torch.uint64 or torch.float64) and vals (any 8-byte dtype) by
+    key, in their own storage; unstable (see include/ips4o.h)."""
     import torch
     if not (keys.is_cuda and vals.is_cuda) or keys.shape != vals.shape or keys.dim() != 1:
         raise Ips4oError("sort_kv_ expects two 1-D CUDA tensors of the same length")
+    if keys.device != vals.device:
+        raise Ips4oError("sort_kv_ expects keys and vals on the same device")
     if not (keys.is_contiguous() and vals.is_contiguous()) or vals.element_size() != 8:
         raise Ips4oError("sort_kv_ expects contiguous tensors and 8-byte values")
-    kt = IPS4O_F64 if keys.dtype == torch.float64 else IPS4O_U64
-    if kt == IPS4O_U64 and keys.element_size() != 8:
-        raise Ips4oError("sort_kv_ keys must be 64-bit")
-    ips4o_sort_kv(keys.data_ptr(), vals.data_ptr(), keys.shape[0], kt,
-                  torch.cuda.current_stream(keys.device).cuda_stream)
+    if keys.dtype == torch.float64:
+        kt = IPS4O_F64
+    elif keys.dtype == torch.uint64:
+        kt = IPS4O_U64
+    else:
+        raise Ips4oError("sort_kv_ keys must be torch.uint64 or torch.float64 (int64 keys would sort as unsigned)")
+    with torch.cuda.device(keys.device):
+        ips4o_sort_kv(keys.data_ptr(), vals.data_ptr(), keys.shape[0], kt,
+                      torch.cuda.current_stream(keys.device).cuda_stream)
 
 
 def ips4o_sort_host(h_ptr: int, n: int, elem_type: int, stream: int = 0) -> None:
@@ -149,8 +165,10 @@ def ips4o_profile_read() -> dict:
 
 
 def ips4o_debug_classify(d_in: int, n: int, elem_type: int, h_splitters, nspl: int, eq: bool,
-                         d_out: int, stream: int = 0) -> None:
-    _check(lib().ips4o_debug_classify(ctypes.c_void_p(d_in), n, elem_type, h_splitters, nspl, int(eq),
+                         d_out: int, stream: int = 0, lut: bool = False) -> None:
+    """flags = eq | lut << 1: lut selects K2's production classifier (bucket-hint table)."""
+    flags = int(bool(eq)) | (int(bool(lut)) << 1)
+    _check(lib().ips4o_debug_classify(ctypes.c_void_p(d_in), n, elem_type, h_splitters, nspl, flags,
                                       ctypes.c_void_p(d_out), ctypes.c_void_p(stream)),
            "ips4o_debug_classify")
 

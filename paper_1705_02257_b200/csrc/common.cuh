@@ -149,10 +149,13 @@ struct StripeDesc {
 
 enum {
     CTR_STRIPE = 0,   // K2 stripe ticket
-    CTR_NEXT = 1,     // next-level task queue length
+    CTR_NEXT = 1,     // next-level task queue length (accumulates over a level's batches)
     CTR_TICKET = 2,   // cleanup ticket
     CTR_ERROR = 3,    // error bits
     CTR_EQ = 4,       // tasks partitioned with equality buckets
+    CTR_BMOVES = 5,   // K3 block writes (swaps and placements)
+    CTR_AMOVES = 6,   // Appendix-A empty-block moves
+    CTR_FB = 7,       // base-case fallback queue length (leaves the cell kernel hands back)
     CTR_BASE0 = 8,    // base-case queue lengths, one per size class (4)
     CTR_N = 16
 };
@@ -161,15 +164,52 @@ constexpr int NUM_BASE_CLASSES = 4;
 __host__ __device__ __forceinline__ u32 base_class(u64 n, u32 c0max, u32 c1max) {
     return n <= c0max ? 0u : n <= c1max ? 1u : n <= 8192 ? 2u : 3u;
 }
-enum { ERR_SPILL = 1, ERR_CONSERVE = 2, ERR_QUEUE = 4, ERR_CAPACITY = 8, ERR_PROGRESS = 16 };
+enum { ERR_SPILL = 1, ERR_CONSERVE = 2, ERR_QUEUE = 4, ERR_CAPACITY = 8, ERR_PROGRESS = 16, ERR_ITER = 32 };
+
+// Per-batch fields written on the device (k_init, k_plan) and read by every level kernel at
+// entry: the host never writes them, so nothing is staged through host memory and the
+// whole level loop can run inside one CUDA graph (asynchronous on the
+// caller's stream, no host synchronisation inside the sort).
+struct LevelDyn {
+    void* data;           // the array being sorted (element 0 of the call)
+    u64 n;
+    TaskDesc* q_next;     // next-level queue K4 appends to (ctr[CTR_NEXT] entries)
+    u64 seed;             // this batch's sampling seed
+    u32 ntasks, nstripes; // this batch
+    u32 emit;             // 0: debug single step, no emission
+    u32 k4_cta;           // cleanup: one CTA per bucket (few buckets) instead of warp groups
+    u32 moves_gx;         // k_moves: CTAs per task
+    u32 from_splitters;   // K1 builds task 0's classifier from dsplit (debug partition step)
+    u32 nspl, spl_eq;     //   (its splitter count, equality buckets)
+    u32 more;             // set by k_epi: tasks remain
+    u32 pad_;
+};
+
+// Device-side recursion scheduler state (the task queues of the level loop).
+struct Sched {
+    TaskDesc* qa;         // tasks of the current level (na of them, ca already planned)
+    TaskDesc* qb;         // tasks of the next level (ctr[CTR_NEXT] of them)
+    u32 na, ca;
+    u32 level;
+    u32 pad_;
+    u64 ntot;             // elements of the current level (stripe length)
+    u64 seed;
+};
+
+// Device statistics of a call (u64 words), accumulated by k_init / k_plan / k_epi.
+enum {
+    DS_LEVELS = 0, DS_DIST_TASKS, DS_BASE_TASKS, DS_EQ_TASKS, DS_DIST_ELEMS, DS_BASE_ELEMS,
+    DS_BATCHES, DS_ERROR, DS_BLOCK_MOVES, DS_AMOVES, DS_FALLBACK, DS_BASE_C0, DS_BASE_C1, DS_BASE_C2,
+    DS_BASE_C3, DS_ITERS, DS_N = 16
+};
 
 struct LevelArgs {
-    void* data;
+    void* data;       // (from dyn)
     const TaskParam* tp;
-    u32 ntasks;
+    u32 ntasks;       // (from dyn)
     const StripeDesc* sd;
     const u32* stripe_order;
-    u32 nstripes;
+    u32 nstripes;     // (from dyn)
     u64* tree;        // [T][256] BFS tree a[1..k'-1] (index 0 unused)
     u64* spl;         // [T][256] sorted padded splitters s[1..k'-1]
     u32* s_count;     // [S][256] elements per bucket in stripe
@@ -184,7 +224,7 @@ struct LevelArgs {
     u64* bnd;         // [T][257] element-exact bucket starts e_0..e_256
     u32* dblk;        // [T][257] delimiters d_i (block index, rounded up)
     u32* nfb;         // [T][256] full blocks of bucket i
-    u32* btot;        // [T][256] bucket sizes: zeroed by K1, each K2 stripe adds its counts
+    u64* btot;        // [T][256] bucket sizes: zeroed by K1, each K2 stripe adds its counts
     unsigned short* lut;  // [T][LUT_STRIDE] bucket-hint tables
     u32* mov;         // [T][257] prefix of Appendix-A moves over buckets
     u64* wr;          // [T][256] control lines: word 0 packed (w:32 | r+RBIAS:32) block
@@ -194,16 +234,43 @@ struct LevelArgs {
     u32* cflag;       // [T][256] cleanup: overhang saved
     void* ovf;        // [T][B]   overflow blocks
     int* ovf_owner;   // [T]
-    TaskDesc* q_next;
-    TaskDesc* q_base;
-    u32 q_cap;
+    TaskDesc* q_next; // (from dyn)
+    TaskDesc* q_base; // base-case queues by size class: class c at q_base + qb_off[c], qb_cap[c] tasks
+    TaskDesc* q_fb;   // [q_cap] base-case fallback queue (clustered leaves -> merge sort)
+    TaskDesc* q_lvl0; // [qn_cap] level queue A
+    TaskDesc* q_lvl1; // [qn_cap] level queue B
+    u32 qb_off[4], qb_cap[4];
+    u32 q_cap;        // fallback queue capacity (tasks) = sum of qb_cap
+    u32 qn_cap;       // level queue capacity (tasks)
+    u32 tcap, scap;   // tasks / stripes per batch this workspace holds
     u32* ctr;         // [CTR_N]
     u64* spill_ctr;
     u64* base_elems;  // sum of sizes of emitted base-case tasks
+    u64* dsplit;      // [256] debug splitters (key images)
     u32 base_cap;     // tasks with <= base_cap elements go to the base case
-    int emit;         // emit next-level / base tasks (0 for the debug single step)
-    u64 seed;
+    int emit;         // (from dyn)
+    u64 seed;         // (from dyn)
+    LevelDyn* dyn;
+    Sched* sched;
+    u64* dstats;      // [DS_N]
+    u64* plog_t;      // profile stamps (globaltimer ns) and kinds; plog_n entries
+    u32* plog_k;
+    u32* plog_n;
+    u32 plog_cap;
 };
+
+// Each level kernel starts with this: the per-batch fields come from device memory.
+__device__ __forceinline__ LevelArgs with_dyn(const LevelArgs& A0) {
+    LevelArgs A = A0;
+    const LevelDyn* D = A0.dyn;
+    A.data = D->data;
+    A.ntasks = D->ntasks;
+    A.nstripes = D->nstripes;
+    A.emit = (int)D->emit;
+    A.seed = D->seed;
+    A.q_next = D->q_next;
+    return A;
+}
 
 // ---------------------------------------------------------------- device helpers
 

@@ -111,8 +111,9 @@ __device__ __forceinline__ void block_sort_smem(typename TR::V* s, u32 n) {
 
 template <class TR, int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS) k_base_merge(const TaskDesc* tasks, u32 start, const u32* d_ntasks,
-                                                         void* vdata) {
-    const u32 ntasks = *d_ntasks;  // tasks [start, ntasks) (the count lives on the device)
+                                                         const LevelDyn* dyn, u32 cap) {
+    const u32 ntasks = min(*d_ntasks, cap);  // tasks [start, ntasks) (the count lives on the device)
+    void* vdata = dyn->data;
     typedef typename TR::V V;
     extern __shared__ __align__(16) unsigned char smem5[];
     V* s = reinterpret_cast<V*>(smem5);
@@ -280,7 +281,9 @@ __device__ void rec_items_sort(ulonglong2 (&itm)[ITEMS], u32 n, ulonglong2* it, 
 }
 
 template <int KREC_ITEMS>
-__global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks, u32 ntasks, void* vdata) {
+__global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks, const u32* d_ntasks, const LevelDyn* dyn, u32 cap) {
+    const u32 ntasks = min(*d_ntasks, cap);
+    void* vdata = dyn->data;
     typedef RecBase<KREC_ITEMS> RecBase;
     extern __shared__ __align__(16) unsigned char smem5[];
     ulonglong2* it = reinterpret_cast<ulonglong2*>(smem5);
@@ -431,7 +434,10 @@ template <> struct CellWork<TF64> {
 
 template <class TR, int NT, int E>
 __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320 ? 3 : (sizeof(typename TR::V) * NT * E <= 65536 ? 2 : 1)))
-    k_base_cell(const TaskDesc* tasks, u32 ntasks, void* vdata, TaskDesc* fb_queue, u32* fb_count, u32 fb_cap) {
+    k_base_cell(const TaskDesc* tasks, const u32* d_ntasks, const LevelDyn* dyn, TaskDesc* fb_queue, u32* fb_count,
+                u32 fb_cap) {
+    const u32 ntasks = min(*d_ntasks, fb_cap);  // (the count lives on the device: the grid is fixed)
+    void* vdata = dyn->data;
     typedef typename TR::V V;
     typedef CellBase<TR, NT, E> CB;
     typedef typename CellWork<TR>::T TW;

@@ -475,7 +475,8 @@ __device__ __forceinline__ void k2_drain(typename TR::V* buf, K2Defer<TR, E>& df
 }
 
 template <class TR, int NT, int E, int MINB>
-__global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
+__global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A0) {
+    const LevelArgs A = with_dyn(A0);
     typedef typename TR::V V;
     typedef K2Smem<TR, NT, E> SM;
     constexpr int B = TR::B;
@@ -616,7 +617,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A) {
         if (tid < (u32)MAXK) {
             const u32 cb = nbl[tid] * (u32)B + cnt[tid];
             A.s_count[(u64)sidx * MAXK + tid] = cb;
-            if (cb) atomicAdd(&A.btot[(u64)sd.task * MAXK + tid], cb);
+            if (cb) atomicAdd((unsigned long long*)&A.btot[(u64)sd.task * MAXK + tid], (unsigned long long)cb);
             A.s_fill[(u64)sidx * MAXK + tid] = f;
             A.s_spoff[(u64)sidx * MAXK + tid] = excl;
             slotb[tid] = excl;

@@ -34,7 +34,8 @@ __device__ __forceinline__ void copy_rec(u32* dst, const u32* src) {
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
+__global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A0) {
+    const LevelArgs A = with_dyn(A0);
     typedef K2RecSmem<NT> SM;
     constexpr int B = TRec::B;     // records per block
     constexpr int NW = NT / 32;
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A) {
         if (tid < (u32)MAXK) {
             const u32 cb = nbl[tid] * (u32)B + cnt[tid] + nh_b;
             A.s_count[(u64)sidx * MAXK + tid] = cb;
-            if (cb) atomicAdd(&A.btot[(u64)sd.task * MAXK + tid], cb);
+            if (cb) atomicAdd((unsigned long long*)&A.btot[(u64)sd.task * MAXK + tid], (unsigned long long)cb);
             A.s_fill[(u64)sidx * MAXK + tid] = f;
             A.s_spoff[(u64)sidx * MAXK + tid] = excl;
             slotb[tid] = excl;

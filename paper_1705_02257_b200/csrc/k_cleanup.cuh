@@ -57,7 +57,9 @@ __device__ __forceinline__ u32 emit_kind(const LevelArgs& A, const TaskParam& tp
 #endif
 constexpr u32 K4_GROUP = IPS4O_K4_GROUP;
 template <class TR>
-__global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
+__global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A0) {
+    if (A0.dyn->k4_cta) return;  // this batch is cleaned up by k_cleanup_cta
+    const LevelArgs A = with_dyn(A0);
     typedef typename TR::V V;
     constexpr int B = TR::B;
     static_assert(MAXK % K4_GROUP == 0, "groups never span tasks");
@@ -248,11 +250,12 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
             for (u32 gi = 0; gi < K4_GROUP; ++gi) cntq += s_kind[gi] == lane ? 1u : 0u;
             if (cntq) {
                 u32* ctr = lane < 4u ? &A.ctr[CTR_BASE0 + lane] : &A.ctr[CTR_NEXT];
-                TaskDesc* q = lane < 4u ? A.q_base + (u64)lane * A.q_cap : A.q_next;
+                TaskDesc* q = lane < 4u ? A.q_base + A.qb_off[lane] : A.q_next;
+                const u32 cap = lane < 4u ? A.qb_cap[lane] : A.qn_cap;
                 u32 i = atomicAdd(ctr, cntq);
                 for (u32 gi = 0; gi < K4_GROUP; ++gi) {
                     if (s_kind[gi] != lane) continue;
-                    if (i < A.q_cap) q[i] = s_td[gi];
+                    if (i < cap) q[i] = s_td[gi];
                     else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
                     ++i;
                 }
@@ -263,9 +266,13 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A) {
     if (lane == 0 && base_elems) atomicAdd((unsigned long long*)A.base_elems, (unsigned long long)base_elems);
 }
 
-// Few buckets with many stripes each (the top level): one CTA per bucket.
+// Few buckets with many stripes each (the top level): one CTA per bucket, buckets taken in
+// ticket order by a persistent grid (a bucket's predecessor always has an earlier ticket, so
+// it is held by a running CTA: the wait below cannot deadlock).
 template <class TR>
-__global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A) {
+__global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A0) {
+    if (!A0.dyn->k4_cta) return;  // this batch is cleaned up by the warp kernel
+    const LevelArgs A = with_dyn(A0);
     typedef typename TR::V V;
     constexpr int B = TR::B;
     __shared__ V s_ovh[B];
@@ -274,15 +281,19 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A) {
     __shared__ u32 s_wsum[K4_THREADS / 32];
     __shared__ u32 s_ticket;
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const u32 nticket = A.ntasks * MAXK;
+    for (;;) {
+    __syncthreads();  // the previous bucket's shared state is no longer read
     if (tid == 0) s_ticket = atomicAdd(&A.ctr[CTR_TICKET], 1u);
     __syncthreads();
     const u32 ticket = s_ticket;
+    if (ticket >= nticket) break;
     const u32 t = ticket / MAXK, b = ticket % MAXK;
     const TaskParam tp = A.tp[t];
     u32* flag = A.cflag + (u64)t * MAXK;
     if (b >= tp.K) {
         if (tid == 0) st_release_u32(flag + b, 1u);
-        return;
+        continue;
     }
     V* data = reinterpret_cast<V*>(A.data);
     const u64* bnd = A.bnd + (u64)t * (MAXK + 1);
@@ -334,7 +345,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A) {
     const u64 nslots = hl + (e1 - ts);
     if ((u64)nsrc != nslots) {
         if (tid == 0) atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_CONSERVE);
-        return;
+        continue;
     }
     // wait until the bucket owning block d-1 (which holds our head) saved its overhang
     if (tid == 0 && hl > 0 && d >= 1) {
@@ -389,13 +400,14 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A) {
         if (kd < 4u) {
             atomicAdd((unsigned long long*)A.base_elems, (unsigned long long)(e1 - e0));
             const u32 i = atomicAdd(&A.ctr[CTR_BASE0 + kd], 1u);
-            if (i < A.q_cap) A.q_base[(u64)kd * A.q_cap + i] = td;
+            if (i < A.qb_cap[kd]) A.q_base[A.qb_off[kd] + i] = td;
             else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
         } else if (kd == 4u) {
             const u32 i = atomicAdd(&A.ctr[CTR_NEXT], 1u);
-            if (i < A.q_cap) A.q_next[i] = td;
+            if (i < A.qn_cap) A.q_next[i] = td;
             else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
         }
+    }
     }
 }
 

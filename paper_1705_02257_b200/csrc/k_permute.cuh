@@ -24,11 +24,14 @@ namespace ips4o {
 constexpr int K2P_MAXST = 1024;  // stripes of one task staged in shared memory by k_prepare
 
 template <class TR>
-__global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
+__global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A0) {
+    const LevelArgs A = with_dyn(A0);
     constexpr int B = TR::B;
     __shared__ u32 s_d[MAXK + 1];
     __shared__ u32 s_wsum[MAXK / 32];
+    __shared__ u64 s_wsum64[MAXK / 32];
     const u32 t = blockIdx.x, b = threadIdx.x, lane = b & 31, w = b >> 5;
+    if (t >= A.ntasks) return;  // (grid = the workspace's task capacity)
     const TaskParam tp = A.tp[t];
     const u32 S0 = tp.stripe_begin, NS = tp.nstripes;
 
@@ -42,20 +45,20 @@ __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
             s_fe[j] = A.sd[S0 + j].sb + A.s_nfull[S0 + j];
         }
     }
-    const u32 c = A.btot[(u64)t * MAXK + b];  // summed by K2 over the task's stripes
+    const u64 c = A.btot[(u64)t * MAXK + b];  // summed by K2 over the task's stripes (64-bit)
     __syncthreads();  // staged stripe ranges
-    // exclusive scan over the 256 buckets
-    u32 incl = c;
+    // exclusive scan over the 256 buckets (64-bit: a task may exceed 2^32 elements)
+    u64 incl64 = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        u32 y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (u32)o) incl += y;
+        u64 y = __shfl_up_sync(0xffffffffu, incl64, o);
+        if (lane >= (u32)o) incl64 += y;
     }
-    if (lane == 31) s_wsum[w] = incl;
+    if (lane == 31) s_wsum64[w] = incl64;
     __syncthreads();
-    u32 woff = 0;
-    for (u32 ww = 0; ww < w; ++ww) woff += s_wsum[ww];
-    const u64 e = tp.lo + woff + incl - c;
+    u64 woff64 = 0;
+    for (u32 ww = 0; ww < w; ++ww) woff64 += s_wsum64[ww];
+    const u64 e = tp.lo + woff64 + incl64 - c;
     A.bnd[(u64)t * (MAXK + 1) + b] = e;
     if (b == MAXK - 1) A.bnd[(u64)t * (MAXK + 1) + MAXK] = e + c;  // == hi
     // delimiter: e rounded up to the block grid of origin g (e < g only for e = lo)
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
     const u32 moves = nf - fullpre;
     A.nfb[(u64)t * MAXK + b] = nf;
     __syncthreads();
-    incl = moves;
+    u32 incl = moves;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         u32 y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -107,14 +110,17 @@ __global__ void __launch_bounds__(MAXK) k_prepare(LevelArgs A) {
     }
     if (lane == 31) s_wsum[w] = incl;
     __syncthreads();
-    woff = 0;
+    u32 woff = 0;
     for (u32 ww = 0; ww < w; ++ww) woff += s_wsum[ww];
     A.mov[(u64)t * (MAXK + 1) + b] = woff + incl - moves;
-    if (b == MAXK - 1) A.mov[(u64)t * (MAXK + 1) + MAXK] = woff + incl;
+    if (b == MAXK - 1) {
+        A.mov[(u64)t * (MAXK + 1) + MAXK] = woff + incl;
+        if (woff + incl) atomicAdd(&A.ctr[CTR_AMOVES], woff + incl);
+    }
     // w_i = d_i, r_i = d_i + nf_i - 1 (block indices; r biased).  A task whose
     // elements all fell into this one bucket (equal keys) has, after the Appendix-A moves,
     // only blocks of this bucket in [d, d+nf): every block is in place, w_i = d_i + nf_i.
-    const bool all_here = (u64)c == tp.hi - tp.lo;
+    const bool all_here = c == tp.hi - tp.lo;
     const u32 w0 = all_here ? d + nf : d;
     *ctl_wr(A.wr, t, b) = ((u64)w0 << 32) | (u64)(u32)(d + nf - 1u + RBIAS);
     *ctl_readers(A.wr, t, b) = 0;
@@ -183,20 +189,25 @@ __device__ __forceinline__ u32 last_le(u32 n, u64 x, F key) {
 }
 
 template <class TR>
-__global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
+__global__ void __launch_bounds__(256) k_moves(LevelArgs A0) {
+    const LevelArgs A = with_dyn(A0);
     constexpr int B = TR::B;
     // the task's per-stripe block counts and the per-bucket move ranges, staged in shared
     // memory: the searches below are then shared-memory lookups
     __shared__ u32 s_sb[K2P_MAXST], s_se[K2P_MAXST], s_F[K2P_MAXST], s_pE[K2P_MAXST], s_pF[K2P_MAXST];
     __shared__ u32 s_mov[MAXK + 1], s_d[MAXK + 1], s_nf[MAXK];
-    const u32 t = blockIdx.y;
+    // work items (task t, part bx of gx): grid-stride (the grid is fixed; gx from the plan)
+    const u32 gx = A0.dyn->moves_gx;
+    for (u32 item = blockIdx.x; item < A.ntasks * gx; item += gridDim.x) {
+    const u32 t = item / gx, bx = item % gx;
+    __syncthreads();  // the previous item's shared tables are no longer read
     const u32 lane = threadIdx.x & 31;
     const u32 wib = threadIdx.x >> 5;
     const TaskParam tp = A.tp[t];
     const u32 S0 = tp.stripe_begin, NS = tp.nstripes;
     const u32* mov = A.mov + (u64)t * (MAXK + 1);
     const u32 M = mov[MAXK];
-    if (M == 0 || blockIdx.x * (blockDim.x >> 5) * 32u >= M) return;
+    if (M == 0 || bx * (blockDim.x >> 5) * 32u >= M) continue;
     const bool staged = NS <= (u32)K2P_MAXST;
     for (u32 i = threadIdx.x; i <= (u32)MAXK; i += blockDim.x) {
         s_mov[i] = mov[i];
@@ -219,12 +230,12 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
     auto F_of = [&](u32 j) { return staged ? s_F[j] : A.s_nfull[S0 + j]; };
     auto pE_of = [&](u32 j) { return staged ? s_pE[j] : A.prefE[S0 + j]; };
     auto pF_of = [&](u32 j) { return staged ? s_pF[j] : A.prefF[S0 + j]; };
-    const u32 nwarps = gridDim.x * (blockDim.x >> 5);
+    const u32 nwarps = gx * (blockDim.x >> 5);
     char* base = reinterpret_cast<char*>(A.data) + tp.g * TR::S;
     // every lane locates one move (five binary searches), then the warp copies the 32
     // blocks two at a time (the moves are independent: sources are full blocks, targets
     // empty ones)
-    for (u32 m0 = (blockIdx.x * (blockDim.x >> 5) + wib) * 32u; m0 < M; m0 += nwarps * 32u) {
+    for (u32 m0 = (bx * (blockDim.x >> 5) + wib) * 32u; m0 < M; m0 += nwarps * 32u) {
         const u32 m = m0 + lane;
         u32 src = 0, dst = 0;
         if (m < M) {
@@ -258,6 +269,7 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A) {
             BlockIO<TR>::store(base + (u64)d0 * (B * TR::S), lane, v0);
             if (two) BlockIO<TR>::store(base + (u64)d1 * (B * TR::S), lane, v1);
         }
+    }
     }
 }
 
@@ -358,7 +370,10 @@ __global__ void k_timer_start() { g_k3_t0 = gtimer(); }
 #endif
 
 template <class TR>
-__global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A) {
+__global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A0) {
+    const LevelArgs A = with_dyn(A0);
+    if (A.ntasks == 0) return;
+    u32 nmoves = 0;  // block writes of this warp (lane 0)
     constexpr int B = TR::B;
     constexpr u32 BB = B * TR::S;  // block bytes
     constexpr int C = K3_SLOTS;
@@ -380,7 +395,7 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A) {
         }
         __syncthreads();
         const u32 nt = s_next;
-        if (nt == 0xFFFFFFFFu || nt >= T) return;
+        if (nt == 0xFFFFFFFFu || nt >= T) break;
         t = nt;
         if (tid < (u32)MAXK) s_spl[tid] = A.spl[(u64)t * MAXK + tid];
         __syncthreads();
@@ -498,6 +513,7 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A) {
                     }
                 }
                 held &= ~wrt;
+                if (lane == 0) nmoves += __popc(wrt);
             }
             // 6. consume the loads: taken blocks become held; swap targets are classified -- already in
             //    place: skip, else ours is written there and we carry on
@@ -514,6 +530,7 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A) {
                     if (d != dc) {
                         const int ow = __shfl_sync(0xffffffffu, my_ow, c);
                         BlockIO<TR>::store(tbase + (u64)ow * BB, lane, cur[c]);
+                        if (lane == 0) ++nmoves;
                         cur[c] = nxt[c];
                         if (lane == (u32)c) my_dest = d;
                     }
@@ -524,6 +541,7 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A) {
         __syncthreads();
         if (tid == 0) atomicOr(&A.tdone[t >> 5], 1u << (t & 31));
     }
+    if (lane == 0 && nmoves) atomicAdd(&A.ctr[CTR_BMOVES], nmoves);
 }
 
 
@@ -571,7 +589,10 @@ __device__ __forceinline__ bool mbar_test(u64* mbar, u32 parity) {
 }
 
 template <class TR>
-__global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A) {
+__global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
+    const LevelArgs A = with_dyn(A0);
+    if (A.ntasks == 0) return;
+    u32 nmoves = 0;  // block writes of this chain
     typedef K3TSmem<TR> SM;
     constexpr u32 BB = SM::BB;
     extern __shared__ __align__(128) unsigned char smk3[];
@@ -712,6 +733,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A) {
                 }
                 bulk_s2g(dst, mybuf + xb * BB, BB);
                 bulk_commit();
+                ++nmoves;
                 st = CH_FREE;
                 progressed = true;
             }
@@ -727,6 +749,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A) {
                     if (od != dest) {
                         bulk_s2g(tbase + (u64)slot * BB, mybuf + xb * BB, BB);
                         bulk_commit();
+                        ++nmoves;
                         xb ^= 1u;
                         dest = od;
                     }  // else: already in place, skip it and keep ours
@@ -740,6 +763,9 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A) {
         if (tid == 0) atomicOr(&A.tdone[t >> 5], 1u << (t & 31));
     }
     bulk_wait0();  // every block store is complete before the kernel ends
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nmoves += __shfl_xor_sync(0xffffffffu, nmoves, o);
+    if (lane == 0 && nmoves) atomicAdd(&A.ctr[CTR_BMOVES], nmoves);
 }
 
 }  // namespace ips4o

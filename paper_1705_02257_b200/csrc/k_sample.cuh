@@ -12,13 +12,12 @@
 
 namespace ips4o {
 
-// threads of a K1 CTA: 8 sample keys per thread (register network of 8 + merge passes)
-#ifndef IPS4O_K1_PER_THREAD
-#define IPS4O_K1_PER_THREAD 8
-#endif
-template <int SAMPLE> struct K1Cfg { static constexpr int THREADS = SAMPLE / IPS4O_K1_PER_THREAD; };
-constexpr int K1_SAMPLE = 4096;        // sample capacity for ordinary tasks (32 KB smem)
+// A K1 CTA has 1024 threads: 4 (ordinary tasks) or 8 (big tasks) sample keys per thread
+// (register network + merge passes).
+constexpr int K1_THREADS = 1024;
+constexpr int K1_SAMPLE = 4096;        // sample capacity for ordinary tasks
 constexpr int K1_SAMPLE_BIG = 8192;    // for tasks of >= 2^22 elements (dynamic smem, 64 KB)
+constexpr size_t K1_SMEM = (size_t)(K1_SAMPLE_BIG + K1_SAMPLE_BIG / 16) * 8 + 16;
 #ifndef IPS4O_K1_BIG_LOG
 #define IPS4O_K1_BIG_LOG 22
 #endif
@@ -82,7 +81,7 @@ __device__ void build_lut_block(const u64* s_dist, u32 nd, u32 kp, unsigned shor
 }
 
 __device__ void build_tree_block(const u64* s_dist, u32 nd, u32 eq, u64* g_tree, u64* g_spl,
-                                 TaskParam* tp, u32* btot, unsigned short* g_lut, u32* scr) {
+                                 TaskParam* tp, u64* btot, unsigned short* g_lut, u32* scr) {
     u32 kp = 2;
     while (kp < nd + 1) kp <<= 1;
     u32 logk = 0;
@@ -102,7 +101,7 @@ __device__ void build_tree_block(const u64* s_dist, u32 nd, u32 eq, u64* g_tree,
         }
         g_tree[j] = v;
     }
-    for (u32 i = threadIdx.x; i < (u32)MAXK; i += blockDim.x) btot[i] = 0u;
+    for (u32 i = threadIdx.x; i < (u32)MAXK; i += blockDim.x) btot[i] = 0ull;
     if (threadIdx.x == 0) {
         tp->kprime = kp;
         tp->logk = logk;
@@ -119,15 +118,10 @@ struct TKey {
     __host__ __device__ __forceinline__ static V pad() { return ~0ull; }
 };
 
+// One task t: sample, sort the sample, pick the splitters, build the classifier.
 template <class TR, int SAMPLE>
-__global__ void __launch_bounds__(K1Cfg<SAMPLE>::THREADS) k_sample(LevelArgs A) {
-    constexpr int K1_THREADS = K1Cfg<SAMPLE>::THREADS;
+__device__ __forceinline__ void k1_task(const LevelArgs& A, u32 t, u64* keys, u64* dist, u32& s_flag, u32& s_nd) {
     typedef typename TR::V V;
-    extern __shared__ __align__(16) unsigned char smem1[];
-    u64* keys = reinterpret_cast<u64*>(smem1);
-    __shared__ u64 dist[MAXK];
-    __shared__ u32 s_flag, s_nd;
-    const u32 t = blockIdx.x;
     TaskParam* tp = const_cast<TaskParam*>(A.tp) + t;
     const u64 lo = tp->lo, hi = tp->hi, n = hi - lo;
     const V* data = reinterpret_cast<const V*>(A.data);
@@ -172,7 +166,7 @@ __global__ void __launch_bounds__(K1Cfg<SAMPLE>::THREADS) k_sample(LevelArgs A) 
 #pragma unroll
     for (int q = 0; q < PER; ++q) keys[padidx(q * K1_THREADS + threadIdx.x)] = sk[q];
     __syncthreads();
-    block_sort_smem<TKey, K1_THREADS, SAMPLE / K1_THREADS>(keys, (u32)SAMPLE);
+    block_sort_smem<TKey, K1_THREADS, PER>(keys, (u32)SAMPLE);
     // equidistant picks s_i = S[i*alpha - 1]; duplicates?
     if (threadIdx.x == 0) s_flag = 0;
     __syncthreads();
@@ -201,6 +195,32 @@ __global__ void __launch_bounds__(K1Cfg<SAMPLE>::THREADS) k_sample(LevelArgs A) 
     build_tree_block(dist, s_nd, eq, A.tree + (u64)t * MAXK, A.spl + (u64)t * MAXK, tp, A.btot + (u64)t * MAXK,
                      A.lut + (u64)t * LUT_STRIDE, reinterpret_cast<u32*>(keys));  // (the sample is done)
     if (threadIdx.x == 0 && eq) atomicAdd(&A.ctr[CTR_EQ], 1u);
+}
+
+// K1: one CTA per task of the batch (grid = the workspace's task capacity; CTAs past the
+// batch exit).  Tasks of >= 2^22 elements take an 8192-key sample, the others 4096.  The
+// debug partition step (dyn->from_splitters) builds task 0's classifier from given splitters.
+template <class TR>
+__global__ void __launch_bounds__(K1_THREADS) k_sample(LevelArgs A0) {
+    const LevelArgs A = with_dyn(A0);
+    extern __shared__ __align__(16) unsigned char smem1[];
+    u64* keys = reinterpret_cast<u64*>(smem1);
+    __shared__ u64 dist[MAXK];
+    __shared__ u32 s_flag, s_nd;
+    for (u32 t = blockIdx.x; t < A.ntasks; t += gridDim.x) {
+        if (A0.dyn->from_splitters) {
+            const u32 ns = A0.dyn->nspl;
+            for (u32 i = threadIdx.x; i < ns; i += blockDim.x) dist[i] = A.dsplit[i];
+            __syncthreads();
+            build_tree_block(dist, ns, A0.dyn->spl_eq, A.tree, A.spl, const_cast<TaskParam*>(A.tp), A.btot, A.lut,
+                             reinterpret_cast<u32*>(keys));
+            return;
+        }
+        const u64 n = A.tp[t].hi - A.tp[t].lo;
+        if (n >= K1_BIG_TASK) k1_task<TR, K1_SAMPLE_BIG>(A, t, keys, dist, s_flag, s_nd);
+        else k1_task<TR, K1_SAMPLE>(A, t, keys, dist, s_flag, s_nd);
+        __syncthreads();
+    }
 }
 
 // Debug path: classifier from splitters given by the caller (already key-transformed).

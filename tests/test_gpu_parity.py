@@ -6,9 +6,9 @@ Layers (SURVEY.md §4 "build test layers"):
         multisets, every element of [e_i, e_{i+1}) in bucket i;
   (iv)  whole sorts bit-exact vs oracle.sort on every distribution and type, sizes that
         span several tiles / stripes / levels with ragged tails, degenerate inputs;
-  (v)   full BASELINE sizes in the bench launch configuration: non-decreasing keys and an
-        equal multiset digest (properties that hold at any size), plus exact oracle
-        parity where the oracle finishes in seconds (config 1).
+  (v)   full BASELINE sizes: tests/test_full_parity.py (element-wise oracle parity);
+  (vi)  asynchrony: back-to-back sorts without synchronisation, two streams, CUDA-graph
+        capture and replay; measured auxiliary memory.
 """
 import ctypes
 
@@ -22,8 +22,7 @@ torch = pytest.importorskip("torch")
 import oracle  # noqa: E402
 import paper_1705_02257_b200 as ips4o  # noqa: E402
 import workloads as W  # noqa: E402
-from gpu_util import (check_equal_to_oracle, digest, keys_nondecreasing, to_dev,  # noqa: E402
-                            to_host)
+from gpu_util import check_equal_to_oracle, to_dev, to_host  # noqa: E402
 
 TYPES = [W.ELEM_U64, W.ELEM_F64, W.ELEM_PAIR, W.ELEM_REC100]
 CAP = {W.ELEM_U64: 16384, W.ELEM_F64: 16384, W.ELEM_PAIR: 8192, W.ELEM_REC100: 1024}
@@ -105,9 +104,36 @@ def _keys_of(a, et):
     return a
 
 
+def _classify_gpu(el, et, spl, eq, lut):
+    d_in = to_dev(el, et)
+    out = torch.empty(el.shape[0], dtype=torch.int32, device="cuda")
+    buf, ptr, ns = ips4o.splitters_buffer(_spl_keys(spl, et), et)
+    ips4o.ips4o_debug_classify(d_in.data_ptr(), el.shape[0], et, ptr, ns, eq, out.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream, lut=lut)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint32)
+
+
+def _as_elems(elems, et, seed):
+    """Elements of type et whose (classification) key is `elems`.  Records: key bytes 0..7 =
+    the big-endian key, bytes 8..9 = 0, so that the oracle's 10-byte order and the GPU's
+    part-0 order agree (also for equality with a splitter)."""
+    if et == W.ELEM_PAIR:
+        return np.stack([elems.astype(np.uint64), np.arange(elems.shape[0], dtype=np.uint64)], axis=1)
+    if et == W.ELEM_REC100:
+        el = W.rec100(elems.shape[0], seed)
+        el[:, :8] = elems.astype(">u8").view(np.uint8).reshape(-1, 8)
+        el[:, 8:10] = 0
+        return el
+    return elems
+
+
 @pytest.mark.parametrize("et", TYPES)
 @pytest.mark.parametrize("eq", [False, True])
-def test_classify_vs_oracle(et, eq):
+@pytest.mark.parametrize("lut", [False, True], ids=["tree", "lut"])
+def test_classify_vs_oracle(et, eq, lut):
+    """Both GPU classifiers -- the tree descent (classify_key, used by K3) and K2's
+    bucket-hint table -- against the oracle's linear-scan-pinned classify."""
     rng = np.random.default_rng(100 + et)
     for trial in range(20):
         nspl = int(rng.integers(1, 128 if eq else 256)) if trial % 3 else int(rng.integers(1, 8))
@@ -122,24 +148,67 @@ def test_classify_vs_oracle(et, eq):
         else:
             spl = np.unique(rng.integers(0, 1 << 40, size=nspl * 2, dtype=np.uint64))[:nspl]
             elems = np.concatenate([rng.integers(0, 1 << 40, size=5000, dtype=np.uint64), spl])
-        if et == W.ELEM_PAIR:
-            el = np.stack([elems.astype(np.uint64), np.arange(elems.shape[0], dtype=np.uint64)], axis=1)
-        elif et == W.ELEM_REC100:
-            if eq:
-                continue   # record splitters compare on key part 0 only: no 10-byte equality test
-            el = W.rec100(elems.shape[0], trial)
-            el[:, :8] = elems.astype(">u8").view(np.uint8).reshape(-1, 8)
-        else:
-            el = elems
+        el = _as_elems(elems, et, trial)
         exp = oracle.classify(_oracle_spl(spl, et), eq, el)
-        d_in = to_dev(el, et)
-        out = torch.empty(el.shape[0], dtype=torch.int32, device="cuda")
-        buf, ptr, ns = ips4o.splitters_buffer(_spl_keys(spl, et), et)
-        ips4o.ips4o_debug_classify(d_in.data_ptr(), el.shape[0], et, ptr, ns, eq, out.data_ptr(),
-                                   torch.cuda.current_stream().cuda_stream)
-        torch.cuda.synchronize()
-        got = out.cpu().numpy().view(np.uint32)
-        assert np.array_equal(got, exp), (et, eq, trial)
+        got = _classify_gpu(el, et, spl, eq, lut)
+        assert np.array_equal(got, exp), (et, eq, lut, trial)
+
+
+def _adversarial_cases(rng, et):
+    """Splitter sets that stress the bucket-hint table (4096 cells over [s_1, s_k'-1]):
+    several splitters in one cell (binary search inside the cell), keys equal to splitters,
+    keys below s_1, keys at / past the last cell, the extremes of the key domain."""
+    top = (1 << 64) - 1
+    cases = []
+    # 200 splitters packed into [0, 1000] plus a few far away: one cell holds them all
+    a = np.sort(rng.choice(1000, size=200, replace=False)).astype(np.uint64)
+    b = np.array([1 << 60, (1 << 60) + 5, top - 3], dtype=np.uint64)
+    cases.append(np.concatenate([a, b]))
+    # dense runs of consecutive values around several centres
+    c = np.unique(np.concatenate([np.arange(k, k + 40, dtype=np.uint64) for k in (10, 1 << 33, 1 << 62)]))
+    cases.append(c[:255])
+    # powers of two (one splitter per binade: cells of very different populations)
+    cases.append(np.array([1 << i for i in range(0, 64, 1)], dtype=np.uint64))
+    # a single splitter; two adjacent splitters; the largest keys
+    cases.append(np.array([12345], dtype=np.uint64))
+    cases.append(np.array([7, 8], dtype=np.uint64))
+    cases.append(np.array([top - 2, top - 1, top], dtype=np.uint64))
+    out = []
+    for spl in cases:
+        near = np.concatenate([spl, spl - np.uint64(1), spl + np.uint64(1), np.array([0, 1, top, top - 1], np.uint64)])
+        rnd = rng.integers(0, 1 << 63, size=4000, dtype=np.uint64) * np.uint64(2)
+        small = rng.integers(0, 2000, size=2000).astype(np.uint64)
+        out.append((spl, np.concatenate([near, rnd, small])))
+    return out
+
+
+@pytest.mark.parametrize("et", [W.ELEM_U64, W.ELEM_PAIR, W.ELEM_REC100])
+@pytest.mark.parametrize("eq", [False, True])
+def test_classify_lut_adversarial(et, eq):
+    rng = np.random.default_rng(7 + et + 10 * eq)
+    for spl, elems in _adversarial_cases(rng, et):
+        if eq:
+            spl = spl[:127]
+        el = _as_elems(elems, et, 3)
+        exp = oracle.classify(_oracle_spl(spl, et), eq, el)
+        for lut in (False, True):
+            got = _classify_gpu(el, et, spl, eq, lut)
+            assert np.array_equal(got, exp), (et, eq, lut, spl[:4])
+
+
+@pytest.mark.parametrize("eq", [False, True])
+def test_classify_lut_f64_signs(eq):
+    """f64 keys through the order-preserving image: negative and positive values, splitters
+    clustered near 0, huge magnitudes."""
+    rng = np.random.default_rng(31 + eq)
+    spl = np.unique(np.concatenate([rng.standard_normal(40) * 1e-300, rng.standard_normal(40) * 1e300,
+                                    [-1.5, -1.0, 1.0, 1.5]]))[: (127 if eq else 255)]
+    x = np.concatenate([spl, -spl, np.nextafter(spl, np.inf), np.nextafter(spl, -np.inf),
+                        rng.standard_normal(3000), rng.standard_normal(3000) * 1e300, [1e-320, -1e-320]])
+    x = x[np.isfinite(x) & (x != 0)]
+    exp = oracle.classify(spl, eq, x)
+    for lut in (False, True):
+        assert np.array_equal(_classify_gpu(x, W.ELEM_F64, spl, eq, lut), exp), lut
 
 
 # ------------------------------------------------------------ (iii) one step
@@ -147,6 +216,10 @@ def test_classify_vs_oracle(et, eq):
 def _partition_case(et, n, nspl, eq, seed, offset=0, kind="uniform"):
     rng = np.random.default_rng(seed)
     a = _gen(et, n + offset, seed, kind)
+    if et == W.ELEM_REC100 and eq:
+        # a record step classifies on key bytes 0..7; with key bytes 8..9 zero its equality
+        # buckets are the oracle's (10-byte equality with the splitter)
+        a[:, 8:10] = 0
     keys = _keys_of(a, et)
     pool = np.unique(keys[offset:])
     nspl = min(nspl, pool.shape[0])
@@ -186,9 +259,9 @@ def test_partition_once_vs_oracle(et):
     cases = [(64, 3, False), (1000, 7, False), (4099, 255, False), (100_003, 255, False),
              (300_001, 100, True), (2_000_003, 255, False), (1_500_017, 127, True)]
     for i, (n, nspl, eq) in enumerate(cases):
-        if et == W.ELEM_REC100 and (eq or n > 400_000):
-            continue
-        _partition_case(et, n, nspl, eq, seed=7 + i)
+        if et == W.ELEM_REC100 and n > 2_000_000:
+            n = 1_000_003
+        _partition_case(et, n, nspl, eq, seed=7 + i, kind="few" if (eq and et == W.ELEM_REC100) else "uniform")
 
 
 @pytest.mark.parametrize("et", [W.ELEM_U64, W.ELEM_F64])
@@ -268,14 +341,106 @@ def test_equality_buckets_all_zero_one_step():
     assert st["distribution_tasks"] == 1 and st["equality_tasks"] == 1 and st["base_tasks"] == 0
 
 
-def test_stats_and_aux_bytes():
+@pytest.mark.parametrize("et,e", [(W.ELEM_U64, 20), (W.ELEM_U64, 24), (W.ELEM_PAIR, 22), (W.ELEM_REC100, 20)])
+def test_aux_memory_measured(et, e):
+    """Auxiliary device memory, measured: the device-memory delta (cudaMemGetInfo) of the
+    first sort after ips4o_release_workspace is the workspace ips4o_aux_bytes(n) reports
+    (plus the instantiated level-loop graph, whose size the driver decides, allowed
+    <= 4 MiB), and stays a small fraction of the input (Theorem 2)."""
+    n = 1 << e
+    _, a = W.make({W.ELEM_U64: "uniform", W.ELEM_PAIR: "pair16", W.ELEM_REC100: "rec100"}[et], n, 4)
+    t = to_dev(a, et)
+    torch.cuda.synchronize()
+    ips4o.ips4o_release_workspace()
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    ips4o.sort_(t)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    st = ips4o.ips4o_last_stats()
+    aux = ips4o.ips4o_aux_bytes(n, et)
+    assert st["aux_bytes"] == aux
+    delta = free0 - free1
+    assert delta <= aux + (4 << 20) + (2 << 20), (delta, aux)   # + graph + allocation granularity
+    input_bytes = n * W.ELEM_SIZE[et]
+    assert aux < input_bytes, (aux, input_bytes)                # < 1x the input even at 2^20
+    assert st["device_error"] == 0
+    check_equal_to_oracle(et, a, to_host(t, et), oracle.sort(a))
+
+
+def test_aux_bytes_headline_fraction():
+    """The headline config's workspace is a few percent of its 2 GiB input."""
+    assert ips4o.ips4o_aux_bytes(1 << 28, W.ELEM_U64) < 0.05 * (8 << 28)
+
+
+def test_stats_levels_and_syncs():
     n = 1 << 24
     a = W.u64_uniform(n, 4)
     _sort_gpu(a, W.ELEM_U64)
     st = ips4o.ips4o_last_stats()
-    assert st["aux_bytes"] <= ips4o.ips4o_aux_bytes(n, W.ELEM_U64)
-    assert ips4o.ips4o_aux_bytes(1 << 28, W.ELEM_U64) < 0.05 * (8 << 28)
-    assert st["levels"] >= 2
+    assert st["levels"] == 2 and st["host_syncs"] == 0 and st["device_error"] == 0
+    assert st["base_elements"] == n and sum(st["base_tasks_by_class"]) == st["base_tasks"]
+    assert st["block_moves"] > 0 and st["batches"] >= 2
+
+
+# ------------------------------------------------- asynchrony, streams, graph capture
+
+def test_back_to_back_without_sync():
+    """Several sorts (different sizes, small and large) enqueued back to back on a stream
+    kept busy by other work, with no synchronisation in between: every call's parameters
+    travel as kernel arguments, so none can see another call's (staging slots)."""
+    s = torch.cuda.Stream()
+    arrays = [W.u64_uniform(n, 20 + i) for i, n in enumerate([3000, 70_001, 500, 1 << 20, 9000, 2, 300_000])]
+    devs = [to_dev(a, W.ELEM_U64) for a in arrays]
+    torch.cuda.synchronize()
+    big = torch.empty(1 << 27, dtype=torch.int64, device="cuda")
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            big.add_(1)          # keep the stream busy before the sorts are reached
+        for t in devs:
+            ips4o.ips4o_sort(t.data_ptr(), t.shape[0], W.ELEM_U64, s.cuda_stream)
+    torch.cuda.synchronize()
+    for a, t in zip(arrays, devs):
+        assert np.array_equal(to_host(t, W.ELEM_U64), oracle.sort(a))
+
+
+def test_two_streams_share_the_workspace():
+    """Sorts alternating between two streams: the library orders them (workspace event)."""
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    arrays = [W.u64_uniform(n, 40 + i) for i, n in enumerate([1 << 20, 12_345, 1 << 19, 4000, 1 << 20])]
+    devs = [to_dev(a, W.ELEM_U64) for a in arrays]
+    torch.cuda.synchronize()
+    for i, t in enumerate(devs):
+        s = s1 if i % 2 == 0 else s2
+        ips4o.ips4o_sort(t.data_ptr(), t.shape[0], W.ELEM_U64, s.cuda_stream)
+    torch.cuda.synchronize()
+    for a, t in zip(arrays, devs):
+        assert np.array_equal(to_host(t, W.ELEM_U64), oracle.sort(a))
+
+
+@pytest.mark.parametrize("et,n", [(W.ELEM_U64, 1 << 22), (W.ELEM_U64, 5000), (W.ELEM_PAIR, 1 << 20),
+                                  (W.ELEM_F64, (1 << 21) + 3)])
+def test_graph_capture_replay(et, n):
+    """ips4o_sort captured into a caller's CUDA graph (no host sync inside the sort), replayed
+    on restored inputs: every replay matches the oracle bit for bit."""
+    _, a = W.make({W.ELEM_U64: "uniform", W.ELEM_PAIR: "pair16", W.ELEM_F64: "f64_exponential"}[et], n, 6)
+    exp = oracle.sort(a)
+    pristine = to_dev(a, et)
+    work = pristine.clone()
+    ips4o.sort_(work)            # warm: the workspace exists for this type and n
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    work.copy_(pristine)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        ips4o.ips4o_sort(work.data_ptr(), n, et, torch.cuda.current_stream().cuda_stream)
+    for _ in range(3):
+        work.copy_(pristine)
+        g.replay()
+        torch.cuda.synchronize()
+        check_equal_to_oracle(et, a, to_host(work, et), exp)
+
 
 
 @pytest.mark.parametrize("key_type", [W.ELEM_U64, W.ELEM_F64])
@@ -316,24 +481,4 @@ def test_type_switching_and_reuse():
         check_equal_to_oracle(et, a, _sort_gpu(a, et), oracle.sort(a))
 
 
-# ------------------------------------------------------ (v) full BASELINE sizes
-
-FULL = [("uniform", 28), ("f64_uniform", 28), ("f64_exponential", 28), ("rootdup", 27),
-        ("twodup", 27), ("eightdup", 27), ("almostsorted", 27), ("reversesorted", 27),
-        ("zeros", 27), ("sorted", 27), ("ones", 27), ("pair16", 27), ("rec100", 24)]
-
-
-@pytest.mark.parametrize("dist,e", FULL)
-def test_full_size_properties(dist, e):
-    et, a = W.make(dist, 1 << e, 1)
-    t = to_dev(a, et)
-    del a
-    before = digest(t)
-    ips4o.sort_(t)
-    torch.cuda.synchronize()
-    assert keys_nondecreasing(t, et)
-    assert digest(t) == before
-    if et == W.ELEM_PAIR:
-        # payload = original index: a permutation of 0..n-1 travelling with its key
-        pay = t.view(torch.int64)[:, 1]
-        assert int(pay.sum().item()) == (1 << e) * ((1 << e) - 1) // 2
+# (v) full BASELINE sizes: tests/test_full_parity.py (element-wise oracle parity)

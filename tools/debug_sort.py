@@ -1,41 +1,34 @@
-"""Debug helper: sort one workload of one size on cuda:0 and compare with numpy (child process)."""
-import os
+"""Debug helper (tools only): sort one input, report stats and the first mismatching ranges."""
 import sys
-import time
+import numpy as np
+import torch
+sys.path.insert(0, "."); sys.path.insert(0, "tests")
+import oracle
+import paper_1705_02257_b200 as ips4o
+import workloads as W
+from gpu_util import to_dev, to_host
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
-
-import numpy as np  # noqa: E402
-import torch  # noqa: E402
-
-import paper_1705_02257_b200 as ips4o  # noqa: E402
-import workloads as W  # noqa: E402
-from gpu_util import to_dev, to_host  # noqa: E402
-
-
-def main():
-    dist, n, seed = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else 1
+def run(dist, n, prof=False, seed=1):
     et, a = W.make(dist, n, seed)
+    ips4o.ips4o_profile_enable(prof)
     t = to_dev(a, et)
-    t0 = time.time()
     ips4o.sort_(t)
     torch.cuda.synchronize()
-    dt = time.time() - t0
+    st = ips4o.ips4o_last_stats()
     got = to_host(t, et)
-    if et == W.ELEM_REC100:
-        ok = np.array_equal(np.sort(np.ascontiguousarray(a).view("S100").ravel()),
-                            np.ascontiguousarray(got).view("S100").ravel()) or \
-            np.array_equal(np.sort(np.ascontiguousarray(a[:, :10]).view("S10").ravel()),
-                           np.ascontiguousarray(got[:, :10]).view("S10").ravel())
-    elif et == W.ELEM_PAIR:
-        ok = np.array_equal(np.sort(a[:, 0]), got[:, 0])
-    else:
-        ok = np.array_equal(np.sort(a), got)
-    print(dist, n, "OK" if ok else "MISMATCH", f"{dt*1e3:.1f} ms", ips4o.ips4o_last_stats(), flush=True)
-    return 0 if ok else 1
-
+    exp = oracle.sort(a)
+    k = got if et != W.ELEM_PAIR else got[:, 0]
+    ke = exp if et != W.ELEM_PAIR else exp[:, 0]
+    bad = np.nonzero(k != ke)[0] if et != W.ELEM_REC100 else np.nonzero((got[:, :10] != exp[:, :10]).any(1))[0]
+    print(dist, n, "prof" if prof else "", "mismatches", bad.size, "first", bad[:5], "last", bad[-5:] if bad.size else "")
+    print({kk: v for kk, v in st.items() if kk not in ("reserved_",)})
+    if bad.size:
+        srt = np.all(k[1:] >= k[:-1]) if et != W.ELEM_REC100 else None
+        print("output sorted:", srt, " multiset equal:", np.array_equal(np.sort(k), ke) if et != W.ELEM_REC100 else None)
 
 if __name__ == "__main__":
-    sys.exit(main())
+    torch.cuda.set_device(0)
+    for spec in sys.argv[1:]:
+        d, e = spec.split(":")[:2]
+        prof = spec.endswith(":p")
+        run(d, int(e), prof)
