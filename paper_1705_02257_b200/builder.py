@@ -11,15 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libips4o.so")
 # experimental build variants (tuning only): name -> extra nvcc flags
-VARIANTS = {"bb256": ["-DIPS4O_BLOCK_BYTES=256"],
-            "k3s2": ["-DIPS4O_K3_SLOTS=2"], "k3s8": ["-DIPS4O_K3_SLOTS=8"],
-            "k3s4m3": ["-DIPS4O_K3_MINB=3"], "k3s2m8": ["-DIPS4O_K3_SLOTS=2", "-DIPS4O_K3_MINB=8"],
-            "k3tl": ["-DIPS4O_K3_TIMELINE"], "cellbig": ["-DIPS4O_CELL_SMALL=0"],
-            "k3t_2x32": ["-DIPS4O_K3T_WARPS=2", "-DIPS4O_K3T_CHAINS=32"],
-            "k3t_8x8": ["-DIPS4O_K3T_WARPS=8", "-DIPS4O_K3T_CHAINS=8"],
-            "k3t_3x16": ["-DIPS4O_K3T_WARPS=3", "-DIPS4O_K3T_CHAINS=16"],
-            "k3t_4x24": ["-DIPS4O_K3T_WARPS=4", "-DIPS4O_K3T_CHAINS=24"],
-            "k2s1": ["-DIPS4O_K2_STAGES=1"], "k2wf": ["-DIPS4O_K2_WFLUSH=1"], "baseprof": ["-DIPS4O_BASE_PROF"], "k2tree": ["-DIPS4O_K2_LUT=0"], "basess0": ["-DIPS4O_BASE_STREAMS=0"], "cell1024": ["-DIPS4O_CELL_BIG_NT=1024"], "basewb0": ["-DIPS4O_BASE_TMA_WB=0"]}
+VARIANTS = {"cellE8": ["-DIPS4O_CELL_E=8"], "k3regs": ["-DIPS4O_K3_SLOTS=4"]}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

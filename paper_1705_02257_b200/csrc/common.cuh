@@ -14,8 +14,11 @@ constexpr u32 RBIAS = 0x80000000u;   // bias of the packed read pointer (SURVEY 
 // Each bucket's permutation control pair: the packed (w, r) word, then its reader count.
 // (Spreading the pairs over 256-byte lines -- one L2 slice each -- measured no faster.)
 constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
-#ifndef IPS4O_CELL_C1MAX  // largest leaf of the middle base-case class (8-byte types)
+#ifndef IPS4O_CELL_C1MAX  // largest leaf of base-case class 1 (8-byte types)
 #define IPS4O_CELL_C1MAX 4096
+#endif
+#ifndef IPS4O_CELL_C2MAX  // largest leaf of base-case class 2 (8/16-byte types)
+#define IPS4O_CELL_C2MAX 6144
 #endif
 #ifndef IPS4O_K2_LUT  // K2 classifies through the bucket-hint table (1) or the splitter tree only (0)
 #define IPS4O_K2_LUT 1
@@ -59,7 +62,7 @@ struct TU64 {
     typedef u64 V;
     static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 0, PARTS = 1;
     static constexpr u32 LEAF = 4096;  // target base-case size of the adaptive k
-    static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX;  // largest leaves of base-case classes 0, 1
+    static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX, C2MAX = IPS4O_CELL_C2MAX;  // largest leaves of base-case classes 0-2
     __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v; }
     __device__ __forceinline__ static bool less(V a, V b) { return a < b; }
     __host__ __device__ __forceinline__ static V pad() { return ~0ull; }
@@ -71,7 +74,7 @@ struct TF64 {
     typedef u64 V;
     static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 1, PARTS = 1;
     static constexpr u32 LEAF = 4096;
-    static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX;
+    static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX, C2MAX = IPS4O_CELL_C2MAX;
     __host__ __device__ __forceinline__ static u64 key(V v, u32 = 0) {
         return (v >> 63) ? ~v : (v | 0x8000000000000000ull);
     }
@@ -83,7 +86,7 @@ struct TPair {
     typedef ulonglong2 V;
     static constexpr int S = 16, B = BLOCK_BYTES / 16, VEC = 1, CAP = 8192, TYPE = 2, PARTS = 1;
     static constexpr u32 LEAF = 4096;
-    static constexpr u32 C0MAX = 2048, C1MAX = 4096;
+    static constexpr u32 C0MAX = 2048, C1MAX = 4096, C2MAX = IPS4O_CELL_C2MAX;
     __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v.x; }
     __device__ __forceinline__ static bool less(V a, V b) {
         return a.x < b.x || (a.x == b.x && a.y < b.y);
@@ -102,7 +105,7 @@ struct TRec {
     typedef Rec100 V;
     static constexpr int S = 100, B = 4, VEC = 0, CAP = 1024, TYPE = 3, PARTS = 2;
     static constexpr u32 LEAF = 512;
-    static constexpr u32 C0MAX = 512, C1MAX = 1024;  // record leaves: base-case classes
+    static constexpr u32 C0MAX = 512, C1MAX = 1024, C2MAX = 1024;  // record leaves: base-case classes
     __device__ __forceinline__ static u64 hi_of(u32 w0, u32 w1) {
         return ((u64)__byte_perm(w0, 0, 0x0123) << 32) | (u64)__byte_perm(w1, 0, 0x0123);
     }
@@ -157,12 +160,15 @@ enum {
     CTR_AMOVES = 6,   // Appendix-A empty-block moves
     CTR_FB = 7,       // base-case fallback queue length (leaves the cell kernel hands back)
     CTR_BASE0 = 8,    // base-case queue lengths, one per size class (4)
+    CTR_TK0 = 12,     // base-case leaf tickets, one per size class (4)
     CTR_N = 16
 };
 constexpr int NUM_BASE_CLASSES = 4;
-// base-case size classes: <= 2048, <= 4096, <= 8192, <= 16384 elements
-__host__ __device__ __forceinline__ u32 base_class(u64 n, u32 c0max, u32 c1max) {
-    return n <= c0max ? 0u : n <= c1max ? 1u : n <= 8192 ? 2u : 3u;
+// base-case size classes (8-byte types): <= 2048, <= 4096, <= 6144, <= 16384 elements; each
+// class's CTA tile is sized to its leaves, so that the per-element loops stay mostly full
+template <class TR>
+__host__ __device__ __forceinline__ u32 base_class(u64 n) {
+    return n <= TR::C0MAX ? 0u : n <= TR::C1MAX ? 1u : n <= TR::C2MAX ? 2u : 3u;
 }
 enum { ERR_SPILL = 1, ERR_CONSERVE = 2, ERR_QUEUE = 4, ERR_CAPACITY = 8, ERR_PROGRESS = 16, ERR_ITER = 32 };
 

@@ -58,7 +58,7 @@ static Caps caps_for(u64 n) {
     // stripes of a task: <= m/L + 1.5 with L >= MIN_STRIPE (k_plan)
     c.scap = (u32)std::min<u64>(MAXS, 2ull * c.tcap + n / MIN_STRIPE + 8);
     // base tasks of one batch: <= tcap*256 buckets, and <= n / (smallest size of the class)
-    const u64 minsz[4] = {2, (u64)TR::C0MAX + 1, (u64)TR::C1MAX + 1, 8193};
+    const u64 minsz[4] = {2, (u64)TR::C0MAX + 1, (u64)TR::C1MAX + 1, (u64)TR::C2MAX + 1};
     u64 tot = 0;
     for (int k = 0; k < 4; ++k) {
         const u64 q = std::min<u64>((u64)c.tcap * MAXK, n / minsz[k] + 1);
@@ -342,22 +342,15 @@ static int ensure_ws(u64 n) {
 // ------------------------------------------------------------------ kernels and grids
 
 // cell base-case configurations of the size classes (threads, elements per thread)
-#ifndef IPS4O_CELL_BIG_NT  // threads of the base-case CTA for leaves of 4097..8192 elements
-#define IPS4O_CELL_BIG_NT 512
+// 8 elements per thread (16 in the 8-byte types' largest class), the CTA sized to the class.
+#ifndef IPS4O_CELL_E  // elements per thread of the 8-byte types' base-case classes 0-2
+#define IPS4O_CELL_E 16
 #endif
-#ifndef IPS4O_CELL_SMALL
-#define IPS4O_CELL_SMALL 1
-#endif
-#ifndef IPS4O_CELL_OVERSUB  // base-case grid: resident CTAs times this (persistent loops)
-#define IPS4O_CELL_OVERSUB 8
-#endif
-// 8-byte types: 16 elements per thread in small CTAs (more leaves in flight per SM);
-// 16-byte types: 8 per thread (register budget)
 template <class TR> struct CellCfg {
-    static constexpr bool small = IPS4O_CELL_SMALL && TR::S == 8;
-    static constexpr int NT0 = small ? 128 : 256, E0 = small ? 16 : 8;
-    static constexpr int NT1 = small ? (int)TR::C1MAX / 16 : 512, E1 = small ? 16 : 8;
-    static constexpr int NT2 = IPS4O_CELL_BIG_NT, E2 = 8192 / IPS4O_CELL_BIG_NT;  // leaves of <= 8192
+    static constexpr int E0 = TR::S == 8 ? IPS4O_CELL_E : 8, NT0 = (int)TR::C0MAX / E0;
+    static constexpr int E1 = TR::S == 8 ? IPS4O_CELL_E : 8, NT1 = (int)TR::C1MAX / E1;
+    static constexpr int E2 = TR::S == 8 ? IPS4O_CELL_E : 8, NT2 = (int)TR::C2MAX / E2;
+    static constexpr int E3 = TR::S == 8 ? 16 : 8, NT3 = (int)TR::CAP / E3;
 };
 template <class TR>
 struct MergeCfg {
@@ -371,7 +364,7 @@ static cudaError_t cell_setup(u32* grid, int nsm) {
     if (e != cudaSuccess) return e;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_base_cell<TR, NT, E>, NT, CB::smem);
-    *grid = (u32)std::max(1, occ) * IPS4O_CELL_OVERSUB * (u32)nsm;
+    *grid = (u32)std::max(1, occ) * (u32)nsm;  // resident CTAs (leaves are taken by ticket)
     return e;
 }
 
@@ -415,7 +408,7 @@ static int prepare_kernels(void) {
         CK((cell_setup<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>(&g_ws.cell_grid[0], nsm)));
         CK((cell_setup<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>(&g_ws.cell_grid[1], nsm)));
         CK((cell_setup<TR, CellCfg<TR>::NT2, CellCfg<TR>::E2>(&g_ws.cell_grid[2], nsm)));
-        if constexpr (TR::CAP >= 16384) CK((cell_setup<TR, 1024, 16>(&g_ws.cell_grid[3], nsm)));
+        if constexpr (TR::CAP > TR::C2MAX) CK((cell_setup<TR, CellCfg<TR>::NT3, CellCfg<TR>::E3>(&g_ws.cell_grid[3], nsm)));
         typedef MergeCfg<TR> M;
         CK(cudaFuncSetAttribute(k_base_merge<TR, M::TH, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)M::BC::smem));
@@ -494,7 +487,8 @@ static int enqueue_cell(Enq& q, cudaStream_t s, u32 c) {
     const LevelArgs& A = g_ws.A;
     typedef CellBase<TR, NT, E> CB;
     LAUNCH(KK_BASE, (k_base_cell<TR, NT, E><<<g_ws.cell_grid[c], NT, CB::smem, s>>>(
-                         A.q_base + A.qb_off[c], A.ctr + CTR_BASE0 + c, A.dyn, A.q_fb, A.ctr + CTR_FB, A.q_cap)));
+                         A.q_base + A.qb_off[c], A.ctr + CTR_BASE0 + c, A.qb_cap[c], A.ctr + CTR_TK0 + c, A.dyn,
+                         A.q_fb, A.ctr + CTR_FB, A.q_cap)));
     return IPS4O_OK;
 }
 
@@ -533,8 +527,8 @@ static int enqueue_base(Enq& q) {
         rc = enqueue_cell<TR, CellCfg<TR>::NT2, CellCfg<TR>::E2>(q, ss[2], 2);
         if (rc) return rc;
         STAMP(KK_BASE);
-        if constexpr (TR::CAP >= 16384) {
-            rc = enqueue_cell<TR, 1024, 16>(q, ss[3], 3);
+        if constexpr (TR::CAP > TR::C2MAX) {
+            rc = enqueue_cell<TR, CellCfg<TR>::NT3, CellCfg<TR>::E3>(q, ss[3], 3);
             if (rc) return rc;
             STAMP(KK_BASE);
         }
@@ -552,9 +546,10 @@ static int enqueue_base(Enq& q) {
     }
 }
 
-// One iteration of the level loop: plan, K1..K4, base case, epilogue (sets the condition).
+// One iteration of the level loop: plan, K1..K4, base case, epilogue (sets the condition;
+// eager mode: no handle, the host reads LevelDyn::more).
 template <class TR>
-static int enqueue_body(Enq& q, cudaGraphConditionalHandle h) {
+static int enqueue_body(Enq& q, cudaGraphConditionalHandle h, u32 use_handle = 1u) {
     const LevelArgs& A = g_ws.A;
     STAMP(STAMP_BEGIN);
     LAUNCH(KK_OTHER, (k_plan<TR><<<1, PLAN_THREADS, 0, q.st>>>(A, (u32)g_ws.num_sms)));
@@ -563,7 +558,7 @@ static int enqueue_body(Enq& q, cudaGraphConditionalHandle h) {
     if (rc) return rc;
     rc = enqueue_base<TR>(q);
     if (rc) return rc;
-    LAUNCH(KK_OTHER, (k_epi<<<1, 32, 0, q.st>>>(A, h, 1u)));
+    LAUNCH(KK_OTHER, (k_epi<<<1, 32, 0, q.st>>>(A, h, use_handle)));
     STAMP(KK_OTHER);
     return IPS4O_OK;
 }
@@ -623,6 +618,33 @@ static int get_graph(bool prof, GraphCache** out) {
 static bool g_prof_on = false;
 static u32 g_nodes_per_iter = 0;
 
+// IPS4O_EAGER=1: the same loop driven from the host (one stream sync per iteration to read
+// LevelDyn::more) -- for profilers that cannot look inside conditional graphs (ncu).  Not
+// the product path: it synchronises.
+static bool eager_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("IPS4O_EAGER");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+template <class TR>
+static int run_eager(cudaStream_t st) {
+    for (u64 it = 0;; ++it) {
+        Enq q{st, false};
+        int rc = enqueue_body<TR>(q, 0, 0u);
+        if (rc) return rc;
+        g_nodes_per_iter = q.launches;
+        u32 more = 0;
+        CK(cudaMemcpyAsync(&more, &g_ws.A.dyn->more, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        g_stats.host_syncs++;
+        if (!more || it > MAX_BATCHES) break;
+    }
+    return IPS4O_OK;
+}
+
 template <class TR>
 static int sort_impl(void* data, u64 n, cudaStream_t st) {
     int rc = ensure_ws<TR>(n);
@@ -637,10 +659,18 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
     // previous call's work (the event is recorded at the end of every call)
     if (!capturing && g_ws.have_done && !g_ws.last_captured && g_ws.last_stream != st)
         CK(cudaStreamWaitEvent(st, g_ws.ev_done, 0));
-    const u32 small = n <= (u64)TR::CAP ? base_class(n, TR::C0MAX, TR::C1MAX) : (u32)NUM_BASE_CLASSES;
+    const u32 small = n <= (u64)TR::CAP ? base_class<TR>(n) : (u32)NUM_BASE_CLASSES;
     k_init<<<1, 32, 0, st>>>(g_ws.A, data, n, 0x1234567ull, small);
     CK(cudaGetLastError());
-    if (!capturing) {
+    g_stats.host_syncs = 0;
+    if (!capturing && eager_mode()) {
+        rc = run_eager<TR>(st);
+        if (rc) return rc;
+        CK(cudaEventRecord(g_ws.ev_done, st));
+        g_ws.have_done = true;
+        g_ws.last_captured = false;
+        g_ws.last_stream = st;
+    } else if (!capturing) {
         GraphCache* gc = nullptr;
         rc = get_graph<TR>(g_prof_on, &gc);
         if (rc) return rc;
@@ -664,7 +694,6 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
         g_nodes_per_iter = nodes;
         g_ws.last_captured = true;
     }
-    g_stats.host_syncs = 0;
     return IPS4O_OK;
 }
 

@@ -407,7 +407,6 @@ __device__ unsigned long long g_base_prof[2][8];
 template <class TR, int NT, int E>
 struct CellBase {
     static constexpr u32 TILE = NT * E;
-    static constexpr u32 LOG_CELLS = TILE >= 8192 ? 13 : TILE >= 4096 ? 12 : TILE >= 2048 ? 11 : TILE >= 1024 ? 10 : 9;
     static constexpr size_t x_bytes = (size_t)TILE * sizeof(typename TR::V) + 16;  // + alignment shift
     static constexpr size_t cnt_bytes = (size_t)((E + 4) * NT + 8) * 4;
     static constexpr size_t smem = x_bytes + cnt_bytes;
@@ -433,11 +432,41 @@ template <> struct CellWork<TF64> {
 };
 
 template <class TR, int NT, int E>
-__global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320 ? 3 : (sizeof(typename TR::V) * NT * E <= 65536 ? 2 : 1)))
-    k_base_cell(const TaskDesc* tasks, const u32* d_ntasks, const LevelDyn* dyn, TaskDesc* fb_queue, u32* fb_count,
-                u32 fb_cap) {
-    const u32 ntasks = min(*d_ntasks, fb_cap);  // (the count lives on the device: the grid is fixed)
-    void* vdata = dyn->data;
+struct CellMinB {
+    static constexpr int v = sizeof(typename TR::V) == 8
+                                 ? (E >= 16 ? (NT <= 128 ? 6 : NT <= 256 ? 3 : NT <= 384 ? 2 : 1)
+                                            : (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 512 ? 2 : 1))
+                                 : (NT <= 256 ? 3 : 1);
+};
+__device__ __forceinline__ u32 atoms_inc(u32 saddr) {
+    u32 r;
+    asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(saddr));
+    return r;
+}
+__device__ __forceinline__ u32 lds_u32(u32 saddr) {
+    u32 r;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(saddr));
+    return r;
+}
+template <class V>
+__device__ __forceinline__ void sts_v(u32 saddr, const V& v) {
+    if constexpr (sizeof(V) == 8) {
+        u64 x;
+        memcpy(&x, &v, 8);
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(saddr), "l"(x));
+    } else {
+        ulonglong2 x;
+        memcpy(&x, &v, 16);
+        asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(saddr), "l"(x.x), "l"(x.y));
+    }
+}
+// Leaves are taken from the class queue through an atomic ticket (the grid is the resident
+// CTAs: a CTA that finishes early takes the next leaf); the next leaf's descriptor is known
+// one leaf ahead and its elements are prefetched into L2 by a TMA bulk prefetch.
+template <class TR, int NT, int E>
+__global__ void __launch_bounds__(NT, (CellMinB<TR, NT, E>::v))
+    k_base_cell(const TaskDesc* tasks, const u32* d_ntasks, u32 qcap, u32* ticket, const LevelDyn* dyn,
+                TaskDesc* fb_queue, u32* fb_count, u32 fb_cap) {
     typedef typename TR::V V;
     typedef CellBase<TR, NT, E> CB;
     typedef typename CellWork<TR>::T TW;
@@ -446,87 +475,140 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320
     extern __shared__ __align__(16) unsigned char smc[];
     V* const X0 = reinterpret_cast<V*>(smc);
     u32* cnt = reinterpret_cast<u32*>(smc + CB::x_bytes);
-    __shared__ u64 s_range[2];
-    __shared__ u32 s_flag, s_wsum[NW];
-    V* data = reinterpret_cast<V*>(vdata);
+    __shared__ u32 s_r[4];        // 32-bit key-range halves: hi min / max, lo min / max
+    __shared__ u64 s_r64[2];      // exact 64-bit range (leaves whose high halves are close)
+    __shared__ u32 s_flag, s_wsum[NW], s_next[2];
+    const u32 ntasks = min(*d_ntasks, qcap);  // (the count lives on the device: the grid is fixed)
+    V* data = reinterpret_cast<V*>(dyn->data);
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     uint4* myrun = reinterpret_cast<uint4*>(cnt + cpad<E>(tid * E));  // this thread's E counters
     BASE_PROF_INIT();
-    // the next leaf's descriptor is read one leaf ahead, and its elements are prefetched
-    // into L2 by a TMA bulk prefetch during the current leaf (its load then hits L2)
-    TaskDesc tnext = blockIdx.x < ntasks ? tasks[blockIdx.x] : TaskDesc{0, 0, 0, 0};
-    for (u32 ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
-        const TaskDesc td = tnext;
-        if (ti + gridDim.x < ntasks) tnext = tasks[ti + gridDim.x];
+    if (tid == 0) s_next[0] = atomicAdd(ticket, 1u);
+    __syncthreads();
+    u32 cur = s_next[0], par = 1;
+    while (cur < ntasks) {
+        const TaskDesc td = tasks[cur];
+        if (tid == 0) s_next[par] = atomicAdd(ticket, 1u);  // the next leaf (read after the barriers below)
         const u32 n = (u32)(td.hi - td.lo);
         V* g = data + td.lo;
         // the leaf in shared memory starts at the same offset modulo 16 bytes as in global
         // memory, so that its aligned body leaves by one TMA bulk store
         const u32 p = sizeof(V) == 8 ? (u32)((reinterpret_cast<uintptr_t>(g) >> 3) & 1u) : 0u;
         V* const X = X0 + p;
-        // 2^cb >= n cells, at most the largest power of two <= the tile (a leaf above it,
-        // in a tile that is not a power of two, has up to 1.25 elements per cell)
-        const u32 cb = min(n > 1 ? 32u - (u32)__clz(n - 1) : 1u, CB::LOG_CELLS);
-        const u32 ncell = 1u << cb;
-        __syncthreads();  // the previous leaf is finished
-        BASE_PROF_MARK(0);
+        const u32 ncell = n > 1 ? n : 1u;  // one cell per element (n <= the tile)
         if (tid == 0) {
-            s_range[0] = ~0ull;
-            s_range[1] = 0ull;
+            s_r[0] = ~0u;
+            s_r[1] = 0u;
+            s_r[2] = ~0u;
+            s_r[3] = 0u;
+            s_r64[0] = ~0ull;
+            s_r64[1] = 0ull;
             s_flag = 0;
         }
 #pragma unroll
         for (int k = 0; k < E / 4; ++k) myrun[k] = make_uint4(0u, 0u, 0u, 0u);
-        // 1. load (element j*NT + tid) and the key range
+        // 1. load (element j*NT + tid) and the range of the keys' high 32-bit halves
+        //    (warp reductions in one REDUX instruction each)
+        //    (branch-free over the whole tile: the slots past n load a copy of element n-1,
+        //    which changes no range; they get cells of their own past the leaf's cells)
         V v[E];
-        u64 kmin = ~0ull, kmax = 0ull;
+        u32 hmin = ~0u, hmax = 0u;
 #pragma unroll
         for (int j = 0; j < E; ++j) {
-            const u32 idx = j * NT + tid;
-            if (idx < n) {
-                v[j] = CellWork<TR>::in(g[idx]);
-                const u64 k = TW::key(v[j]);
-                kmin = k < kmin ? k : kmin;
-                kmax = k > kmax ? k : kmax;
-            }
+            const u32 idx = min((u32)(j * NT) + tid, n - 1u);
+            v[j] = CellWork<TR>::in(g[idx]);
+            const u32 h = (u32)(TW::key(v[j]) >> 32);
+            hmin = min(hmin, h);
+            hmax = max(hmax, h);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const u64 a = __shfl_xor_sync(0xffffffffu, kmin, o), b = __shfl_xor_sync(0xffffffffu, kmax, o);
-            kmin = a < kmin ? a : kmin;
-            kmax = b > kmax ? b : kmax;
-        }
-        __syncthreads();
+        hmin = __reduce_min_sync(0xffffffffu, hmin);
+        hmax = __reduce_max_sync(0xffffffffu, hmax);
+        __syncthreads();  // the range words and the counters are reset; the previous leaf is done
         BASE_PROF_MARK(1);
-        if (lane == 0 && w * 32 < n) {
-            atomicMin(&s_range[0], kmin);
-            atomicMax(&s_range[1], kmax);
+        if (lane == 0) {
+            atomicMin(&s_r[0], hmin);
+            atomicMax(&s_r[1], hmax);
         }
         __syncthreads();
         BASE_PROF_MARK(2);
-        if (tid == 0 && ti + gridDim.x < ntasks) {
-            const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + tnext.lo) & ~(uintptr_t)15;
-            const uintptr_t a1 = (reinterpret_cast<uintptr_t>(data + tnext.hi) + 15) & ~(uintptr_t)15;
+        const u32 nxt = s_next[par];
+        if (tid == 0 && nxt < ntasks) {
+            const TaskDesc tn = tasks[nxt];
+            const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + tn.lo) & ~(uintptr_t)15;
+            const uintptr_t a1 = (reinterpret_cast<uintptr_t>(data + tn.hi) + 15) & ~(uintptr_t)15;
             if (a1 > a0) bulk_prefetch_l2(reinterpret_cast<const void*>(a0), (u32)(a1 - a0));
         }
-        kmin = s_range[0];
-        const u64 span = s_range[1] - kmin;
-        if (span == 0) continue;  // all keys equal: already sorted (no write)
-        // cell(key) = floor((key - kmin) * ncell / (span + 1)) as the high half of a 64x64
-        // product with a per-leaf multiplier: monotone, onto [0, ncell)
-        // (every thread computes it: mul = floor((2^64-1)/(span+1)) * ncell keeps
-        // span * mul < ncell * 2^64, so cells stay in [0, ncell))
-        const u64 mul = span < ncell ? 0ull : (span == ~0ull ? (u64)ncell : (~0ull / (span + 1)) * ncell);
-        // 2. cell and rank inside the cell
+        // the key range: from the high halves when they are far apart (a conservative range
+        // at most (d+1)/(d-1) wider than the exact one for d = hmax - hmin >= 16); exact from
+        // the low halves when all high halves are equal; exact 64-bit otherwise
+        const u32 H0 = s_r[0], H1 = s_r[1];
+        u64 kmin, span;
+        if (H1 - H0 >= 16u) {
+            kmin = (u64)H0 << 32;
+            span = ((((u64)H1) << 32) | 0xFFFFFFFFull) - kmin;
+        } else if (H1 == H0) {
+            u32 lmin = ~0u, lmax = 0u;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const u32 l = (u32)TW::key(v[j]);
+                lmin = min(lmin, l);
+                lmax = max(lmax, l);
+            }
+            lmin = __reduce_min_sync(0xffffffffu, lmin);
+            lmax = __reduce_max_sync(0xffffffffu, lmax);
+            if (lane == 0) {
+                atomicMin(&s_r[2], lmin);
+                atomicMax(&s_r[3], lmax);
+            }
+            __syncthreads();
+            kmin = ((u64)H0 << 32) | s_r[2];
+            span = (u64)(s_r[3] - s_r[2]);
+        } else {
+            u64 mn = ~0ull, mx = 0ull;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const u64 k = TW::key(v[j]);
+                mn = k < mn ? k : mn;
+                mx = k > mx ? k : mx;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const u64 a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+                mn = a < mn ? a : mn;
+                mx = b > mx ? b : mx;
+            }
+            if (lane == 0) {
+                atomicMin(&s_r64[0], mn);
+                atomicMax(&s_r64[1], mx);
+            }
+            __syncthreads();
+            kmin = s_r64[0];
+            span = s_r64[1] - kmin;
+        }
+        if (span == 0) {  // all keys equal: already sorted (no write)
+            cur = nxt;
+            par ^= 1u;
+            continue;
+        }
+        // cell(key) = floor(x * ncell / (span32 + 1)) for x = (key - kmin) >> s, the top 32
+        // bits of the offset (s = 0 when the span fits 32 bits): one 32x32 multiply-high with
+        // a per-leaf multiplier, monotone, onto [0, ncell).  (mul = floor(ncell * 2^32 /
+        // (span32 + 1)) < 2^32 for span32 >= ncell; otherwise s = 0 and the cell is x itself,
+        // a single key value.)
+        const u32 bl = 64u - (u32)__clzll((long long)span);
+        const u32 sh = bl > 32u ? bl - 32u : 0u;
+        const u32 span32 = (u32)(span >> sh);
+        const u32 mul = span32 >= ncell ? (u32)(((u64)ncell << 32) / ((u64)span32 + 1ull)) : 0u;
+        // 2. cell and rank inside the cell (slots past n: cell = the slot index >= n)
+        const u32 s_cnt = (u32)__cvta_generic_to_shared(cnt);
         u32 cr[E];  // cell | rank << 16
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             const u32 idx = j * NT + tid;
-            if (idx < n) {
-                const u64 x = TW::key(v[j]) - kmin;
-                const u32 c = mul ? (u32)__umul64hi(x, mul) : (u32)x;
-                cr[j] = c | (atomicAdd(&cnt[cpad<E>(c)], 1u) << 16);
-            }
+            const u32 x = (u32)((TW::key(v[j]) - kmin) >> sh);
+            u32 c = mul ? __umulhi(x, mul) : x;
+            c = idx < n ? c : idx;
+            cr[j] = c | (atoms_inc(s_cnt + 4u * cpad<E>(c)) << 16);
         }
         __syncthreads();
         BASE_PROF_MARK(3);
@@ -572,12 +654,17 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320
                 const u32 q = atomicAdd(fb_count, 1u);
                 if (q < fb_cap) fb_queue[q] = td;
             }
+            cur = nxt;
+            par ^= 1u;
             continue;
         }
+        {
+            const u32 s_x = (u32)__cvta_generic_to_shared(X);
 #pragma unroll
-        for (int j = 0; j < E; ++j) {
-            const u32 idx = j * NT + tid;
-            if (idx < n) X[cnt[cpad<E>(cr[j] & 0xFFFFu)] + (cr[j] >> 16)] = v[j];
+            for (int j = 0; j < E; ++j) {
+                const u32 pos = lds_u32(s_cnt + 4u * cpad<E>(cr[j] & 0xFFFFu)) + (cr[j] >> 16);
+                sts_v<V>(s_x + pos * (u32)sizeof(V), v[j]);
+            }
         }
         __syncthreads();
         BASE_PROF_MARK(6);
@@ -597,7 +684,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320
                 bs[4 * k + 2] = q.z;
                 bs[4 * k + 3] = q.w;
             }
-            bs[E] = tid + 1 < (u32)NT ? cnt[cpad<E>((tid + 1) * E)] : n;
+            bs[E] = tid + 1 < (u32)NT ? cnt[cpad<E>((tid + 1) * E)] : (u32)CB::TILE;
             // cells of 2 (most multi-element cells), of 3-4 and larger ones in separate
             // loops, so that a warp's lanes run the same code in each
             u32 m2 = 0, m34 = 0, mbig = 0;
@@ -605,7 +692,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320
             for (int k = 0; k < E; ++k) {
                 const u32 m = bs[k + 1] - bs[k];
                 m2 |= (m == 2u ? 1u : 0u) << k;
-                m34 |= (m == 3u || m == 4u ? 1u : 0u) << k;
+                m34 |= (m - 3u <= 1u ? 1u : 0u) << k;
                 mbig |= (m > 4u ? 1u : 0u) << k;
             }
             const u32 enext = bs[E];
@@ -685,6 +772,8 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 320
         // 5. write back
         for (u32 i = tid; i < n; i += NT) g[i] = X[i];
 #endif
+        cur = nxt;
+        par ^= 1u;
     }
     if (IPS4O_BASE_TMA_WB && tid == 0) bulk_wait0();
     BASE_PROF_FLUSH(NT >= 512 ? 1 : 0);

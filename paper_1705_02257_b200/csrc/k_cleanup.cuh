@@ -41,7 +41,7 @@ __device__ __forceinline__ u32 emit_kind(const LevelArgs& A, const TaskParam& tp
     if (!emit) return 5u;
     if (sz <= A.base_cap) {
         *td = TaskDesc{e0, e1, 0u, 0u};
-        return base_class(sz, TR::C0MAX, TR::C1MAX);
+        return base_class<TR>(sz);
     }
     *td = TaskDesc{e0, e1, part, 0u};
     return 4u;

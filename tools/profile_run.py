@@ -25,7 +25,9 @@ def main():
         work.copy_(pristine)
         ips4o.ips4o_sort(work.data_ptr(), arr.shape[0], et, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
-    ok = bench.verify(work, et, pristine)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from gpu_util import digest, keys_nondecreasing
+    ok = keys_nondecreasing(work, et) and digest(work) == digest(pristine)
     print("ok" if ok else "MISMATCH", ips4o.ips4o_last_stats())
     return 0 if ok else 1
 
