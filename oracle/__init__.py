@@ -28,8 +28,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ips4o_oracle.c")
 _LIB = os.path.join(_HERE, "libips4o_oracle.so")
 
-ELEM_U64, ELEM_F64, ELEM_PAIR, ELEM_REC100 = 0, 1, 2, 3
-_SIZES = {0: 8, 1: 8, 2: 16, 3: 100}
+ELEM_U64, ELEM_F64, ELEM_PAIR, ELEM_REC100, ELEM_PAIR_F64, ELEM_QUARTET_F64 = 0, 1, 2, 3, 4, 5
+_SIZES = {0: 8, 1: 8, 2: 16, 3: 100, 4: 16, 5: 32}
 
 
 class Params(ctypes.Structure):
@@ -96,6 +96,10 @@ def type_of(a: np.ndarray) -> int:
         return ELEM_PAIR
     if a.dtype == np.uint8 and a.ndim == 2 and a.shape[1] == 100:
         return ELEM_REC100
+    if a.dtype == np.float64 and a.ndim == 2 and a.shape[1] == 2:
+        return ELEM_PAIR_F64
+    if a.dtype == np.float64 and a.ndim == 2 and a.shape[1] == 4:
+        return ELEM_QUARTET_F64
     raise TypeError(f"unsupported array {a.dtype} {a.shape}")
 
 

@@ -17,7 +17,7 @@
  * Readings where the paper is silent follow SURVEY.md §8(c) S1-S28 and are
  * listed in DESIGN.md "Readings".  No blocking, fusion or reordering beyond
  * what the algorithm states; every element is moved with memcpy and compared
- * through a per-type less() so the code reads the same for all four types.
+ * through a per-type less() so the code reads the same for all six types.
  * Nothing here is shared with the CUDA path.
  */
 #include "ips4o_oracle.h"
@@ -44,6 +44,18 @@ static int less_f64(const void* a, const void* b) {
 }
 static int less_pair(const void* a, const void* b) { return less_u64(a, b); } /* key at offset 0 */
 static int less_rec100(const void* a, const void* b) { return memcmp(a, b, 10) < 0; }
+/* The paper's Pair: one 64-bit floating point key and one 64-bit value. */
+static int less_pair_f64(const void* a, const void* b) { return less_f64(a, b); } /* key at offset 0 */
+/* The paper's Quartet: three 64-bit floating point keys compared lexicographically, and one
+ * 64-bit value. */
+static int less_quartet_f64(const void* a, const void* b) {
+    double x[3], y[3];
+    memcpy(x, a, 24);
+    memcpy(y, b, 24);
+    if (x[0] != y[0]) return x[0] < y[0];
+    if (x[1] != y[1]) return x[1] < y[1];
+    return x[2] < y[2];
+}
 
 typedef struct {
     size_t s;
@@ -56,6 +68,8 @@ static int get_type(int type, etype* t) {
         case 1: t->s = 8; t->less = less_f64; return 1;
         case 2: t->s = 16; t->less = less_pair; return 1;
         case 3: t->s = 100; t->less = less_rec100; return 1;
+        case 4: t->s = 16; t->less = less_pair_f64; return 1;
+        case 5: t->s = 32; t->less = less_quartet_f64; return 1;
         default: return 0;
     }
 }

@@ -17,6 +17,10 @@
  *   1 f64     8 B, IEEE '<' (inputs carry no NaN and no -0.0)
  *   2 pair    16 B {u64 key; u64 payload}, ordered by key only
  *   3 rec100  100 B, key = bytes [0,10) compared with memcmp
+ *   4 pair_f64     16 B {f64 key; f64 payload}, ordered by the key (the paper's Pair,
+ *                  PAPER.md:447-448)
+ *   5 quartet_f64  32 B {f64 k0, k1, k2; f64 payload}, keys compared lexicographically
+ *                  (the paper's Quartet)
  */
 #ifndef IPS4O_ORACLE_H
 #define IPS4O_ORACLE_H

@@ -376,3 +376,80 @@ def test_generators_deterministic_and_clean():
     u = W.u_stream(1, 0, 4)
     assert u[0] != W.u_stream(0, 1, 1)[0]   # seeds do not alias at shifted indices
     assert len(np.unique(W.eight_dup(1 << 20))) < (1 << 20)
+
+
+# ------------------------------- the paper's Pair and Quartet (f64 keys)
+
+def _check_f64_records(et, a, out):
+    """Pair (key, payload) / Quartet (k0, k1, k2, payload): the key sequence equals the
+    lexicographic sort of the input's keys (numpy.lexsort, a library routine: the key sequence
+    is unique), and the payloads (original indices) are a permutation that carries each
+    record's keys."""
+    nk = 1 if et == W.ELEM_PAIR_F64 else 3
+    keys = a[:, :nk]
+    order = np.lexsort(tuple(keys[:, j] for j in reversed(range(nk))))
+    assert np.array_equal(out[:, :nk].view(np.uint64), keys[order].view(np.uint64))
+    pay = out[:, nk].astype(np.int64)
+    assert np.array_equal(np.sort(pay), np.arange(a.shape[0]))
+    assert np.array_equal(a[pay, :nk].view(np.uint64), out[:, :nk].view(np.uint64))
+
+
+@pytest.mark.parametrize("dist", ["pair_f64", "quartet_f64", "quartet_f64_dup"])
+def test_f64_record_types_default_params(dist):
+    for seed in (1, 2, 3):
+        et, a = W.make(dist, 1 << 15, seed)
+        _check_f64_records(et, a, oracle.sort(a))
+
+
+@pytest.mark.parametrize("dist", ["pair_f64", "quartet_f64_dup"])
+def test_f64_record_types_small_blocks_debug(dist):
+    """Block machinery (k_max=8, b=3, n0=2) with the three-zone invariant asserted."""
+    rng = np.random.default_rng(11)
+    for it in range(60):
+        n = int(rng.integers(2, 400))
+        et, a = W.make(dist, n, it)
+        if et == W.ELEM_PAIR_F64:
+            a[:, 0] = np.floor(a[:, 0] * 7) - 3.0 + 0.5        # 7 distinct nonzero keys
+        p = oracle.params(et, k_max=8, b=3, n0=2, debug=True)
+        st = oracle.Stats()
+        _check_f64_records(et, a, oracle.sort(a, p, st))
+
+
+def test_quartet_brute_force_permutations():
+    """All orderings of 6 quartets with ties in k0 and k1 (brute force, lexicographic)."""
+    base = np.array([[0.5, 0.25, 0.75, 0], [0.5, 0.25, 0.5, 1], [0.5, -0.5, 0.9, 2],
+                     [-1.0, 3.0, 0.1, 3], [0.5, 0.25, 0.75, 4], [2.0, -7.0, 0.3, 5]])
+    exp_keys = sorted(tuple(r[:3]) for r in base)
+    for perm in itertools.permutations(range(6)):
+        a = np.ascontiguousarray(base[list(perm)])
+        p = oracle.params(W.ELEM_QUARTET_F64, k_max=4, b=1, n0=1, debug=True)
+        out = oracle.sort(a, p)
+        assert [tuple(r[:3]) for r in out] == exp_keys
+
+
+def test_quartet_classify_linear_scan():
+    """Classification of quartets: the number of splitters <= e under the lexicographic order
+    (ties right) and equality buckets, by a linear scan over
+    Python tuples."""
+    rng = np.random.default_rng(5)
+    for eq in (False, True):
+        for it in range(20):
+            _, pool = W.make("quartet_f64_dup", 400, it)
+            tup = sorted({tuple(r[:3]) for r in pool})
+            nspl = int(rng.integers(1, 30 if eq else 60))
+            pick = sorted(rng.choice(len(tup), size=min(nspl, len(tup)), replace=False))
+            spl = np.array([list(tup[i]) + [0.0] for i in pick])
+            _, el = W.make("quartet_f64_dup", 500, 100 + it)
+            el[:50] = spl[rng.integers(0, len(spl), 50)]
+            got = oracle.classify(spl, eq, el)
+            st = [tuple(r[:3]) for r in spl]
+            kp = 2
+            while kp < len(st) + 1:
+                kp *= 2
+            st = st + [st[-1]] * (kp - 1 - len(st))   # padded with the largest splitter (SURVEY S6)
+            for e, g in zip(el, got):
+                k = tuple(e[:3])
+                i = sum(1 for s in st if s <= k)
+                if eq:
+                    i = 2 * i - (1 if i >= 1 and st[i - 1] == k else 0)
+                assert g == i

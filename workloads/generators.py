@@ -25,15 +25,17 @@ import math
 import numpy as np
 
 __all__ = [
-    "ELEM_U64", "ELEM_F64", "ELEM_PAIR", "ELEM_REC100", "ELEM_SIZE", "ELEM_NAMES",
+    "ELEM_U64", "ELEM_F64", "ELEM_PAIR", "ELEM_REC100", "ELEM_PAIR_F64", "ELEM_QUARTET_F64", "ELEM_SIZE",
+    "ELEM_NAMES", "pair_f64", "quartet_f64", "quartet_f64_dup",
     "u_stream", "u64_uniform", "f64_uniform", "f64_exponential", "root_dup",
     "two_dup", "eight_dup", "almost_sorted", "reverse_sorted", "sorted_seq", "zeros", "ones",
     "pair16", "rec100", "make", "DISTRIBUTIONS", "CONFIGS",
 ]
 
-ELEM_U64, ELEM_F64, ELEM_PAIR, ELEM_REC100 = 0, 1, 2, 3
-ELEM_SIZE = {ELEM_U64: 8, ELEM_F64: 8, ELEM_PAIR: 16, ELEM_REC100: 100}
-ELEM_NAMES = {ELEM_U64: "u64", ELEM_F64: "f64", ELEM_PAIR: "pair16", ELEM_REC100: "rec100"}
+ELEM_U64, ELEM_F64, ELEM_PAIR, ELEM_REC100, ELEM_PAIR_F64, ELEM_QUARTET_F64 = 0, 1, 2, 3, 4, 5
+ELEM_SIZE = {ELEM_U64: 8, ELEM_F64: 8, ELEM_PAIR: 16, ELEM_REC100: 100, ELEM_PAIR_F64: 16, ELEM_QUARTET_F64: 32}
+ELEM_NAMES = {ELEM_U64: "u64", ELEM_F64: "f64", ELEM_PAIR: "pair16", ELEM_REC100: "rec100",
+              ELEM_PAIR_F64: "pair_f64", ELEM_QUARTET_F64: "quartet_f64"}
 
 _GAMMA = np.uint64(0x9E3779B97F4A7C15)
 _M1 = np.uint64(0xBF58476D1CE4E5B9)
@@ -174,6 +176,39 @@ def rec100(n: int, seed: int) -> np.ndarray:
     return out
 
 
+def pair_f64(n: int, seed: int) -> np.ndarray:
+    """The paper's Pair: f64 key uniform [0,1) = (u(seed,i) >> 11) * 2^-53,
+    f64 payload = i (exact below 2^53).  float64[n,2]."""
+    out = np.empty((n, 2), dtype=np.float64)
+    out[:, 0] = f64_uniform(n, seed)
+    out[:, 1] = np.arange(n, dtype=np.float64)
+    return out
+
+
+def _f64_stream(seed: int, start: int, n: int) -> np.ndarray:
+    return (u_stream(seed, start, n) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+
+def quartet_f64(n: int, seed: int) -> np.ndarray:
+    """The paper's Quartet: three f64 keys, each uniform [0,1) from its own
+    stretch of the seed's stream (k_j = f64 rule at index j*n + i), compared
+    lexicographically; f64 payload = i.  float64[n,4]."""
+    out = np.empty((n, 4), dtype=np.float64)
+    for j in range(3):
+        out[:, j] = _f64_stream(seed + 2000, j * n, n)
+    out[:, 3] = np.arange(n, dtype=np.float64)
+    return out
+
+
+def quartet_f64_dup(n: int, seed: int) -> np.ndarray:
+    """Quartet with duplicate-heavy leading keys (test input for the lexicographic order):
+    k0 in 64 values, k1 in 16 values (both in [-0.5, 0.5), nonzero), k2 uniform [0,1)."""
+    out = quartet_f64(n, seed)
+    out[:, 0] = np.floor(out[:, 0] * 64.0) / 64.0 - 0.4921875
+    out[:, 1] = np.floor(out[:, 1] * 16.0) / 16.0 - 0.46875
+    return out
+
+
 DISTRIBUTIONS = {
     "uniform": (ELEM_U64, u64_uniform),
     "f64_uniform": (ELEM_F64, f64_uniform),
@@ -188,6 +223,9 @@ DISTRIBUTIONS = {
     "ones": (ELEM_U64, ones),
     "pair16": (ELEM_PAIR, pair16),
     "rec100": (ELEM_REC100, rec100),
+    "pair_f64": (ELEM_PAIR_F64, pair_f64),
+    "quartet_f64": (ELEM_QUARTET_F64, quartet_f64),
+    "quartet_f64_dup": (ELEM_QUARTET_F64, quartet_f64_dup),
 }
 
 # BASELINE.json configs (name -> (distribution, log2 n)); "H" is the headline.
