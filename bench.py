@@ -51,8 +51,11 @@ CONFIGS = {
     "F3_ones": ("ones", 27, "f3: 2^27 u64 all equal to 1 (PAPER.md:444 Ones)"),
     "C4": ("pair16", 27, "C4: 2^27 Pair16 (u64 key uniform [0,2^32), payload = index)"),
     "C5": ("rec100", 24, "C5: 2^24 100-byte records (10-byte key)"),
+    "F3_pair_f64": ("pair_f64", 27, "f3: 2^27 the paper's Pair (f64 key uniform [0,1) + f64 payload)"),
+    "F3_quartet": ("quartet_f64", 26, "f3: 2^26 the paper's Quartet (three f64 keys, lexicographic, + payload)"),
 }
-DTYPE = {W.ELEM_U64: "u64", W.ELEM_F64: "f64", W.ELEM_PAIR: "u64x2", W.ELEM_REC100: "u8x100"}
+DTYPE = {W.ELEM_U64: "u64", W.ELEM_F64: "f64", W.ELEM_PAIR: "u64x2", W.ELEM_REC100: "u8x100",
+         W.ELEM_PAIR_F64: "f64x2", W.ELEM_QUARTET_F64: "f64x4"}
 BW_NOMINAL = 8000.0  # GB/s, the north star's "roughly 8 TB/s"
 
 
@@ -180,7 +183,7 @@ def make_input(cfg: str, n_override: int | None = None):
 
 def host_to_device(a: np.ndarray, et: int):
     import torch
-    if et == W.ELEM_F64:
+    if et in (W.ELEM_F64, W.ELEM_PAIR_F64, W.ELEM_QUARTET_F64):
         return torch.from_numpy(a).cuda()
     if et in (W.ELEM_U64, W.ELEM_PAIR):
         return torch.from_numpy(a.view(np.int64)).cuda().view(torch.uint64)
@@ -243,6 +246,9 @@ def cpu_baseline(dist: str, log2: int, secs_target: float = 15.0):
         np.sort(np.ascontiguousarray(c).view("S100").ravel())
     elif et == W.ELEM_PAIR:
         np.sort(c.view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k"])
+    elif et in (W.ELEM_PAIR_F64, W.ELEM_QUARTET_F64):
+        nk = 1 if et == W.ELEM_PAIR_F64 else 3
+        c[np.lexsort(tuple(c[:, j] for j in reversed(range(nk))))]
     else:
         c.sort()
     t_lib = time.perf_counter() - t1
@@ -480,6 +486,12 @@ class OracleVerify:
         exp, a, et = self.res, self.a, self.et
         if et in (W.ELEM_U64, W.ELEM_F64):
             return bool(np.array_equal(got.view(np.uint64), exp.view(np.uint64)))
+        if et in (W.ELEM_PAIR_F64, W.ELEM_QUARTET_F64):
+            nk = 1 if et == W.ELEM_PAIR_F64 else 3
+            pay = got[:, nk].astype(np.int64)
+            return bool(np.array_equal(got[:, :nk].view(np.uint64), exp[:, :nk].view(np.uint64)) and
+                        np.array_equal(np.sort(pay), np.arange(a.shape[0])) and
+                        np.array_equal(a[pay, :nk].view(np.uint64), got[:, :nk].view(np.uint64)))
         if et == W.ELEM_PAIR:
             # (the Pair16 workload's payload is the original index)
             pay = got[:, 1]

@@ -20,6 +20,11 @@
  *                    the payload order inside a run of equal keys is unspecified.
  *   IPS4O_REC100_K10 100 B record; key = bytes [0,10) compared as unsigned bytes
  *                    (memcmp order); payload = bytes [10,100); unstable.
+ *   IPS4O_PAIR_F64   16 B {double key; double value}: the paper's Pair;
+ *                    ordered by the key (no NaN / -0.0 keys); unstable.
+ *   IPS4O_QUARTET_F64 32 B {double k0, k1, k2; double value}: the paper's Quartet
+ *                    (PAPER.md:447-449); keys compared lexicographically (no NaN / -0.0);
+ *                    unstable.  16-byte aligned.
  *
  * Conventions for every entry point:
  *   - Device pointers are CUDA device memory of the current device; the caller owns it.
@@ -52,13 +57,15 @@ typedef enum {
     IPS4O_U64 = 0,
     IPS4O_F64 = 1,
     IPS4O_PAIR_U64 = 2,
-    IPS4O_REC100_K10 = 3
+    IPS4O_REC100_K10 = 3,
+    IPS4O_PAIR_F64 = 4,
+    IPS4O_QUARTET_F64 = 5
 } ips4o_type;
 
 typedef enum {
     IPS4O_OK = 0,
     IPS4O_EINVAL = -1,   /* null pointer with n > 0, bad type, n >= 2^36, bad splitters */
-    IPS4O_EALIGN = -2,   /* data pointer not aligned to 8 B (u64/f64), 16 B (pair), 4 B (rec100) */
+    IPS4O_EALIGN = -2,   /* data pointer not aligned to 8 B (u64/f64), 16 B (pairs, quartets), 4 B (rec100) */
     IPS4O_ENOMEM = -3,   /* workspace allocation failed */
     IPS4O_ECUDA = -4,    /* CUDA launch/runtime error, see ips4o_error_string */
     IPS4O_EINTERNAL = -5 /* a device-side consistency check failed (conservation, capacity) */
@@ -149,7 +156,8 @@ const char* ips4o_kernel_kind_name(int kind);
 /* Classification of d_in[0..n) with GIVEN splitters:
  * h_splitters is HOST memory holding nspl strictly increasing keys in the element
  * type's key format (u64: uint64; f64: double; pair: uint64 key; rec100: the big-endian
- * uint64 of key bytes 0..7, the key part a distribution step classifies on).
+ * uint64 of key bytes 0..7, the key part a distribution step classifies on; pair_f64: double
+ * key; quartet_f64: double k0).
  * flags bit 0 enables equality buckets; bit 1 selects K2's production classifier (the
  * bucket-hint table, k2_bucket_keys_lut) instead of the tree descent (classify_key).
  * Writes the bucket index of every element to d_bucket_out (device, uint32[n]), using the

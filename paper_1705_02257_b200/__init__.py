@@ -17,8 +17,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # IPS4O_LIB may name an alternative build (tuning experiments, e.g. libips4o_bb256.so)
 LIB_PATH = os.environ.get("IPS4O_LIB") or os.path.join(_HERE, "libips4o.so")
 
-IPS4O_U64, IPS4O_F64, IPS4O_PAIR_U64, IPS4O_REC100_K10 = 0, 1, 2, 3
-ELEM_SIZE = {0: 8, 1: 8, 2: 16, 3: 100}
+IPS4O_U64, IPS4O_F64, IPS4O_PAIR_U64, IPS4O_REC100_K10, IPS4O_PAIR_F64, IPS4O_QUARTET_F64 = 0, 1, 2, 3, 4, 5
+ELEM_SIZE = {0: 8, 1: 8, 2: 16, 3: 100, 4: 16, 5: 32}
 NUM_KERNEL_KINDS = 8
 
 # every symbol include/ips4o.h declares
@@ -195,6 +195,10 @@ def elem_type_of(t) -> int:
         return IPS4O_PAIR_U64
     if t.dtype == torch.uint8 and t.dim() == 2 and t.shape[1] == 100:
         return IPS4O_REC100_K10
+    if t.dtype == torch.float64 and t.dim() == 2 and t.shape[1] == 2:
+        return IPS4O_PAIR_F64
+    if t.dtype == torch.float64 and t.dim() == 2 and t.shape[1] == 4:
+        return IPS4O_QUARTET_F64
     raise TypeError(f"unsupported tensor {t.dtype} {tuple(t.shape)}")
 
 
@@ -220,4 +224,6 @@ def splitters_buffer(splitters, elem_type: int):
         a = a.astype(np.float64)
     elif elem_type in (IPS4O_U64, IPS4O_PAIR_U64):
         a = a.astype(np.uint64)
+    elif elem_type in (IPS4O_PAIR_F64, IPS4O_QUARTET_F64):
+        a = a.astype(np.float64)
     return a, a.ctypes.data_as(ctypes.c_void_p), a.shape[0]

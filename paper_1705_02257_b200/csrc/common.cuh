@@ -58,9 +58,12 @@ constexpr int BLOCK_BYTES = IPS4O_BLOCK_BYTES;  // block b*s in bytes for the 8/
 // less(): the base-case order.  For PAIR it is (key, payload) lexicographic -- a valid
 // unstable order that also makes padding with the all-ones element harmless.
 
+// Trait flags: WIDE = elements are moved as 32-bit words by the record-style K2 (k_classify_wide);
+// F64KEY = key parts are IEEE doubles compared through the order-preserving image.
 struct TU64 {
     typedef u64 V;
     static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 0, PARTS = 1;
+    static constexpr bool WIDE = false, F64KEY = false;
     static constexpr u32 LEAF = 4096;  // target base-case size of the adaptive k
     static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX, C2MAX = IPS4O_CELL_C2MAX;  // largest leaves of base-case classes 0-2
     __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v; }
@@ -73,6 +76,7 @@ struct TU64 {
 struct TF64 {
     typedef u64 V;
     static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 1, PARTS = 1;
+    static constexpr bool WIDE = false, F64KEY = true;
     static constexpr u32 LEAF = 4096;
     static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX, C2MAX = IPS4O_CELL_C2MAX;
     __host__ __device__ __forceinline__ static u64 key(V v, u32 = 0) {
@@ -85,6 +89,7 @@ struct TF64 {
 struct TPair {
     typedef ulonglong2 V;
     static constexpr int S = 16, B = BLOCK_BYTES / 16, VEC = 1, CAP = 8192, TYPE = 2, PARTS = 1;
+    static constexpr bool WIDE = false, F64KEY = false;
     static constexpr u32 LEAF = 4096;
     static constexpr u32 C0MAX = 2048, C1MAX = 4096, C2MAX = IPS4O_CELL_C2MAX;
     __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v.x; }
@@ -103,7 +108,8 @@ struct Rec100 {
 };
 struct TRec {
     typedef Rec100 V;
-    static constexpr int S = 100, B = 4, VEC = 0, CAP = 1024, TYPE = 3, PARTS = 2;
+    static constexpr int S = 100, B = 4, VEC = 0, CAP = 1024, TYPE = 3, PARTS = 2, RW = 25;
+    static constexpr bool WIDE = true, F64KEY = false;
     static constexpr u32 LEAF = 512;
     static constexpr u32 C0MAX = 512, C1MAX = 1024, C2MAX = 1024;  // record leaves: base-case classes
     __device__ __forceinline__ static u64 hi_of(u32 w0, u32 w1) {
@@ -112,6 +118,57 @@ struct TRec {
     __device__ __forceinline__ static u64 lo_of(u32 w2) { return (u64)__byte_perm(w2, 0, 0x4401); }
     __device__ __forceinline__ static u64 key(const V& v, u32 part) {
         return part ? lo_of(v.w[2]) : hi_of(v.w[0], v.w[1]);
+    }
+    // key part from the record's words (K2 works on word copies)
+    __device__ __forceinline__ static u64 key_w(const u32* w, u32 part) { return part ? lo_of(w[2]) : hi_of(w[0], w[1]); }
+};
+
+// The paper's Pair: an f64 key and an f64 value, 16 B, ordered by the key
+// (through the order-preserving image; no NaN / -0.0), unstable.
+struct TPairF64 {
+    typedef ulonglong2 V;
+    static constexpr int S = 16, B = BLOCK_BYTES / 16, VEC = 1, CAP = 8192, TYPE = 4, PARTS = 1;
+    static constexpr bool WIDE = false, F64KEY = true;
+    static constexpr u32 LEAF = 4096;
+    static constexpr u32 C0MAX = 2048, C1MAX = 4096, C2MAX = IPS4O_CELL_C2MAX;
+    __device__ __forceinline__ static u64 key(V v, u32 = 0) { return TF64::key(v.x); }
+    __device__ __forceinline__ static bool less(V a, V b) {
+        const u64 ka = key(a), kb = key(b);
+        return ka < kb || (ka == kb && a.y < b.y);
+    }
+    __host__ __device__ __forceinline__ static V pad() { return make_ulonglong2(0x7FFFFFFFFFFFFFFFull, ~0ull); }
+};
+
+// The paper's Quartet: three f64 keys compared lexicographically and an f64 value
+// (PAPER.md:447-449), 32 B.  Like the records, a distribution step classifies on one key
+// part (the image of k_part); an equality bucket of part p is re-partitioned on part p+1;
+// the base case compares all three.
+struct Quad {
+    u64 w[4];
+};
+struct TQuad {
+    typedef Quad V;
+    static constexpr int S = 32, B = BLOCK_BYTES / 32, VEC = 0, CAP = 4096, TYPE = 5, PARTS = 3, RW = 8;
+    static constexpr bool WIDE = true, F64KEY = true;
+    static constexpr u32 LEAF = 2048;
+    static constexpr u32 C0MAX = 4096, C1MAX = 4096, C2MAX = 4096;  // one class: the merge-sort base case
+    __device__ __forceinline__ static u64 key(const V& v, u32 part) { return TF64::key(v.w[part]); }
+    __device__ __forceinline__ static u64 key_w(const u32* w, u32 part) {
+        return TF64::key(((u64)w[2 * part + 1] << 32) | w[2 * part]);
+    }
+    __device__ __forceinline__ static bool less(const V& a, const V& b) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const u64 x = TF64::key(a.w[i]), y = TF64::key(b.w[i]);
+            if (x != y) return x < y;
+        }
+        return a.w[3] < b.w[3];
+    }
+    __host__ __device__ __forceinline__ static V pad() {
+        Quad q;
+        q.w[0] = q.w[1] = q.w[2] = 0x7FFFFFFFFFFFFFFFull;  // key image ~0 (above every key)
+        q.w[3] = ~0ull;
+        return q;
     }
 };
 
@@ -355,6 +412,15 @@ struct BlockIO {
             const u32 w1 = __shfl_sync(0xffffffffu, r.w[0], 1);
             const u32 w2 = __shfl_sync(0xffffffffu, r.w[0], 2);
             return part ? TRec::lo_of(w2) : TRec::hi_of(w0, w1);
+        } else if constexpr (TR::S == 32) {
+            // key part p = words 2p, 2p+1 of element 0: lane p/2, words (2p)%4, (2p)%4+1
+            const u32 src = part >> 1, o = (part & 1u) * 2u;
+            const u32 w0 = __shfl_sync(0xffffffffu, o ? r.w[2] : r.w[0], src);
+            const u32 w1 = __shfl_sync(0xffffffffu, o ? r.w[3] : r.w[1], src);
+            u32 ww[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            ww[2 * part] = w0;
+            ww[2 * part + 1] = w1;
+            return TR::key_w(ww, part);
         } else {
             const u32 w0 = __shfl_sync(0xffffffffu, r.w[0], 0);
             const u32 w1 = __shfl_sync(0xffffffffu, r.w[1], 0);

@@ -149,7 +149,7 @@ struct Workspace {
     u32 k2_blocks = 0, k3_blocks = 0, k3t_blocks = 0, k4w_blocks = 0, k4c_blocks = 0;
     u32 cell_grid[5] = {0, 0, 0, 0, 0};
     int kernels_type = -1;
-    GraphCache graphs[4][2];     // [type][profile]
+    GraphCache graphs[6][2];     // [type][profile]
     u64 graphs_gen = 0;
     LevelArgs A;                 // static fields (workspace pointers, capacities)
 };
@@ -354,7 +354,7 @@ template <class TR> struct CellCfg {
 };
 template <class TR>
 struct MergeCfg {
-    static constexpr int TH = TR::CAP >= 16384 ? 1024 : 512;
+    static constexpr int TH = TR::CAP >= 16384 ? 1024 : TR::CAP >= 8192 ? 512 : 256;
     typedef BaseClass<TR, TH, 16> BC;
 };
 template <class TR, int NT, int E>
@@ -391,14 +391,21 @@ static int prepare_kernels(void) {
     const int nsm = g_ws.num_sms;
     int occ2 = 0, occ3 = 0, occ3t = 0;
     CK(cudaFuncSetAttribute(k_sample<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1_SMEM));
-    if constexpr (TR::S == 100) {
-        CK(cudaFuncSetAttribute(k_classify_rec<K2REC_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)K2RecSmem<K2REC_THREADS>::total));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_classify_rec<K2REC_THREADS>, K2REC_THREADS,
-                                                         K2RecSmem<K2REC_THREADS>::total));
-        CK(cudaFuncSetAttribute(k_base_rec<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase<2>::smem));
-        CK(cudaFuncSetAttribute(k_base_rec<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase<4>::smem));
-        g_ws.cell_grid[0] = g_ws.cell_grid[1] = 4u * nsm;
+    if constexpr (TR::WIDE) {
+        CK(cudaFuncSetAttribute(k_classify_rec<TR, K2REC_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)K2RecSmem<TR, K2REC_THREADS>::total));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_classify_rec<TR, K2REC_THREADS>, K2REC_THREADS,
+                                                         K2RecSmem<TR, K2REC_THREADS>::total));
+        if constexpr (TR::S == 100) {
+            CK(cudaFuncSetAttribute(k_base_rec<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase<2>::smem));
+            CK(cudaFuncSetAttribute(k_base_rec<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase<4>::smem));
+            g_ws.cell_grid[0] = g_ws.cell_grid[1] = 4u * nsm;
+        } else {
+            typedef MergeCfg<TR> M;
+            CK(cudaFuncSetAttribute(k_base_merge<TR, M::TH, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)M::BC::smem));
+            g_ws.cell_grid[4] = 2u * nsm;
+        }
     } else {
         typedef K2Cfg<TR> C;
         CK(cudaFuncSetAttribute(k_classify<TR, C::NT, C::E, C::MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -460,8 +467,9 @@ static int enqueue_level(Enq& q) {
     const u32 T = A.tcap;
     LAUNCH(KK_SAMPLE, (k_sample<TR><<<T, K1_THREADS, K1_SMEM, st>>>(A)));
     STAMP(KK_SAMPLE);
-    if constexpr (TR::S == 100) {
-        LAUNCH(KK_CLASSIFY, (k_classify_rec<K2REC_THREADS><<<g_ws.k2_blocks, K2REC_THREADS, K2RecSmem<K2REC_THREADS>::total, st>>>(A)));
+    if constexpr (TR::WIDE) {
+        LAUNCH(KK_CLASSIFY, (k_classify_rec<TR, K2REC_THREADS><<<g_ws.k2_blocks, K2REC_THREADS,
+                                                                 K2RecSmem<TR, K2REC_THREADS>::total, st>>>(A)));
     } else {
         typedef K2Cfg<TR> C;
         LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E, C::MINB><<<g_ws.k2_blocks, C::NT, K2Smem<TR, C::NT, C::E>::total, st>>>(A)));
@@ -506,6 +514,13 @@ static int enqueue_base(Enq& q) {
         STAMP(KK_BASE);
         LAUNCH(KK_BASE, (k_base_rec<4><<<g_ws.cell_grid[1], KREC_THREADS, RecBase<4>::smem, st>>>(
                              A.q_base + A.qb_off[1], A.ctr + CTR_BASE0 + 1, A.dyn, A.qb_cap[1])));
+        STAMP(KK_BASE);
+        return IPS4O_OK;
+    } else if constexpr (TR::WIDE) {
+        // quartets: one class, sorted by the merge sort (lexicographic order of three keys)
+        typedef MergeCfg<TR> M;
+        LAUNCH(KK_BASE, (k_base_merge<TR, M::TH, 16><<<g_ws.cell_grid[4], M::TH, M::BC::smem, st>>>(
+                             A.q_base + A.qb_off[0], 0u, A.ctr + CTR_BASE0 + 0, A.dyn, A.qb_cap[0])));
         STAMP(KK_BASE);
         return IPS4O_OK;
     } else {
@@ -703,6 +718,8 @@ static int type_size(int t) {
         case IPS4O_F64: return 8;
         case IPS4O_PAIR_U64: return 16;
         case IPS4O_REC100_K10: return 100;
+        case IPS4O_PAIR_F64: return 16;
+        case IPS4O_QUARTET_F64: return 32;
         default: return 0;
     }
 }
@@ -723,7 +740,9 @@ static int check_args(const void* p, u64 n, int type) {
         return IPS4O_EINVAL;
     }
     const uintptr_t a = (uintptr_t)p;
-    const int need = type == IPS4O_PAIR_U64 ? 16 : type == IPS4O_REC100_K10 ? 4 : 8;
+    const int need = (type == IPS4O_PAIR_U64 || type == IPS4O_PAIR_F64 || type == IPS4O_QUARTET_F64) ? 16
+                     : type == IPS4O_REC100_K10                                                   ? 4
+                                                                                                  : 8;
     if (n > 0 && (a % need)) {
         snprintf(g_errbuf, sizeof g_errbuf, "data pointer not %d-byte aligned", need);
         return IPS4O_EALIGN;
@@ -734,7 +753,7 @@ static int check_args(const void* p, u64 n, int type) {
 template <class TR>
 static int splitters_to_keys(const void* h, u32 nspl, std::vector<u64>& out) {
     out.resize(nspl);
-    if (TR::TYPE == 1) {
+    if (TR::F64KEY) {
         for (u32 i = 0; i < nspl; ++i) {
             u64 bits;
             memcpy(&bits, (const char*)h + 8 * i, 8);
@@ -885,6 +904,8 @@ static int sort_locked(void* d_data, uint64_t n, int elem_type, cudaStream_t st)
         case IPS4O_F64: rc = sort_impl<TF64>(d_data, n, st); break;
         case IPS4O_PAIR_U64: rc = sort_impl<TPair>(d_data, n, st); break;
         case IPS4O_REC100_K10: rc = sort_impl<TRec>(d_data, n, st); break;
+        case IPS4O_PAIR_F64: rc = sort_impl<TPairF64>(d_data, n, st); break;
+        case IPS4O_QUARTET_F64: rc = sort_impl<TQuad>(d_data, n, st); break;
         default: rc = IPS4O_EINVAL;
     }
     g_stats.has_device_stats = rc == IPS4O_OK ? 1u : 0u;
@@ -1003,6 +1024,8 @@ size_t ips4o_aux_bytes(uint64_t n, int elem_type) {
         case IPS4O_F64: c = caps_for<TF64>(n); break;
         case IPS4O_PAIR_U64: c = caps_for<TPair>(n); break;
         case IPS4O_REC100_K10: c = caps_for<TRec>(n); break;
+        case IPS4O_PAIR_F64: c = caps_for<TPairF64>(n); break;
+        case IPS4O_QUARTET_F64: c = caps_for<TQuad>(n); break;
         default: return 0;
     }
     return layout_of(c).total;
@@ -1094,6 +1117,8 @@ int ips4o_debug_classify(const void* d_in, uint64_t n, int elem_type, const void
         case IPS4O_F64: return debug_classify_impl<TF64>(d_in, n, h_splitters, nspl, flags, d_bucket_out, st);
         case IPS4O_PAIR_U64: return debug_classify_impl<TPair>(d_in, n, h_splitters, nspl, flags, d_bucket_out, st);
         case IPS4O_REC100_K10: return debug_classify_impl<TRec>(d_in, n, h_splitters, nspl, flags, d_bucket_out, st);
+        case IPS4O_PAIR_F64: return debug_classify_impl<TPairF64>(d_in, n, h_splitters, nspl, flags, d_bucket_out, st);
+        case IPS4O_QUARTET_F64: return debug_classify_impl<TQuad>(d_in, n, h_splitters, nspl, flags, d_bucket_out, st);
         default: return IPS4O_EINVAL;
     }
 }
@@ -1114,6 +1139,8 @@ int ips4o_debug_partition_once(void* d_data, uint64_t n, int elem_type, const vo
         case IPS4O_F64: rc = debug_partition_impl<TF64>(d_data, n, h_splitters, nspl, eq, (u64*)h_bounds_out, K_out, st); break;
         case IPS4O_PAIR_U64: rc = debug_partition_impl<TPair>(d_data, n, h_splitters, nspl, eq, (u64*)h_bounds_out, K_out, st); break;
         case IPS4O_REC100_K10: rc = debug_partition_impl<TRec>(d_data, n, h_splitters, nspl, eq, (u64*)h_bounds_out, K_out, st); break;
+        case IPS4O_PAIR_F64: rc = debug_partition_impl<TPairF64>(d_data, n, h_splitters, nspl, eq, (u64*)h_bounds_out, K_out, st); break;
+        case IPS4O_QUARTET_F64: rc = debug_partition_impl<TQuad>(d_data, n, h_splitters, nspl, eq, (u64*)h_bounds_out, K_out, st); break;
         default: rc = IPS4O_EINVAL;
     }
     g_stats.has_device_stats = rc == IPS4O_OK ? 1u : 0u;

@@ -430,6 +430,13 @@ template <> struct CellWork<TF64> {
     __device__ __forceinline__ static u64 in(u64 v) { return TF64::key(v); }
     __device__ __forceinline__ static u64 out(u64 k) { return (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k; }
 };
+template <> struct CellWork<TPairF64> {  // f64-key pairs: the key word as its image
+    typedef TPair T;
+    __device__ __forceinline__ static ulonglong2 in(ulonglong2 v) { return make_ulonglong2(TF64::key(v.x), v.y); }
+    __device__ __forceinline__ static ulonglong2 out(ulonglong2 k) {
+        return make_ulonglong2((k.x >> 63) ? (k.x & 0x7FFFFFFFFFFFFFFFull) : ~k.x, k.y);
+    }
+};
 
 template <class TR, int NT, int E>
 struct CellMinB {

@@ -1,11 +1,11 @@
-// k_classify_rec.cuh -- K2 for 100-byte records (local classification).
+// k_classify_rec.cuh -- K2 for wide elements moved as 32-bit words: the 100-byte records
+// and the 32-byte quartets (local classification).
 //
-// Same algorithm as k_classify.cuh with records: a tile of NT records is staged in shared
-// memory by coalesced 4-byte loads (records are only 4-byte aligned), each thread
-// classifies one record on the task's key part (branchless descent + ballot peers), the
-// record is copied into its bucket's 4-record buffer block (400 B), and full buffers are
-// written back to the consumed front of the stripe by warp-cooperative coalesced copies.
-// The block grid of a record task starts at lo (no 16-byte alignment requirement).
+// Same algorithm as k_classify.cuh: a tile of elements is staged in shared memory by a TMA
+// bulk copy (records are only 4-byte aligned: the < 16 bytes around the aligned body by
+// plain loads), each thread classifies its elements on the task's key part, the element's
+// words are copied into its bucket's buffer block (records: 4 x 100 B, quartets: 16 x 32 B),
+// and full buffers leave by TMA bulk stores into the consumed front of the stripe.
 #pragma once
 #include "common.cuh"
 #include "k_classify.cuh"
@@ -14,11 +14,11 @@ namespace ips4o {
 
 constexpr int K2REC_RPT = 2;  // records per thread and tile
 
-template <int NT>
+template <class TR, int NT>
 struct K2RecSmem {
     static constexpr int NW = NT / 32;
-    static constexpr size_t buf_bytes = (size_t)MAXK * TRec::B * 100;
-    static constexpr size_t stage_bytes = (size_t)NT * K2REC_RPT * 100 + 16;
+    static constexpr size_t buf_bytes = (size_t)MAXK * TR::B * TR::S;
+    static constexpr size_t stage_bytes = (size_t)NT * K2REC_RPT * TR::S + 16;
     static constexpr size_t wcnt_bytes = 0;
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
     static constexpr size_t arr_bytes = 5 * MAXK * 4;
@@ -28,18 +28,19 @@ struct K2RecSmem {
         buf_bytes + stage_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes + lut_bytes;
 };
 
+template <int RW>
 __device__ __forceinline__ void copy_rec(u32* dst, const u32* src) {
 #pragma unroll
-    for (int i = 0; i < 25; ++i) dst[i] = src[i];
+    for (int i = 0; i < RW; ++i) dst[i] = src[i];
 }
 
-template <int NT>
+template <class TR, int NT>
 __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A0) {
     const LevelArgs A = with_dyn(A0);
-    typedef K2RecSmem<NT> SM;
-    constexpr int B = TRec::B;     // records per block
+    typedef K2RecSmem<TR, NT> SM;
+    constexpr int B = TR::B;       // elements per block
     constexpr int NW = NT / 32;
-    constexpr u32 RW = 25;         // words per record
+    constexpr u32 RW = TR::RW;     // words per element
     extern __shared__ __align__(128) unsigned char smem[];
     u32* buf = reinterpret_cast<u32*>(smem);                                   // [256][B][25]
     u32* stage = reinterpret_cast<u32*>(smem + SM::buf_bytes);                 // [NT][25]
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A0) {
     u32* nbl = nfl + MAXK;
     constexpr int RPT = K2REC_RPT;
     constexpr int RS = RPT;  // record slots per thread
-    __shared__ u32 s_head[3 * 25], s_hb[3];
+    __shared__ u32 s_head[3 * RW], s_hb[3];
     __shared__ __align__(8) u64 s_mbar;
     u32 sphase = 0;
     if (threadIdx.x == 0) {
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A0) {
             // stage the tile: the 16-byte aligned body of its bytes by one TMA bulk copy
             // (mbarrier completion), the < 16 bytes before / after it by plain loads; record
             // r of the tile then starts at stage word dw + 25 r
-            const uintptr_t p0 = (uintptr_t)(gw + tb * RW), p1 = p0 + (uintptr_t)len * 100u;
+            const uintptr_t p0 = (uintptr_t)(gw + tb * RW), p1 = p0 + (uintptr_t)len * (u32)TR::S;
             const uintptr_t a0 = (p0 + 15) & ~(uintptr_t)15, a1 = p1 & ~(uintptr_t)15;
             const uintptr_t w0 = p0 & ~(uintptr_t)15;  // stage byte 0
             const u32 dw = (u32)((p0 - w0) / 4);
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A0) {
             for (int r = 0; r < RS; ++r) {
                 const u32* my = rec_ptr(r);
                 const bool ok = r < RPT ? tid + r * NT < len : (with_head && tid < nhead);
-                key[r] = ok ? (tp.part ? TRec::lo_of(my[2]) : TRec::hi_of(my[0], my[1])) : 0ull;
+                key[r] = ok ? TR::key_w(my, tp.part) : 0ull;
                 valid |= (ok ? 1u : 0u) << r;
             }
             u32 bk[RS], pos[RS];
@@ -176,9 +177,9 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A0) {
                 const u32 p = pos[r];
                 const u32 q = p / B, off = p % B, nf = nfl[b];
                 if (q == 0) {
-                    copy_rec(buf + (b * B + off) * RW, my);
+                    copy_rec<RW>(buf + (b * B + off) * RW, my);
                 } else if (q < nf) {
-                    copy_rec(gw + (mb + (u64)(slotb[b] + q) * B + off) * RW, my);
+                    copy_rec<RW>(gw + (mb + (u64)(slotb[b] + q) * B + off) * RW, my);
                 } else {
                     pos[r] = p - nf * B;
                     defer |= 1u << r;
@@ -198,14 +199,14 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A0) {
             __syncthreads();
 #pragma unroll
             for (int r = 0; r < RS; ++r)
-                if (defer & (1u << r)) copy_rec(buf + (bk[r] * B + pos[r]) * RW, rec_ptr(r));
+                if (defer & (1u << r)) copy_rec<RW>(buf + (bk[r] * B + pos[r]) * RW, rec_ptr(r));
             __syncthreads();
             if (tid == 0) fence_proxy_async_smem();  // generic reads of the stage before the next TMA write
         }
         // head records: classified now, spilled with the bucket's partial buffer
         if (tid < nhead) {
             const u32* my = s_head + tid * RW;
-            u64 hk[1] = {tp.part ? TRec::lo_of(my[2]) : TRec::hi_of(my[0], my[1])};
+            u64 hk[1] = {TR::key_w(my, tp.part)};
             s_hb[tid] = classify_key(hk[0], tree, spl, tp.logk, tp.kprime, tp.eq);  // (a partial warp)
         }
         __syncthreads();

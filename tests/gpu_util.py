@@ -84,6 +84,14 @@ def check_equal_to_oracle(et, inp, got, exp):
         ri = np.sort(inp.view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k", "v"])
         ro = np.sort(got.view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k", "v"])
         assert np.array_equal(ri, ro)
+    elif et in (W.ELEM_PAIR_F64, W.ELEM_QUARTET_F64):
+        # keys (1 or 3 doubles) bit-exact; the f64 payload is the original index: a permutation
+        # carrying its record's keys
+        nk = 1 if et == W.ELEM_PAIR_F64 else 3
+        assert np.array_equal(got[:, :nk].view(np.uint64), exp[:, :nk].view(np.uint64))
+        pay = got[:, nk].astype(np.int64)
+        assert np.array_equal(np.sort(pay), np.arange(inp.shape[0]))
+        assert np.array_equal(inp[pay, :nk].view(np.uint64), got[:, :nk].view(np.uint64))
     else:
         assert np.array_equal(got[:, :10], exp[:, :10])
         assert np.array_equal(np.sort(inp.view("S100").ravel()), np.sort(got.view("S100").ravel()))

@@ -32,7 +32,7 @@ torch = pytest.importorskip("torch")
 import oracle  # noqa: E402
 import paper_1705_02257_b200 as ips4o  # noqa: E402
 import workloads as W  # noqa: E402
-from gpu_util import to_dev, to_host  # noqa: E402
+from gpu_util import check_equal_to_oracle, to_dev, to_host  # noqa: E402
 
 # (distribution, log2 n, seed)
 FULL = [
@@ -47,6 +47,9 @@ FULL = [
     ("rec100", 24, 1),             # C5
     ("uniform", 23, 2), ("uniform", 24, 3), ("uniform", 25, 2),  # K1 8192-key sample, 2-stripe level-2 tasks
     ("f64_exponential", 25, 3),
+    ("pair_f64", 27, 1),           # f3: the paper's Pair (f64 key + payload)
+    ("quartet_f64", 26, 1),        # f3: the paper's Quartet (three f64 keys + payload)
+    ("quartet_f64_dup", 24, 1),    #     with duplicate-heavy leading keys
 ]
 IDS = [f"{d}-2^{e}-s{s}" for d, e, s in FULL]
 LOOKAHEAD = 2
@@ -129,5 +132,7 @@ def test_full_size_vs_oracle(ahead, i):
         assert np.array_equal(got.view(np.uint64), exp.view(np.uint64)), f"{dist} 2^{e}: differs from the oracle"
     elif et == W.ELEM_PAIR:
         _check_pair(a, got, exp)
-    else:
+    elif et == W.ELEM_REC100:
         _check_rec(got, exp)
+    else:
+        check_equal_to_oracle(et, a, got, exp)

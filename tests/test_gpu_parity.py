@@ -306,11 +306,22 @@ def test_sort_duplicates_vs_oracle(et, kind):
 
 @pytest.mark.parametrize("dist", ["rootdup", "twodup", "eightdup", "almostsorted", "reversesorted",
                                   "sorted", "zeros", "ones", "uniform", "f64_uniform", "f64_exponential",
-                                  "pair16", "rec100"])
+                                  "pair16", "rec100", "pair_f64", "quartet_f64", "quartet_f64_dup"])
 def test_distributions_vs_oracle(dist):
     for seed in (1, 2, 3):
         et, a = W.make(dist, (1 << 18) if dist == "rec100" else (1 << 21), seed)
         check_equal_to_oracle(et, a, _sort_gpu(a, et), oracle.sort(a))
+
+
+@pytest.mark.parametrize("dist", ["pair_f64", "quartet_f64", "quartet_f64_dup"])
+def test_f64_record_types_sizes_vs_oracle(dist):
+    """The paper's Pair and Quartet: sizes at every base-case boundary
+    (quartets: 4096 = capacity of the merge-sort base case), several levels, a ragged tail;
+    the duplicate-heavy quartets exercise equality buckets on key parts 0 and 1."""
+    for i, n in enumerate([2, 3, 17, 2048, 2049, 4096, 4097, 8192, 8193, 70_001, 1_000_003]):
+        et, a = W.make(dist, n, 300 + i)
+        check_equal_to_oracle(et, a, _sort_gpu(a, et), oracle.sort(a))
+        assert ips4o.ips4o_last_stats()["device_error"] == 0
 
 
 def test_config1_full_size_vs_oracle():
