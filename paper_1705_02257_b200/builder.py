@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libips4o.so")
 # experimental build variants (tuning only): name -> extra nvcc flags
-VARIANTS = {"cellE8": ["-DIPS4O_CELL_E=8"], "k3regs": ["-DIPS4O_K3_SLOTS=4"]}
+VARIANTS = {"cellE8": ["-DIPS4O_CELL_E=8"], "k3relaxed": ["-DIPS4O_K3_RELAXED=1"]}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

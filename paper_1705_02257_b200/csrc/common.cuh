@@ -498,6 +498,16 @@ __device__ __forceinline__ void red_add_release_u32(u32* p, u32 v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ u64 atom_add_release_u64(u64* p, u64 v) {
+    u64 old;
+    asm volatile("atom.release.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ u64 atom_add_acquire_u64(u64* p, u64 v) {
+    u64 old;
+    asm volatile("atom.acquire.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
+}
 __device__ __forceinline__ u32 atom_add_acquire_u32(u32* p, u32 v) {
     u32 old;
     asm volatile("atom.acquire.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");

@@ -18,6 +18,9 @@
 
 namespace ips4o {
 
+#ifndef IPS4O_K3_RELAXED  // 1: the pointer atomics without release / acquire semantics (measurement)
+#define IPS4O_K3_RELAXED 0
+#endif
 #ifndef IPS4O_K3_IDLE_NS  // back-off of a K3 warp whose chains all wait
 #define IPS4O_K3_IDLE_NS 32
 #endif
@@ -691,8 +694,15 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
                 } else {
                     pb = b;
                     K3_TL_EVENT(1);
-                    const u32 r0 = atomicAdd(ctl_readers(A.wr, t, pb), 1u);
-                    const u64 old = atomicAdd((unsigned long long*)ctl_wr(A.wr, t, pb), ~0ull + (u64)(r0 >> 31));
+                    // the reader announcement is ordered before the take by the
+                    // take's release semantics; a writer's claim (acquire) that observes this
+                    // take then also observes the announcement
+                    atomicAdd(ctl_readers(A.wr, t, pb), 1u);
+#if IPS4O_K3_RELAXED
+                    const u64 old = atomicAdd((unsigned long long*)ctl_wr(A.wr, t, pb), ~0ull);
+#else
+                    const u64 old = atom_add_release_u64(ctl_wr(A.wr, t, pb), ~0ull);
+#endif
                     const int ow = (int)(u32)(old >> 32), orr = (int)((u32)old - RBIAS);
                     if (orr < ow) {
                         atomicSub(ctl_readers(A.wr, t, pb), 1u);
@@ -707,7 +717,11 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
                 }
             } else if (st == CH_HELD) {
                 K3_TL_EVENT(0);
+#if IPS4O_K3_RELAXED
                 const u64 old = atomicAdd((unsigned long long*)ctl_wr(A.wr, t, dest), 1ull << 32);
+#else
+                const u64 old = atom_add_acquire_u64(ctl_wr(A.wr, t, dest), 1ull << 32);
+#endif
                 const int ow = (int)(u32)(old >> 32), orr = (int)((u32)old - RBIAS);
                 slot = (u32)ow;
                 if (ow <= orr) {
@@ -720,7 +734,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
                 }
                 progressed = true;
             }
-            if (st == CH_WAITW && *(volatile u32*)ctl_readers(A.wr, t, dest) == 0u) {
+            if (st == CH_WAITW && ld_acquire_u32(ctl_readers(A.wr, t, dest)) == 0u) {
                 // no reader left at the crossing: write into the empty block
                 // (past the task end: the overflow block).  (Never spin here:
                 // the reader may be a chain of this warp.)
@@ -741,7 +755,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
             if ((st == CH_TAKING || st == CH_SWAPPING) && mbar_test(mymbar, phase)) {
                 phase ^= 1u;
                 if (st == CH_TAKING) {
-                    atomicSub(ctl_readers(A.wr, t, pb), 1u);  // the block has been read
+                    red_add_release_u32(ctl_readers(A.wr, t, pb), ~0u);  // the block has been read (release)
                     dest = classify_buf(mybuf + xb * BB);
                     st = CH_HELD;
                 } else {
