@@ -114,7 +114,7 @@ def ips4o_sort_kv(keys_ptr: int, vals_ptr: int, n: int, key_type: int, stream: i
 
 def sort_kv_(keys, vals):
     """Sort CUDA tensors keys (torch.uint64 or torch.float64) and vals (any 8-byte dtype) by
-    key, in their own storage; unstable (see include/ips4o.h)."""
+    key, in place in their own storage (both 16-byte aligned); unstable (include/ips4o.h)."""
     import torch
     if not (keys.is_cuda and vals.is_cuda) or keys.shape != vals.shape or keys.dim() != 1:
         raise Ips4oError("sort_kv_ expects two 1-D CUDA tensors of the same length")

@@ -63,7 +63,7 @@ constexpr int BLOCK_BYTES = IPS4O_BLOCK_BYTES;  // block b*s in bytes for the 8/
 struct TU64 {
     typedef u64 V;
     static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 0, PARTS = 1;
-    static constexpr bool WIDE = false, F64KEY = false;
+    static constexpr bool WIDE = false, F64KEY = false, KV = false;
     static constexpr u32 LEAF = 4096;  // target base-case size of the adaptive k
     static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX, C2MAX = IPS4O_CELL_C2MAX;  // largest leaves of base-case classes 0-2
     __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v; }
@@ -76,7 +76,7 @@ struct TU64 {
 struct TF64 {
     typedef u64 V;
     static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 1, PARTS = 1;
-    static constexpr bool WIDE = false, F64KEY = true;
+    static constexpr bool WIDE = false, F64KEY = true, KV = false;
     static constexpr u32 LEAF = 4096;
     static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX, C2MAX = IPS4O_CELL_C2MAX;
     __host__ __device__ __forceinline__ static u64 key(V v, u32 = 0) {
@@ -89,7 +89,7 @@ struct TF64 {
 struct TPair {
     typedef ulonglong2 V;
     static constexpr int S = 16, B = BLOCK_BYTES / 16, VEC = 1, CAP = 8192, TYPE = 2, PARTS = 1;
-    static constexpr bool WIDE = false, F64KEY = false;
+    static constexpr bool WIDE = false, F64KEY = false, KV = false;
     static constexpr u32 LEAF = 4096;
     static constexpr u32 C0MAX = 2048, C1MAX = 4096, C2MAX = IPS4O_CELL_C2MAX;
     __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v.x; }
@@ -109,7 +109,7 @@ struct Rec100 {
 struct TRec {
     typedef Rec100 V;
     static constexpr int S = 100, B = 4, VEC = 0, CAP = 1024, TYPE = 3, PARTS = 2, RW = 25;
-    static constexpr bool WIDE = true, F64KEY = false;
+    static constexpr bool WIDE = true, F64KEY = false, KV = false;
     static constexpr u32 LEAF = 512;
     static constexpr u32 C0MAX = 512, C1MAX = 1024, C2MAX = 1024;  // record leaves: base-case classes
     __device__ __forceinline__ static u64 hi_of(u32 w0, u32 w1) {
@@ -128,7 +128,7 @@ struct TRec {
 struct TPairF64 {
     typedef ulonglong2 V;
     static constexpr int S = 16, B = BLOCK_BYTES / 16, VEC = 1, CAP = 8192, TYPE = 4, PARTS = 1;
-    static constexpr bool WIDE = false, F64KEY = true;
+    static constexpr bool WIDE = false, F64KEY = true, KV = false;
     static constexpr u32 LEAF = 4096;
     static constexpr u32 C0MAX = 2048, C1MAX = 4096, C2MAX = IPS4O_CELL_C2MAX;
     __device__ __forceinline__ static u64 key(V v, u32 = 0) { return TF64::key(v.x); }
@@ -149,7 +149,7 @@ struct Quad {
 struct TQuad {
     typedef Quad V;
     static constexpr int S = 32, B = BLOCK_BYTES / 32, VEC = 0, CAP = 4096, TYPE = 5, PARTS = 3, RW = 8;
-    static constexpr bool WIDE = true, F64KEY = true;
+    static constexpr bool WIDE = true, F64KEY = true, KV = false;
     static constexpr u32 LEAF = 2048;
     static constexpr u32 C0MAX = 4096, C1MAX = 4096, C2MAX = 4096;  // one class: the merge-sort base case
     __device__ __forceinline__ static u64 key(const V& v, u32 part) { return TF64::key(v.w[part]); }
@@ -171,6 +171,37 @@ struct TQuad {
         return q;
     }
 };
+
+// Structure-of-arrays key-value elements (ips4o_sort_kv): keys (u64, or f64 through the
+// order-preserving image) in one array, u64 values in another, moved together.  In registers,
+// shared memory and the spill an element is the pair {key, value}; in global memory a block
+// of B elements is a key block (B*8 bytes) in the key array and a value block in the value
+// array.  Both arrays must be 16-byte aligned (TMA).
+struct TKV {
+    typedef ulonglong2 V;
+    static constexpr int S = 16, B = BLOCK_BYTES / 16, VEC = 1, CAP = 8192, TYPE = 6, PARTS = 1;
+    static constexpr bool WIDE = false, F64KEY = false, KV = true;
+    static constexpr u32 LEAF = 4096;
+    static constexpr u32 C0MAX = 2048, C1MAX = 4096, C2MAX = IPS4O_CELL_C2MAX;
+    __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v.x; }
+    __device__ __forceinline__ static bool less(V a, V b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
+    __host__ __device__ __forceinline__ static V pad() { return make_ulonglong2(~0ull, ~0ull); }
+};
+struct TKVF64 {
+    typedef ulonglong2 V;
+    static constexpr int S = 16, B = BLOCK_BYTES / 16, VEC = 1, CAP = 8192, TYPE = 7, PARTS = 1;
+    static constexpr bool WIDE = false, F64KEY = true, KV = true;
+    static constexpr u32 LEAF = 4096;
+    static constexpr u32 C0MAX = 2048, C1MAX = 4096, C2MAX = IPS4O_CELL_C2MAX;
+    __device__ __forceinline__ static u64 key(V v, u32 = 0) { return TF64::key(v.x); }
+    __device__ __forceinline__ static bool less(V a, V b) {
+        const u64 ka = key(a), kb = key(b);
+        return ka < kb || (ka == kb && a.y < b.y);
+    }
+    __host__ __device__ __forceinline__ static V pad() { return make_ulonglong2(0x7FFFFFFFFFFFFFFFull, ~0ull); }
+};
+// bytes per element index in the (first) data array: the block grid's 16-byte alignment
+template <class TR> struct GridStride { static constexpr int v = TR::KV ? 8 : TR::S; };
 
 // ------------------------------------------------------------- level descriptors
 
@@ -234,7 +265,8 @@ enum { ERR_SPILL = 1, ERR_CONSERVE = 2, ERR_QUEUE = 4, ERR_CAPACITY = 8, ERR_PRO
 // whole level loop can run inside one CUDA graph (asynchronous on the
 // caller's stream, no host synchronisation inside the sort).
 struct LevelDyn {
-    void* data;           // the array being sorted (element 0 of the call)
+    void* data;           // the array being sorted (element 0 of the call); KV types: the keys
+    void* vals;           // KV types: the values (else unused)
     u64 n;
     TaskDesc* q_next;     // next-level queue K4 appends to (ctr[CTR_NEXT] entries)
     u64 seed;             // this batch's sampling seed
@@ -268,6 +300,7 @@ enum {
 
 struct LevelArgs {
     void* data;       // (from dyn)
+    void* vals;       // (from dyn) KV types: the value array
     const TaskParam* tp;
     u32 ntasks;       // (from dyn)
     const StripeDesc* sd;
@@ -327,6 +360,7 @@ __device__ __forceinline__ LevelArgs with_dyn(const LevelArgs& A0) {
     LevelArgs A = A0;
     const LevelDyn* D = A0.dyn;
     A.data = D->data;
+    A.vals = D->vals;
     A.ntasks = D->ntasks;
     A.nstripes = D->nstripes;
     A.emit = (int)D->emit;
@@ -334,6 +368,31 @@ __device__ __forceinline__ LevelArgs with_dyn(const LevelArgs& A0) {
     A.q_next = D->q_next;
     return A;
 }
+
+// Element access to the sorted array(s): one array of V, or (KV types) a key array and a
+// value array addressed with the same element index.
+template <class TR, bool KV = TR::KV>
+struct Mem {
+    typedef typename TR::V V;
+    V* d;
+    __device__ __forceinline__ Mem(void* data, void*) : d(reinterpret_cast<V*>(data)) {}
+    __device__ __forceinline__ V ld(u64 i) const { return d[i]; }
+    __device__ __forceinline__ void st(u64 i, const V& x) const { d[i] = x; }
+    __device__ __forceinline__ u64 key(u64 i, u32 part) const { return TR::key(d[i], part); }
+};
+template <class TR>
+struct Mem<TR, true> {
+    typedef typename TR::V V;
+    u64* k;
+    u64* v;
+    __device__ __forceinline__ Mem(void* keys, void* vals) : k(reinterpret_cast<u64*>(keys)), v(reinterpret_cast<u64*>(vals)) {}
+    __device__ __forceinline__ V ld(u64 i) const { return make_ulonglong2(k[i], v[i]); }
+    __device__ __forceinline__ void st(u64 i, const V& x) const {
+        k[i] = x.x;
+        v[i] = x.y;
+    }
+    __device__ __forceinline__ u64 key(u64 i, u32) const { return TR::key(make_ulonglong2(k[i], 0ull), 0); }
+};
 
 // ---------------------------------------------------------------- device helpers
 
@@ -464,6 +523,18 @@ __device__ __forceinline__ void mbar_wait(u64* mbar, u32 parity) {
     asm volatile("{\n\t.reg .pred p;\n\t"
                  "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
                  "@!p bra W;\n\t}" ::"r"(mb), "r"(parity)
+                 : "memory");
+}
+// several bulk copies completing on one mbarrier: one arrive with the total byte count, then
+// copies without arrive
+__device__ __forceinline__ void mbar_expect_tx(u64* mbar, u32 bytes) {
+    const u32 mb = (u32)__cvta_generic_to_shared(mbar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_tx(void* sdst, const void* gsrc, u32 bytes, u64* mbar) {
+    const u32 mb = (u32)__cvta_generic_to_shared(mbar), sd = (u32)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(sd), "l"(gsrc), "r"(bytes), "r"(mb)
                  : "memory");
 }
 // TMA bulk prefetch of [src, src+bytes) into L2 (16-byte aligned, multiple of 16)

@@ -149,7 +149,7 @@ struct Workspace {
     u32 k2_blocks = 0, k3_blocks = 0, k3t_blocks = 0, k4w_blocks = 0, k4c_blocks = 0;
     u32 cell_grid[5] = {0, 0, 0, 0, 0};
     int kernels_type = -1;
-    GraphCache graphs[6][2];     // [type][profile]
+    GraphCache graphs[8][2];     // [type][profile]
     u64 graphs_gen = 0;
     LevelArgs A;                 // static fields (workspace pointers, capacities)
 };
@@ -421,7 +421,8 @@ static int prepare_kernels(void) {
                                 (int)M::BC::smem));
         g_ws.cell_grid[4] = 2u * nsm;
     }
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_permute<TR>, K3_THREADS, 0));
+    if constexpr (!TR::KV) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_permute<TR>, K3_THREADS, 0));
+    else occ3 = 1;
     CK(cudaFuncSetAttribute(k_permute_tma<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3TSmem<TR>::total));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3t, k_permute_tma<TR>, K3T_THREADS, K3TSmem<TR>::total));
     if (occ2 < 1 || occ3 < 1 || occ3t < 1) {
@@ -479,10 +480,15 @@ static int enqueue_level(Enq& q) {
     STAMP(KK_PREPARE);
     LAUNCH(KK_MOVES, (k_moves<TR><<<2 * g_ws.num_sms, 256, 0, st>>>(A)));
     STAMP(KK_MOVES);
-    if (k3_variant() == 0)
-        LAUNCH(KK_PERMUTE, (k_permute_tma<TR><<<g_ws.k3t_blocks, K3T_THREADS, K3TSmem<TR>::total, st>>>(A)));
-    else
-        LAUNCH(KK_PERMUTE, (k_permute<TR><<<g_ws.k3_blocks, K3_THREADS, 0, st>>>(A)));
+    if constexpr (!TR::KV) {
+        if (k3_variant() == 1) {
+            LAUNCH(KK_PERMUTE, (k_permute<TR><<<g_ws.k3_blocks, K3_THREADS, 0, st>>>(A)));
+            STAMP(KK_PERMUTE);
+            goto k3_done;
+        }
+    }
+    LAUNCH(KK_PERMUTE, (k_permute_tma<TR><<<g_ws.k3t_blocks, K3T_THREADS, K3TSmem<TR>::total, st>>>(A)));
+k3_done:
     STAMP(KK_PERMUTE);
     LAUNCH(KK_CLEANUP, (k_cleanup<TR><<<g_ws.k4w_blocks, K4_THREADS, 0, st>>>(A)));
     LAUNCH(KK_CLEANUP, (k_cleanup_cta<TR><<<g_ws.k4c_blocks, K4_THREADS, 0, st>>>(A)));
@@ -661,7 +667,7 @@ static int run_eager(cudaStream_t st) {
 }
 
 template <class TR>
-static int sort_impl(void* data, u64 n, cudaStream_t st) {
+static int sort_impl(void* data, u64 n, cudaStream_t st, void* vals = nullptr) {
     int rc = ensure_ws<TR>(n);
     if (rc) return rc;
     rc = prepare_kernels<TR>();
@@ -675,7 +681,7 @@ static int sort_impl(void* data, u64 n, cudaStream_t st) {
     if (!capturing && g_ws.have_done && !g_ws.last_captured && g_ws.last_stream != st)
         CK(cudaStreamWaitEvent(st, g_ws.ev_done, 0));
     const u32 small = n <= (u64)TR::CAP ? base_class<TR>(n) : (u32)NUM_BASE_CLASSES;
-    k_init<<<1, 32, 0, st>>>(g_ws.A, data, n, 0x1234567ull, small);
+    k_init<<<1, 32, 0, st>>>(g_ws.A, data, vals, n, 0x1234567ull, small);
     CK(cudaGetLastError());
     g_stats.host_syncs = 0;
     if (!capturing && eager_mode()) {
@@ -912,27 +918,12 @@ static int sort_locked(void* d_data, uint64_t n, int elem_type, cudaStream_t st)
     return rc;
 }
 
-// SoA <-> staging records {key image, value}; f64 keys through the order-preserving map
-// (and back: the map is a bijection on the non-NaN, non -0.0 doubles)
-__global__ void k_kv_gather(const u64* keys, const u64* vals, ulonglong2* out, u64 n, int f64) {
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        const u64 k = keys[i];
-        out[i] = make_ulonglong2(f64 ? TF64::key(k) : k, vals[i]);
-    }
-}
-__global__ void k_kv_scatter(const ulonglong2* in, u64* keys, u64* vals, u64 n, int f64) {
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        const ulonglong2 p = in[i];
-        keys[i] = f64 ? ((p.x >> 63) ? (p.x & 0x7FFFFFFFFFFFFFFFull) : ~p.x) : p.x;
-        vals[i] = p.y;
-    }
-}
 struct Staging {
     void* p = nullptr;
     size_t bytes = 0;
     int dev = -1;
 };
-static Staging g_stage_host, g_stage_kv;
+static Staging g_stage_host;
 static int stage_alloc(Staging& s, size_t bytes) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -994,27 +985,23 @@ int ips4o_sort_kv(uint64_t* d_keys, uint64_t* d_vals, uint64_t n, int key_type, 
         snprintf(g_errbuf, sizeof g_errbuf, "sort_kv: null pointer");
         return IPS4O_EINVAL;
     }
-    if (n >= N_LIMIT) return IPS4O_EINVAL;
-    if ((((uintptr_t)d_keys) | ((uintptr_t)d_vals)) & 7u) return IPS4O_EALIGN;
-    if (n <= 1) return IPS4O_OK;
-    std::lock_guard<std::mutex> lk(g_mu);  // held across gather, sort and scatter
-    cudaStream_t st = (cudaStream_t)stream;
-    int rc = stage_alloc(g_stage_kv, (size_t)n * 16);
-    if (rc) return rc;
-    if (g_ws.have_done) CK(cudaStreamWaitEvent(st, g_ws.ev_done, 0));
-    const u32 grid = (u32)std::min<u64>((n + 255) / 256, 4096);
-    k_kv_gather<<<grid, 256, 0, st>>>((const u64*)d_keys, (const u64*)d_vals, (ulonglong2*)g_stage_kv.p, n,
-                                     key_type == IPS4O_F64);
-    CK(cudaGetLastError());
-    rc = sort_locked(g_stage_kv.p, n, IPS4O_PAIR_U64, st);
-    if (rc) return rc;
-    k_kv_scatter<<<grid, 256, 0, st>>>((const ulonglong2*)g_stage_kv.p, (u64*)d_keys, (u64*)d_vals, n,
-                                      key_type == IPS4O_F64);
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(g_ws.ev_done, st));
+    if (n >= N_LIMIT) {
+        snprintf(g_errbuf, sizeof g_errbuf, "sort_kv: n too large (limit 2^36)");
+        return IPS4O_EINVAL;
+    }
+    if (n > 0 && ((((uintptr_t)d_keys) | ((uintptr_t)d_vals)) & 15u)) {
+        snprintf(g_errbuf, sizeof g_errbuf, "sort_kv: keys and values must be 16-byte aligned");
+        return IPS4O_EALIGN;
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    memset(&g_stats, 0, sizeof g_stats);
+    g_stats.n = n;
     g_stats.elem_type = (uint32_t)key_type;
-    g_stats.staging_bytes = (size_t)n * 16;
-    return IPS4O_OK;
+    if (n <= 1) return IPS4O_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int rc = key_type == IPS4O_F64 ? sort_impl<TKVF64>(d_keys, n, st, d_vals) : sort_impl<TKV>(d_keys, n, st, d_vals);
+    g_stats.has_device_stats = rc == IPS4O_OK ? 1u : 0u;
+    return rc;
 }
 
 size_t ips4o_aux_bytes(uint64_t n, int elem_type) {
@@ -1057,7 +1044,6 @@ const char* ips4o_error_string(int status) {
 int ips4o_release_workspace(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (g_ws.have_done) cudaEventSynchronize(g_ws.ev_done);
-    stage_free(g_stage_kv);
     stage_free(g_stage_host);
     release_all();
     return IPS4O_OK;

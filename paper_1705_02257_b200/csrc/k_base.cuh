@@ -113,22 +113,20 @@ template <class TR, int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS) k_base_merge(const TaskDesc* tasks, u32 start, const u32* d_ntasks,
                                                          const LevelDyn* dyn, u32 cap) {
     const u32 ntasks = min(*d_ntasks, cap);  // tasks [start, ntasks) (the count lives on the device)
-    void* vdata = dyn->data;
     typedef typename TR::V V;
     extern __shared__ __align__(16) unsigned char smem5[];
     V* s = reinterpret_cast<V*>(smem5);
-    V* data = reinterpret_cast<V*>(vdata);
+    const Mem<TR> mem(dyn->data, dyn->vals);
     const u32 tid = threadIdx.x;
     for (u32 ti = start + blockIdx.x; ti < ntasks; ti += gridDim.x) {
         const TaskDesc td = tasks[ti];
         const u32 n = (u32)(td.hi - td.lo);
         const u32 n16 = (n + ITEMS - 1) / ITEMS * ITEMS;
-        V* g = data + td.lo;
         // coalesced load; the last thread's items past n are padding
-        for (u32 i = tid; i < n16; i += THREADS) s[padidx(i)] = i < n ? g[i] : TR::pad();
+        for (u32 i = tid; i < n16; i += THREADS) s[padidx(i)] = i < n ? mem.ld(td.lo + i) : TR::pad();
         __syncthreads();
         block_sort_smem<TR, THREADS, ITEMS>(s, n);
-        for (u32 i = tid; i < n; i += THREADS) g[i] = s[padidx(i)];
+        for (u32 i = tid; i < n; i += THREADS) mem.st(td.lo + i, s[padidx(i)]);
         __syncthreads();
     }
 }
@@ -437,6 +435,12 @@ template <> struct CellWork<TPairF64> {  // f64-key pairs: the key word as its i
         return make_ulonglong2((k.x >> 63) ? (k.x & 0x7FFFFFFFFFFFFFFFull) : ~k.x, k.y);
     }
 };
+template <> struct CellWork<TKV> {  // key-value pairs: sorted as {key, value} pairs
+    typedef TPair T;
+    __device__ __forceinline__ static ulonglong2 in(ulonglong2 v) { return v; }
+    __device__ __forceinline__ static ulonglong2 out(ulonglong2 v) { return v; }
+};
+template <> struct CellWork<TKVF64> : CellWork<TPairF64> {};
 
 template <class TR, int NT, int E>
 struct CellMinB {
@@ -486,7 +490,8 @@ __global__ void __launch_bounds__(NT, (CellMinB<TR, NT, E>::v))
     __shared__ u64 s_r64[2];      // exact 64-bit range (leaves whose high halves are close)
     __shared__ u32 s_flag, s_wsum[NW], s_next[2];
     const u32 ntasks = min(*d_ntasks, qcap);  // (the count lives on the device: the grid is fixed)
-    V* data = reinterpret_cast<V*>(dyn->data);
+    const Mem<TR> mem(dyn->data, dyn->vals);
+    V* data = reinterpret_cast<V*>(dyn->data);  // (AoS types: the leaf's TMA write-back)
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     uint4* myrun = reinterpret_cast<uint4*>(cnt + cpad<E>(tid * E));  // this thread's E counters
     BASE_PROF_INIT();
@@ -500,7 +505,7 @@ __global__ void __launch_bounds__(NT, (CellMinB<TR, NT, E>::v))
         V* g = data + td.lo;
         // the leaf in shared memory starts at the same offset modulo 16 bytes as in global
         // memory, so that its aligned body leaves by one TMA bulk store
-        const u32 p = sizeof(V) == 8 ? (u32)((reinterpret_cast<uintptr_t>(g) >> 3) & 1u) : 0u;
+        const u32 p = (sizeof(V) == 8 && !TR::KV) ? (u32)((reinterpret_cast<uintptr_t>(g) >> 3) & 1u) : 0u;
         V* const X = X0 + p;
         const u32 ncell = n > 1 ? n : 1u;  // one cell per element (n <= the tile)
         if (tid == 0) {
@@ -523,7 +528,7 @@ __global__ void __launch_bounds__(NT, (CellMinB<TR, NT, E>::v))
 #pragma unroll
         for (int j = 0; j < E; ++j) {
             const u32 idx = min((u32)(j * NT) + tid, n - 1u);
-            v[j] = CellWork<TR>::in(g[idx]);
+            v[j] = CellWork<TR>::in(mem.ld(td.lo + idx));
             const u32 h = (u32)(TW::key(v[j]) >> 32);
             hmin = min(hmin, h);
             hmax = max(hmax, h);
@@ -541,9 +546,18 @@ __global__ void __launch_bounds__(NT, (CellMinB<TR, NT, E>::v))
         const u32 nxt = s_next[par];
         if (tid == 0 && nxt < ntasks) {
             const TaskDesc tn = tasks[nxt];
-            const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + tn.lo) & ~(uintptr_t)15;
-            const uintptr_t a1 = (reinterpret_cast<uintptr_t>(data + tn.hi) + 15) & ~(uintptr_t)15;
-            if (a1 > a0) bulk_prefetch_l2(reinterpret_cast<const void*>(a0), (u32)(a1 - a0));
+            if constexpr (TR::KV) {
+                for (int h = 0; h < 2; ++h) {
+                    const u64* arr = h ? mem.v : mem.k;
+                    const uintptr_t a0 = reinterpret_cast<uintptr_t>(arr + tn.lo) & ~(uintptr_t)15;
+                    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(arr + tn.hi) + 15) & ~(uintptr_t)15;
+                    if (a1 > a0) bulk_prefetch_l2(reinterpret_cast<const void*>(a0), (u32)(a1 - a0));
+                }
+            } else {
+                const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + tn.lo) & ~(uintptr_t)15;
+                const uintptr_t a1 = (reinterpret_cast<uintptr_t>(data + tn.hi) + 15) & ~(uintptr_t)15;
+                if (a1 > a0) bulk_prefetch_l2(reinterpret_cast<const void*>(a0), (u32)(a1 - a0));
+            }
         }
         // the key range: from the high halves when they are far apart (a conservative range
         // at most (d+1)/(d-1) wider than the exact one for d = hmax - hmin >= 16); exact from
@@ -752,6 +766,14 @@ __global__ void __launch_bounds__(NT, (CellMinB<TR, NT, E>::v))
                     X[q] = x;
                 }
             }
+        }
+        if constexpr (TR::KV) {
+            // 5. write back: key and value arrays by coalesced stores
+            __syncthreads();
+            for (u32 i = tid; i < n; i += NT) mem.st(td.lo + i, CellWork<TR>::out(X[i]));
+            cur = nxt;
+            par ^= 1u;
+            continue;
         }
         if constexpr (!std::is_same<TW, TR>::value) {
             __syncthreads();

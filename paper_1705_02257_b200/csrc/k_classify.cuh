@@ -41,12 +41,25 @@ struct K2Smem {
 // registers are only consumed when the tile is processed, so the loads of the next tile
 // stay in flight while the current one is classified.
 template <class TR, int NT, int E>
-__device__ __forceinline__ u32 k2_load(const typename TR::V* __restrict__ data, u64 tb, u32 len,
-                                       uint4 (&raw)[E / TR::VEC]) {
+__device__ __forceinline__ u32 k2_load(const Mem<TR>& mem, u64 tb, u32 len, uint4 (&raw)[E / TR::VEC]) {
     typedef typename TR::V V;
     constexpr int VEC = TR::VEC, NV = E / VEC;
     const u32 tid = threadIdx.x;
     u32 valid = 0;
+    if constexpr (TR::KV) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const u32 e0 = (u32)(i * NT + tid);
+            V x = TR::pad();
+            if (e0 < len) {
+                x = mem.ld(tb + e0);
+                valid |= 1u << i;
+            }
+            memcpy(&raw[i], &x, 16);
+        }
+        return valid;
+    } else {
+    const V* data = mem.d;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         const u32 e0 = (u32)(i * NT + tid) * VEC;
@@ -68,14 +81,73 @@ __device__ __forceinline__ u32 k2_load(const typename TR::V* __restrict__ data, 
         }
     }
     return valid;
+    }
 }
 
+// A tile of NT*E elements from element idx into a shared-memory stage by TMA bulk copies
+// completing on mbar (KV: the key tile, then the value tile).
 template <class TR, int NT, int E>
-__device__ __forceinline__ void k2_load_full(const typename TR::V* __restrict__ data, u64 tb,
-                                             uint4 (&raw)[E / TR::VEC]) {
-#pragma unroll
-    for (int i = 0; i < E / TR::VEC; ++i) raw[i] = ld_nc_v4(data + tb + (u64)(i * NT + threadIdx.x) * TR::VEC);
+__device__ __forceinline__ void k2_stage_load(typename TR::V* stage, const Mem<TR>& mem, u64 idx, u64* mbar) {
+    constexpr u32 TILE = NT * E;
+    if constexpr (TR::KV) {
+        u64* sk = reinterpret_cast<u64*>(stage);
+        mbar_expect_tx(mbar, TILE * 16u);
+        bulk_g2s_tx(sk, mem.k + idx, TILE * 8u, mbar);
+        bulk_g2s_tx(sk + TILE, mem.v + idx, TILE * 8u, mbar);
+    } else {
+        bulk_g2s(stage, mem.d + idx, TILE * (u32)sizeof(typename TR::V), mbar);
+    }
 }
+// this thread's elements (i*NT + tid) of a staged tile, as raw 16-byte registers
+template <class TR, int NT, int E>
+__device__ __forceinline__ void k2_stage_read(const typename TR::V* stage, uint4 (&raw)[E / TR::VEC]) {
+    if constexpr (TR::KV) {
+        const u64* sk = reinterpret_cast<const u64*>(stage);
+        const u64* sv = sk + NT * E;
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const u64 k = sk[i * NT + threadIdx.x], v = sv[i * NT + threadIdx.x];
+            raw[i] = make_uint4((u32)k, (u32)(k >> 32), (u32)v, (u32)(v >> 32));
+        }
+    } else {
+        const uint4* sp = reinterpret_cast<const uint4*>(stage);
+#pragma unroll
+        for (int i = 0; i < E / TR::VEC; ++i) raw[i] = sp[i * NT + threadIdx.x];
+    }
+}
+// K2's shared-memory bucket buffers: K*B element slots (KV: a key half and a value half, so
+// that a full block leaves as one key block and one value block)
+template <class TR>
+struct K2Buf {
+    typedef typename TR::V V;
+    __device__ __forceinline__ static void put(V* buf, u32 idx, const V& v) {
+        if constexpr (TR::KV) {
+            u64* b = reinterpret_cast<u64*>(buf);
+            b[idx] = v.x;
+            b[(u32)MAXK * TR::B + idx] = v.y;
+        } else {
+            buf[idx] = v;
+        }
+    }
+    __device__ __forceinline__ static V get(const V* buf, u32 idx) {
+        if constexpr (TR::KV) {
+            const u64* b = reinterpret_cast<const u64*>(buf);
+            return make_ulonglong2(b[idx], b[(u32)MAXK * TR::B + idx]);
+        } else {
+            return buf[idx];
+        }
+    }
+    // block of bucket b to element gidx by TMA bulk stores (bulk-group completion)
+    __device__ __forceinline__ static void flush(const Mem<TR>& mem, u64 gidx, V* buf, u32 b) {
+        if constexpr (TR::KV) {
+            u64* bk = reinterpret_cast<u64*>(buf);
+            bulk_s2g(mem.k + gidx, bk + b * TR::B, TR::B * 8u);
+            bulk_s2g(mem.v + gidx, bk + (u32)MAXK * TR::B + b * TR::B, TR::B * 8u);
+        } else {
+            bulk_s2g(mem.d + gidx, buf + b * TR::B, TR::B * (u32)sizeof(V));
+        }
+    }
+};
 
 // Branchless descent for all E elements of the thread, level by level so that the E
 // independent shared-memory lookups of a level are in flight together.  LOGK = 8 is the
@@ -309,12 +381,12 @@ struct K2Defer {
 };
 
 template <class TR, int NT, int E, int LOGK, bool AGG>
-__device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const uint4 (&raw)[E / TR::VEC],
+__device__ __forceinline__ void k2_tile(const Mem<TR>& mem, const uint4 (&raw)[E / TR::VEC],
                                         u32 valid, bool final_tile, u64 mb, u32 cap,
                                         typename TR::V* buf, u32* nbl,
                                         const u64* tree, const u64* spl, u32* fill, u32* cnt,
                                         u32* slotb, u32* nfl, u32* s_nflushed, u32 logk,
-                                        u32 kprime, u32 eq, const typename TR::V* refill,
+                                        u32 kprime, u32 eq, u64 refill,
                                         typename TR::V* refill_stage, u64* refill_mbar, K2Defer<TR, E>& df,
                                         bool& agg, const unsigned short* lut, u64 lut_lo, u32 lut_sh) {
     typedef typename TR::V V;
@@ -358,11 +430,11 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         if (bk[j] != INV_BUCKET) bk[j] |= pos[j] << 16;
     }
     __syncthreads();
-    if (refill && tid == 0) {
+    if (refill != ~0ull && tid == 0) {
         // every thread has read the stage: load the tile two ahead into it (WAR across the
         // generic and async proxies: fence first)
         fence_proxy_async_smem();
-        bulk_g2s(refill_stage, refill, NT * E * sizeof(V), refill_mbar);
+        k2_stage_load<TR, NT, E>(refill_stage, mem, refill, refill_mbar);
     }
     // 3. per bucket: the previous tile's flush has read the buffer; blocks completed in
     //    this tile and their flush slots.  cnt[b] counts the bucket's stream from the first
@@ -402,7 +474,7 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     //    next block -> deferred
 #pragma unroll
     for (int j = 0; j < E; ++j)
-        if (df.mask & (1u << j)) buf[df.idx[j]] = df.v[j];
+        if (df.mask & (1u << j)) K2Buf<TR>::put(buf, df.idx[j], df.v[j]);
     u32 defer = 0;
 #pragma unroll
     for (int j = 0; j < E; ++j) {
@@ -411,11 +483,11 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
         const u32 p = bk[j] >> 16;
         const u32 q = p / B, off = p % B;
         if (q == 0) {
-            buf[b * B + off] = v[j];
+            K2Buf<TR>::put(buf, b * B + off, v[j]);
         } else {
             const u32 nf = nfl[b];
             if (q < nf) {
-                data[mb + (u64)(slotb[b] + q) * B + off] = v[j];
+                mem.st(mb + (u64)(slotb[b] + q) * B + off, v[j]);
             } else {
                 df.v[j] = v[j];
                 df.idx[j] = b * B + (p - nf * B);
@@ -425,6 +497,8 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     }
     df.mask = defer;
 #if IPS4O_K2_WFLUSH
+    static_assert(!TR::KV, "warp flushes: AoS element types only");
+    typename TR::V* data = mem.d;
     __syncthreads();
     // 5. flush complete buffer blocks: warp w copies the blocks of buckets w, w + NT/32, ...
     //    (one 16-byte vector per lane and block, two blocks in flight); the next tile's
@@ -455,7 +529,7 @@ __device__ __forceinline__ void k2_tile(typename TR::V* __restrict__ data, const
     // 5. flush complete buffer blocks with TMA bulk copies (their reads are awaited at the
     //    next tile's step 3)
     if (tid < (u32)MAXK && nfl[tid]) {
-        bulk_s2g(data + mb + (u64)slotb[tid] * B, buf + tid * B, B * sizeof(V));
+        K2Buf<TR>::flush(mem, mb + (u64)slotb[tid] * B, buf, tid);
         bulk_commit();
     }
 #endif
@@ -469,7 +543,7 @@ __device__ __forceinline__ void k2_drain(typename TR::V* buf, K2Defer<TR, E>& df
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < E; ++j)
-        if (df.mask & (1u << j)) buf[df.idx[j]] = df.v[j];
+        if (df.mask & (1u << j)) K2Buf<TR>::put(buf, df.idx[j], df.v[j]);
     df.mask = 0;
     __syncthreads();
 }
@@ -505,7 +579,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A0) {
     }
     __syncthreads();
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    V* data = reinterpret_cast<V*>(A.data);
+    const Mem<TR> mem(A.data, A.vals);
 
     for (;;) {
         if (tid == 0) {
@@ -544,46 +618,43 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A0) {
             const u64 nft = (me - mb) / TILE;
             uint4 cur[E / TR::VEC];
             constexpr u32 ALL = (E >= 32) ? 0xFFFFFFFFu : ((1u << E) - 1u);
-            constexpr u32 TB = TILE * sizeof(V);
             if (tid == 0) {
                 for (u64 k = 0; k < (u64)K2_STAGES && k < nft; ++k)
-                    bulk_g2s(stage + k * TILE, data + mb + k * TILE, TB, &s_mbar[k]);
+                    k2_stage_load<TR, NT, E>(stage + k * TILE, mem, mb + k * TILE, &s_mbar[k]);
             }
             for (u64 ti = 0; ti < nft; ++ti) {
                 const u32 st = K2_STAGES == 2 ? (u32)(ti & 1) : 0u;
                 mbar_wait(&s_mbar[st], (phase >> st) & 1u);
                 phase ^= 1u << st;
-                const uint4* sp = reinterpret_cast<const uint4*>(stage + st * TILE);
-#pragma unroll
-                for (int i = 0; i < E / TR::VEC; ++i) cur[i] = sp[i * NT + tid];
+                k2_stage_read<TR, NT, E>(stage + st * TILE, cur);
                 // two stages: the tile's first barrier follows every thread's reads of the
                 // stage, and the refill for tile ti+2 is issued after it, inside k2_tile; one
                 // stage: an extra barrier here, then the load of tile ti+1
-                const V* refill = nullptr;
+                u64 refill = ~0ull;
                 if (K2_STAGES == 2) {
-                    refill = ti + 2 < nft ? data + mb + (ti + 2) * TILE : nullptr;
+                    refill = ti + 2 < nft ? mb + (ti + 2) * TILE : ~0ull;
                 } else {
                     __syncthreads();
                     if (tid == 0 && ti + 1 < nft) {
                         fence_proxy_async_smem();
-                        bulk_g2s(stage, data + mb + (ti + 1) * TILE, TB, &s_mbar[0]);
+                        k2_stage_load<TR, NT, E>(stage, mem, mb + (ti + 1) * TILE, &s_mbar[0]);
                     }
                 }
                 if (tp.logk == 8 && !agg)
-                    k2_tile<TR, NT, E, 8, false>(data, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                    k2_tile<TR, NT, E, 8, false>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                                  slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
                                                  refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);
                 else
-                    k2_tile<TR, NT, E, 0, true>(data, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                    k2_tile<TR, NT, E, 0, true>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                                 slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
                                                 refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);
             }
             const u64 tb = mb + nft * TILE;
             if (tb < me) {
-                const u32 vt = k2_load<TR, NT, E>(data, tb, (u32)(me - tb), cur);
-                k2_tile<TR, NT, E, 0, true>(data, cur, vt, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                const u32 vt = k2_load<TR, NT, E>(mem, tb, (u32)(me - tb), cur);
+                k2_tile<TR, NT, E, 0, true>(mem, cur, vt, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                       slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
-                                      nullptr, nullptr, nullptr, df, agg, lut, tp.lut_lo, tp.lut_sh);
+                                      ~0ull, nullptr, nullptr, df, agg, lut, tp.lut_lo, tp.lut_sh);
             }
         }
         if (sd.first && tp.lo < tp.g) {
@@ -591,9 +662,9 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A0) {
             // behind the read frontier (their block grid starts at g)
             const u64 hend = tp.g < tp.hi ? tp.g : tp.hi;
             uint4 hv[E / TR::VEC];
-            const u32 hval = k2_load<TR, NT, E>(data, tp.lo, (u32)(hend - tp.lo), hv);
-            k2_tile<TR, NT, E, 0, true>(data, hv, hval, true, mb, cap, buf, nbl, rtree, spl, fill, cnt, slotb, nfl,
-                           &s_nflushed, tp.logk, tp.kprime, tp.eq, nullptr, nullptr, nullptr, df, agg, lut, tp.lut_lo, tp.lut_sh);
+            const u32 hval = k2_load<TR, NT, E>(mem, tp.lo, (u32)(hend - tp.lo), hv);
+            k2_tile<TR, NT, E, 0, true>(mem, hv, hval, true, mb, cap, buf, nbl, rtree, spl, fill, cnt, slotb, nfl,
+                           &s_nflushed, tp.logk, tp.kprime, tp.eq, ~0ull, nullptr, nullptr, df, agg, lut, tp.lut_lo, tp.lut_sh);
         }
         k2_drain<TR, E>(buf, df);
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area
@@ -632,7 +703,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A0) {
             V* sp = reinterpret_cast<V*>(A.spill) + s_spbase;
             for (u32 b = w; b < (u32)MAXK; b += NT / 32) {
                 const u32 fb = fill[b], ob = slotb[b];
-                for (u32 j = lane; j < fb; j += 32) sp[ob + j] = buf[b * B + j];
+                for (u32 j = lane; j < fb; j += 32) sp[ob + j] = K2Buf<TR>::get(buf, b * B + j);
             }
         }
         if (tid < (u32)MAXK) bulk_wait0();

@@ -19,6 +19,18 @@ namespace ips4o {
 constexpr int K4_MAXSTRIPES = 512;  // >= stripes per level batch (MAXS)
 constexpr int K4_WARPS = K4_THREADS / 32;
 
+// element i of a task's overflow block (KV types: stored as [B keys | B values], the layout
+// of K3's swap buffers)
+template <class TR>
+__device__ __forceinline__ typename TR::V ovf_get(const void* ovf_block, u32 i) {
+    if constexpr (TR::KV) {
+        const u64* p = reinterpret_cast<const u64*>(ovf_block);
+        return make_ulonglong2(p[i], p[TR::B + i]);
+    } else {
+        return reinterpret_cast<const typename TR::V*>(ovf_block)[i];
+    }
+}
+
 // Emission decision for bucket b of task tp (PAPER.md:342 for equality buckets): returns
 // 0..3 = base-case class, 4 = next-level task, 5 = nothing; *td = the task.
 template <class TR>
@@ -72,7 +84,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A0) {
     TaskDesc* s_td = s_td_all[wi];
     u32* s_kind = s_kind_all[wi];
     const u32 ngroups = A.ntasks * (MAXK / K4_GROUP);
-    V* data = reinterpret_cast<V*>(A.data);
+    const Mem<TR> mem(A.data, A.vals);
     const V* spill = reinterpret_cast<const V*>(A.spill);
     u64 base_elems = 0;  // lane 0: elements of this warp's emitted base-case tasks
     for (;;) {
@@ -108,7 +120,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A0) {
                 const u64 db_el = tp.g + (u64)d * B;
                 const u64 in_end = ovf_owner == (int)b ? tp.g + (u64)(tp.nblocks - 1) * B : tp.g + (u64)wfin * B;
                 const u32 ovl = (in_end > db_el && in_end > e1) ? (u32)(in_end - e1) : 0u;
-                for (u32 k = lane; k < ovl; k += 32) s_ovh_all[wi][gi][k] = data[e1 + k];
+                for (u32 k = lane; k < ovl; k += 32) s_ovh_all[wi][gi][k] = mem.ld(e1 + k);
             }
         }
         __syncwarp();
@@ -190,7 +202,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A0) {
                 }
             }
             __syncwarp();
-            const V* ovf = reinterpret_cast<const V*>(A.ovf) + (u64)t * B;
+            const char* ovf = reinterpret_cast<const char*>(A.ovf) + (u64)t * B * TR::S;
             if (few) {
                 // stripe of each spilled source from the lanes of this bucket's segment
                 for (u32 k0 = 0; k0 < nsrc; k0 += 32) {
@@ -204,8 +216,8 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A0) {
                         V val;
                         if (k < ovl) val = s_ovh[k];
                         else if (kk < sp_total) val = spill[sbase + (kk - pre)];
-                        else val = ovf[kk - sp_total];
-                        data[(u64)k < hl ? e0 + k : ts + (k - hl)] = val;
+                        else val = ovf_get<TR>(ovf, kk - sp_total);
+                        mem.st((u64)k < hl ? e0 + k : ts + (k - hl), val);
                     }
                 }
             }
@@ -226,10 +238,10 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A0) {
                     const u64 at = A.s_spbase[S0 + lo] + A.s_spoff[(u64)(S0 + lo) * MAXK + b] + (kk - s_pref[lo]);
                     val = spill[at];
                 } else {
-                    val = ovf[k - ovl - sp_total];
+                    val = ovf_get<TR>(ovf, k - ovl - sp_total);
                 }
                 const u64 dst = (u64)k < hl ? e0 + k : ts + (k - hl);
-                data[dst] = val;
+                mem.st(dst, val);
             }
             // emit the bucket.  Equality buckets are never recursed into; for
             // records an equality bucket of key part 0 (equal first 8 key bytes) still has to
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A0) {
         if (tid == 0) st_release_u32(flag + b, 1u);
         continue;
     }
-    V* data = reinterpret_cast<V*>(A.data);
+    const Mem<TR> mem(A.data, A.vals);
     const u64* bnd = A.bnd + (u64)t * (MAXK + 1);
     const u32* dbl = A.dblk + (u64)t * (MAXK + 1);
     const u64 e0 = bnd[b], e1 = bnd[b + 1];
@@ -305,7 +317,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A0) {
     const u64 db_el = tp.g + (u64)d * B;
     const u64 in_end = own_ovf ? tp.g + (u64)(tp.nblocks - 1) * B : tp.g + (u64)wfin * B;
     const u32 ovl = (in_end > db_el && in_end > e1) ? (u32)(in_end - e1) : 0u;
-    for (u32 k = tid; k < ovl; k += blockDim.x) s_ovh[k] = data[e1 + k];
+    for (u32 k = tid; k < ovl; k += blockDim.x) s_ovh[k] = mem.ld(e1 + k);
     __syncthreads();
     if (tid == 0) {
         __threadfence();
@@ -362,7 +374,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A0) {
     }
     __syncthreads();
     const V* spill = reinterpret_cast<const V*>(A.spill);
-    const V* ovf = reinterpret_cast<const V*>(A.ovf) + (u64)t * B;
+    const char* ovf = reinterpret_cast<const char*>(A.ovf) + (u64)t * B * TR::S;
     // gather: four sources per thread in flight (each is a stripe lookup in shared memory
     // and one dependent load)
     auto src_of = [&](u32 k) -> V {
@@ -377,7 +389,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A0) {
             }
             return spill[s_src[lo] + (kk - s_pref[lo])];
         }
-        return ovf[k - ovl - sp_total];
+        return ovf_get<TR>(ovf, k - ovl - sp_total);
     };
     auto dst_of = [&](u32 k) { return (u64)k < hl ? e0 + k : ts + (k - hl); };
     for (u32 k0 = tid; k0 < nsrc; k0 += 4 * K4_THREADS) {
@@ -390,7 +402,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A0) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const u32 k = k0 + q * K4_THREADS;
-            if (k < nsrc) data[dst_of(k)] = val[q];
+            if (k < nsrc) mem.st(dst_of(k), val[q]);
         }
     }
     // emit the bucket (PAPER.md:342 for equality buckets)

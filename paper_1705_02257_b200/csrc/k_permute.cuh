@@ -234,7 +234,30 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A0) {
     auto pE_of = [&](u32 j) { return staged ? s_pE[j] : A.prefE[S0 + j]; };
     auto pF_of = [&](u32 j) { return staged ? s_pF[j] : A.prefF[S0 + j]; };
     const u32 nwarps = gx * (blockDim.x >> 5);
-    char* base = reinterpret_cast<char*>(A.data) + tp.g * TR::S;
+    char* base = reinterpret_cast<char*>(A.data) + tp.g * GridStride<TR>::v;
+    char* vbase = TR::KV ? reinterpret_cast<char*>(A.vals) + tp.g * 8 : nullptr;
+    // a block in registers (16 B per lane; KV: lanes 0-15 the key block, 16-31 the value block)
+    auto blk_load = [&](u32 x) -> BlockRegs {
+        if constexpr (TR::KV) {
+            BlockRegs r;
+            const char* p = (lane < 16 ? base + (u64)x * (B * 8) + 16 * lane : vbase + (u64)x * (B * 8) + 16 * (lane - 16));
+            asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]) : "l"(p) : "memory");
+            return r;
+        } else {
+            return BlockIO<TR>::load(base + (u64)x * (B * TR::S), lane);
+        }
+    };
+    auto blk_store = [&](u32 x, const BlockRegs& r) {
+        if constexpr (TR::KV) {
+            char* p = (lane < 16 ? base + (u64)x * (B * 8) + 16 * lane : vbase + (u64)x * (B * 8) + 16 * (lane - 16));
+            asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(r.w[0]), "r"(r.w[1]), "r"(r.w[2]),
+                         "r"(r.w[3])
+                         : "memory");
+        } else {
+            BlockIO<TR>::store(base + (u64)x * (B * TR::S), lane, r);
+        }
+    };
     // every lane locates one move (five binary searches), then the warp copies the 32
     // blocks two at a time (the moves are independent: sources are full blocks, targets
     // empty ones)
@@ -266,11 +289,11 @@ __global__ void __launch_bounds__(256) k_moves(LevelArgs A0) {
             const bool two = i + 1 < cnt;
             const u32 s0 = __shfl_sync(0xffffffffu, src, i), d0 = __shfl_sync(0xffffffffu, dst, i);
             const u32 s1 = __shfl_sync(0xffffffffu, src, two ? i + 1 : i), d1 = __shfl_sync(0xffffffffu, dst, two ? i + 1 : i);
-            const BlockRegs v0 = BlockIO<TR>::load(base + (u64)s0 * (B * TR::S), lane);
+            const BlockRegs v0 = blk_load(s0);
             BlockRegs v1;
-            if (two) v1 = BlockIO<TR>::load(base + (u64)s1 * (B * TR::S), lane);
-            BlockIO<TR>::store(base + (u64)d0 * (B * TR::S), lane, v0);
-            if (two) BlockIO<TR>::store(base + (u64)d1 * (B * TR::S), lane, v1);
+            if (two) v1 = blk_load(s1);
+            blk_store(d0, v0);
+            if (two) blk_store(d1, v1);
         }
     }
     }
@@ -591,6 +614,33 @@ __device__ __forceinline__ bool mbar_test(u64* mbar, u32 parity) {
     return ok != 0;
 }
 
+// A block's TMA moves between global memory and a chain's shared-memory swap buffer (KV: the
+// key block and the value block, kept as [keys | values] in shared memory and in the overflow
+// block).
+template <class TR>
+struct K3Blk {
+    static constexpr u32 BB = TR::B * TR::S;
+    __device__ __forceinline__ static void load(char* sbuf, char* kb, char* vb, u32 x, u64* mbar) {
+        if constexpr (TR::KV) {
+            constexpr u32 H = TR::B * 8;
+            mbar_expect_tx(mbar, 2 * H);
+            bulk_g2s_tx(sbuf, kb + (u64)x * H, H, mbar);
+            bulk_g2s_tx(sbuf + H, vb + (u64)x * H, H, mbar);
+        } else {
+            bulk_g2s(sbuf, kb + (u64)x * BB, BB, mbar);
+        }
+    }
+    __device__ __forceinline__ static void store(char* kb, char* vb, u32 x, const char* sbuf) {
+        if constexpr (TR::KV) {
+            constexpr u32 H = TR::B * 8;
+            bulk_s2g(kb + (u64)x * H, sbuf, H);
+            bulk_s2g(vb + (u64)x * H, sbuf + H, H);
+        } else {
+            bulk_s2g(kb + (u64)x * BB, sbuf, BB);
+        }
+    }
+};
+
 template <class TR>
 __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
     const LevelArgs A = with_dyn(A0);
@@ -673,7 +723,8 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
         __syncthreads();
         const TaskParam tp = A.tp[t];
         u32* done = A.done + (u64)t * (MAXK / 32);
-        char* tbase = data + tp.g * TR::S;
+        char* tbase = data + tp.g * GridStride<TR>::v;
+        char* vbase = TR::KV ? reinterpret_cast<char*>(A.vals) + tp.g * 8 : nullptr;
         auto classify_buf = [&](const char* b) {
             typename TR::V v;
             memcpy(&v, b, sizeof(v));
@@ -710,7 +761,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
                     } else {
                         bulk_wait_read0();  // our earlier stores have read this buffer
                         fence_proxy_async_smem();
-                        bulk_g2s(mybuf + xb * BB, tbase + (u64)orr * BB, BB, mymbar);
+                        K3Blk<TR>::load(mybuf + xb * BB, tbase, vbase, (u32)orr, mymbar);
                         st = CH_TAKING;
                     }
                     progressed = true;
@@ -727,7 +778,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
                 if (ow <= orr) {
                     bulk_wait_read0();
                     fence_proxy_async_smem();
-                    bulk_g2s(mybuf + (xb ^ 1) * BB, tbase + (u64)ow * BB, BB, mymbar);
+                    K3Blk<TR>::load(mybuf + (xb ^ 1) * BB, tbase, vbase, (u32)ow, mymbar);
                     st = CH_SWAPPING;
                 } else {
                     st = CH_WAITW;  // empty block: written once the bucket has no readers
@@ -738,14 +789,12 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
                 // no reader left at the crossing: write into the empty block
                 // (past the task end: the overflow block).  (Never spin here:
                 // the reader may be a chain of this warp.)
-                char* dst;
                 if (tp.g + (u64)(slot + 1) * TR::B > tp.hi) {
-                    dst = reinterpret_cast<char*>(A.ovf) + (u64)t * BB;
+                    bulk_s2g(reinterpret_cast<char*>(A.ovf) + (u64)t * BB, mybuf + xb * BB, BB);
                     A.ovf_owner[t] = (int)dest;
                 } else {
-                    dst = tbase + (u64)slot * BB;
+                    K3Blk<TR>::store(tbase, vbase, slot, mybuf + xb * BB);
                 }
-                bulk_s2g(dst, mybuf + xb * BB, BB);
                 bulk_commit();
                 ++nmoves;
                 st = CH_FREE;
@@ -761,7 +810,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
                 } else {
                     const u32 od = classify_buf(mybuf + (xb ^ 1) * BB);
                     if (od != dest) {
-                        bulk_s2g(tbase + (u64)slot * BB, mybuf + xb * BB, BB);
+                        K3Blk<TR>::store(tbase, vbase, slot, mybuf + xb * BB);
                         bulk_commit();
                         ++nmoves;
                         xb ^= 1u;

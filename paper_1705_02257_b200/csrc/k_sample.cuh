@@ -121,10 +121,9 @@ struct TKey {
 // One task t: sample, sort the sample, pick the splitters, build the classifier.
 template <class TR, int SAMPLE>
 __device__ __forceinline__ void k1_task(const LevelArgs& A, u32 t, u64* keys, u64* dist, u32& s_flag, u32& s_nd) {
-    typedef typename TR::V V;
     TaskParam* tp = const_cast<TaskParam*>(A.tp) + t;
     const u64 lo = tp->lo, hi = tp->hi, n = hi - lo;
-    const V* data = reinterpret_cast<const V*>(A.data);
+    const Mem<TR> mem(A.data, A.vals);
 
     // Bucket count: the last levels use an adaptive k aimed at
     // base-case tiles of ~LEAF elements: k = min(256, max(4, pow2_ceil(n/LEAF))).
@@ -160,7 +159,7 @@ __device__ __forceinline__ void k1_task(const LevelArgs& A, u32 t, u64* keys, u6
             const u64 a = lo + n * j / m;
             const u64 b = lo + n * (j + 1) / m;
             const u64 r = mix64(A.seed ^ mix64(lo * 0x9E3779B97F4A7C15ull + j));
-            sk[q] = TR::key(data[a + __umul64hi(r, b - a)], tp->part);
+            sk[q] = mem.key(a + __umul64hi(r, b - a), tp->part);
         }
     }
 #pragma unroll

@@ -38,11 +38,12 @@ constexpr u64 MAX_BATCHES = 1ull << 20;  // safety cap of the level loop (ERR_IT
 // nothing is staged through host memory).  Resets the scheduler and the statistics and puts
 // the whole array into the level queue (n > base capacity) or straight into its base-case
 // size class.
-__global__ void k_init(LevelArgs A0, void* data, u64 n, u64 seed, u32 small_class) {
+__global__ void k_init(LevelArgs A0, void* data, void* vals, u64 n, u64 seed, u32 small_class) {
     if (threadIdx.x != 0) return;
     LevelDyn* D = A0.dyn;
     Sched* Q = A0.sched;
     D->data = data;
+    D->vals = vals;
     D->n = n;
     D->q_next = A0.q_lvl1;
     D->seed = seed;
@@ -83,6 +84,7 @@ __global__ void k_debug_setup(LevelArgs A0, void* data, u64 n, u32 nspl, u32 eq)
     LevelDyn* D = A0.dyn;
     Sched* Q = A0.sched;
     D->data = data;
+    D->vals = nullptr;
     D->n = n;
     D->q_next = A0.q_lvl1;
     D->seed = 1;
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(LevelArgs A0, u32 num_sms
     if (tid < cand) {
         td = qa[ca + tid];
         g = td.lo;
-        while (((base + g * TR::S) & 15u) != 0 && g < td.hi) ++g;
+        while (((base + g * GridStride<TR>::v) & 15u) != 0 && g < td.hi) ++g;
         const u64 main = td.hi - g;
         u64 nsr = max(1ull, (main + L / 2) / L);
         Lt = main;

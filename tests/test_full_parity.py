@@ -116,6 +116,25 @@ def _check_rec(got, exp):
         assert np.array_equal(g, e), "records of equal-key runs differ from the oracle's multiset"
 
 
+def test_full_size_sort_kv_vs_oracle():
+    """ips4o_sort_kv at the C4 size (2^27): u64 keys uniform in [0, 2^32) (duplicates), values =
+    index; keys vs the oracle's key sort, every (key, value) pair preserved."""
+    n = 1 << 27
+    a = W.pair16(n, 2)
+    keys = np.ascontiguousarray(a[:, 0])
+    exp = oracle.sort(keys)
+    dk = to_dev(keys, W.ELEM_U64)
+    dv = torch.from_numpy(np.ascontiguousarray(a[:, 1]).view(np.int64)).cuda()
+    ips4o.sort_kv_(dk, dv)
+    torch.cuda.synchronize()
+    assert ips4o.ips4o_last_stats()["device_error"] == 0
+    gk = to_host(dk, W.ELEM_U64)
+    gv = dv.cpu().numpy().view(np.uint64)
+    assert np.array_equal(gk, exp)
+    assert np.array_equal(np.sort(gv), np.arange(n, dtype=np.uint64))
+    assert np.array_equal(keys[gv.astype(np.int64)], gk)
+
+
 @pytest.mark.parametrize("i", range(len(FULL)), ids=IDS)
 def test_full_size_vs_oracle(ahead, i):
     dist, e, seed = FULL[i]

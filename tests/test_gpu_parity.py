@@ -456,9 +456,10 @@ def test_graph_capture_replay(et, n):
 
 @pytest.mark.parametrize("key_type", [W.ELEM_U64, W.ELEM_F64])
 def test_sort_kv_vs_oracle(key_type):
-    """Structure-of-arrays key-value sort: keys bit-exact vs the oracle's key sort, every
-    (key, value) pair preserved."""
-    for n in (1, 2, 1000, 70_001, 1_000_003):
+    """Structure-of-arrays key-value sort, in place: keys bit-exact vs the oracle's key sort,
+    every (key, value) pair preserved, no staging memory (the pair of arrays is distributed
+    directly: key blocks and value blocks move together)."""
+    for n in (1, 2, 17, 1000, 8192, 8193, 70_001, 1_000_003, (1 << 22) + 5):
         rng = np.random.default_rng(n)
         if key_type == W.ELEM_U64:
             k = W.u64_uniform(n, 5) >> np.uint64(40)   # duplicates
@@ -471,12 +472,23 @@ def test_sort_kv_vs_oracle(key_type):
         torch.cuda.synchronize()
         gk = to_host(dk, key_type)
         gv = dv.cpu().numpy().view(np.uint64)
-        assert np.array_equal(gk, oracle.sort(k))
+        assert np.array_equal(gk.view(np.uint64), oracle.sort(k).view(np.uint64))
+        st = ips4o.ips4o_last_stats()
+        assert st["staging_bytes"] == 0 and st["device_error"] == 0
         kb = k.view(np.uint64) if key_type == W.ELEM_F64 else k
         gkb = gk.view(np.uint64) if key_type == W.ELEM_F64 else gk
         a = np.sort(np.stack([kb, v], 1).view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k", "v"])
         b = np.sort(np.stack([gkb, gv], 1).view([("k", "<u8"), ("v", "<u8")]).ravel(), order=["k", "v"])
         assert np.array_equal(a, b)
+
+
+def test_sort_kv_alignment_and_types():
+    k = torch.zeros(1001, dtype=torch.uint64, device="cuda")
+    v = torch.zeros(1001, dtype=torch.int64, device="cuda")
+    with pytest.raises(ips4o.Ips4oError):
+        ips4o.ips4o_sort_kv(k.data_ptr() + 8, v.data_ptr(), 1000, W.ELEM_U64)   # keys not 16-byte aligned
+    with pytest.raises(ips4o.Ips4oError):
+        ips4o.sort_kv_(k.view(torch.int64), v)                                  # int64 keys: rejected
 
 
 def test_sort_host_entry_point():
