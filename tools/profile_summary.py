@@ -12,12 +12,14 @@ import subprocess
 from collections import OrderedDict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KIND = [("k_sample", "sample_splitters"), ("k_tree_from", "sample_splitters"), ("k_classify", "classify_flush"),
+KIND = [("k_plan", "other"), ("k_epi", "other"), ("k_init", "other"), ("k_sample", "sample_splitters"), ("k_tree_from", "sample_splitters"), ("k_classify", "classify_flush"),
         ("k_prepare", "prepare"), ("k_moves", "empty_block_moves"), ("k_permute", "block_permute"),
         ("k_cleanup", "cleanup"), ("k_base", "base_case")]
 FULL_KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
              "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
              "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+             "smsp__sass_branch_targets.sum", "smsp__sass_branch_targets_threads_divergent.sum",
+             "smsp__sass_branch_targets_threads_uniform.sum", "smsp__thread_inst_executed.sum",
              "launch__registers_per_thread"]
 
 
