@@ -94,7 +94,12 @@ typedef struct {
     uint64_t block_moves;       /* block writes of the block permutation (swaps and placements) */
     uint64_t empty_block_moves; /* Appendix-A moves */
     uint64_t device_error;      /* sticky device consistency flags (0 = none; nonzero: the output is invalid) */
-    uint64_t staging_bytes;     /* device staging of ips4o_sort_host / ips4o_sort_kv (0 for ips4o_sort) */
+    uint64_t staging_bytes;     /* device staging of ips4o_sort_host (0 for ips4o_sort, ips4o_sort_kv) */
+    uint64_t medium_tasks;      /* subproblems sorted completely by one CTA (single-CTA tier) */
+    uint64_t medium_partitions; /* partitioning steps inside the single-CTA tier */
+    uint64_t medium_marks;      /* buckets whose maximum was moved to their first position so that
+                                   searchNextLargest finds them (strictly in-place driver) */
+    uint64_t medium_leaves;     /* leaves sorted in shared memory inside the single-CTA tier */
     uint32_t has_device_stats;  /* 1 if the device-side fields above are valid */
     uint32_t reserved_;
 } ips4o_stats;
@@ -144,10 +149,10 @@ int ips4o_release_workspace(void);
  * ips4o_profile_read() synchronises the recorded events and returns, per kernel kind,
  * the number of launches and the summed device milliseconds, then clears the record.
  * Kinds: 0 sample/splitters, 1 classify_flush, 2 prepare, 3 empty-block moves,
- * 4 block permutation, 5 cleanup, 6 base case, 7 other. */
-#define IPS4O_NUM_KERNEL_KINDS 8
+ * 4 block permutation, 5 cleanup, 6 base case, 7 other, 8 single-CTA tier. */
+#define IPS4O_NUM_KERNEL_KINDS 9
 int ips4o_profile_enable(int on);
-int ips4o_profile_read(uint64_t* launches /*[8]*/, double* ms /*[8]*/);
+int ips4o_profile_read(uint64_t* launches /*[9]*/, double* ms /*[9]*/);
 const char* ips4o_kernel_kind_name(int kind);
 
 /* ------------------------------------------------------- test-only hooks */

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("IPS4O_LIB") or os.path.join(_HERE, "libips4o.so")
 
 IPS4O_U64, IPS4O_F64, IPS4O_PAIR_U64, IPS4O_REC100_K10, IPS4O_PAIR_F64, IPS4O_QUARTET_F64 = 0, 1, 2, 3, 4, 5
 ELEM_SIZE = {0: 8, 1: 8, 2: 16, 3: 100, 4: 16, 5: 32}
-NUM_KERNEL_KINDS = 8
+NUM_KERNEL_KINDS = 9
 
 # every symbol include/ips4o.h declares
 EXPORTS = (
@@ -43,7 +43,9 @@ class Stats(ctypes.Structure):
                 ("batches", ctypes.c_uint64), ("base_tasks_by_class", ctypes.c_uint64 * 4),
                 ("base_fallback_tasks", ctypes.c_uint64), ("block_moves", ctypes.c_uint64),
                 ("empty_block_moves", ctypes.c_uint64), ("device_error", ctypes.c_uint64),
-                ("staging_bytes", ctypes.c_uint64), ("has_device_stats", ctypes.c_uint32),
+                ("staging_bytes", ctypes.c_uint64), ("medium_tasks", ctypes.c_uint64),
+                ("medium_partitions", ctypes.c_uint64), ("medium_marks", ctypes.c_uint64),
+                ("medium_leaves", ctypes.c_uint64), ("has_device_stats", ctypes.c_uint32),
                 ("reserved_", ctypes.c_uint32)]
 
     def as_dict(self):

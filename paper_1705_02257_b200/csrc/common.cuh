@@ -249,7 +249,9 @@ enum {
     CTR_FB = 7,       // base-case fallback queue length (leaves the cell kernel hands back)
     CTR_BASE0 = 8,    // base-case queue lengths, one per size class (4)
     CTR_TK0 = 12,     // base-case leaf tickets, one per size class (4)
-    CTR_N = 16
+    CTR_MED = 16,     // medium (single-CTA tier) queue length
+    CTR_MTK = 17,     // medium task ticket
+    CTR_N = 20
 };
 constexpr int NUM_BASE_CLASSES = 4;
 // base-case size classes (8-byte types): <= 2048, <= 4096, <= 6144, <= 16384 elements; each
@@ -295,7 +297,7 @@ struct Sched {
 enum {
     DS_LEVELS = 0, DS_DIST_TASKS, DS_BASE_TASKS, DS_EQ_TASKS, DS_DIST_ELEMS, DS_BASE_ELEMS,
     DS_BATCHES, DS_ERROR, DS_BLOCK_MOVES, DS_AMOVES, DS_FALLBACK, DS_BASE_C0, DS_BASE_C1, DS_BASE_C2,
-    DS_BASE_C3, DS_ITERS, DS_N = 16
+    DS_BASE_C3, DS_ITERS, DS_MED_TASKS, DS_MED_PARTS, DS_MED_MARKS, DS_MED_LEAVES, DS_N = 24
 };
 
 struct LevelArgs {
@@ -333,6 +335,9 @@ struct LevelArgs {
     TaskDesc* q_next; // (from dyn)
     TaskDesc* q_base; // base-case queues by size class: class c at q_base + qb_off[c], qb_cap[c] tasks
     TaskDesc* q_fb;   // [q_cap] base-case fallback queue (clustered leaves -> merge sort)
+    TaskDesc* q_med;  // [qm_cap] medium tasks of the batch (single-CTA tier, k_cta.cuh)
+    u32 qm_cap;
+    u64 medium_max;   // tasks of base_cap < n <= medium_max go to the single-CTA tier (0: none)
     TaskDesc* q_lvl0; // [qn_cap] level queue A
     TaskDesc* q_lvl1; // [qn_cap] level queue B
     u32 qb_off[4], qb_cap[4];

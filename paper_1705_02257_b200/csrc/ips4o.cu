@@ -16,6 +16,7 @@
 #include "k_classify.cuh"
 #include "k_classify_rec.cuh"
 #include "k_cleanup.cuh"
+#include "k_cta.cuh"
 #include "k_permute.cuh"
 #include "k_sample.cuh"
 #include "k_sched.cuh"
@@ -28,10 +29,10 @@ static std::mutex g_mu;
 static char g_errbuf[512];
 static ips4o_stats g_stats;  // host-side fields of the last call (the rest comes from the device)
 
-enum KernelKind { KK_SAMPLE = 0, KK_CLASSIFY, KK_PREPARE, KK_MOVES, KK_PERMUTE, KK_CLEANUP, KK_BASE, KK_OTHER };
+enum KernelKind { KK_SAMPLE = 0, KK_CLASSIFY, KK_PREPARE, KK_MOVES, KK_PERMUTE, KK_CLEANUP, KK_BASE, KK_OTHER, KK_MEDIUM };
 static const char* kKindNames[IPS4O_NUM_KERNEL_KINDS] = {
     "sample_splitters", "classify_flush", "prepare", "empty_block_moves",
-    "block_permute",    "cleanup",        "base_case", "other"};
+    "block_permute",    "cleanup",        "base_case", "other",             "medium_cta"};
 constexpr u32 STAMP_BEGIN = 255;
 constexpr u32 PLOG_CAP = 1u << 12;
 
@@ -44,6 +45,7 @@ struct Caps {
     u32 qb_cap[4] = {1, 1, 1, 1};  // base-case queue per size class
     u32 q_fb = 1;                // fallback queue
     u32 qn = 1;                  // level queue
+    u32 qm = 1;                  // medium queue (single-CTA tier)
     u64 spill = 64;              // spilled partial-buffer elements
     int esize = 8;
 };
@@ -68,6 +70,8 @@ static Caps caps_for(u64 n) {
     c.q_fb = (u32)tot;
     // next-level tasks hold > CAP elements each
     c.qn = (u32)(n / (CAPB + 1) + 2);
+    // medium tasks of one batch (single-CTA tier): > CAP elements each
+    c.qm = TR::WIDE ? 1u : (u32)std::min<u64>((u64)c.tcap * MAXK, n / (CAPB + 1) + 2);
     // Spill (the partially filled buffers of every stripe): a stripe spills at most
     // min(its length, K*(b-1)) elements.  Multi-stripe tasks have stripes >= 2^16 elements
     // (one quarter-length last stripe), single-stripe tasks an adaptive K < 4*m/LEAF
@@ -79,7 +83,7 @@ static Caps caps_for(u64 n) {
 
 struct Layout {
     size_t tp, sd, order, tree, s_count, s_small, bnd, dblk, nfb, btot, lut, done, tdone, wr, ovf, ovf_owner,
-        qbase, qfb, qlvl, ctr, dsplit, dyn, sched, dstats, plog, spill, total;
+        qbase, qfb, qlvl, qmed, ctr, dsplit, dyn, sched, dstats, plog, spill, total;
 };
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static Layout layout_of(const Caps& c) {
@@ -112,6 +116,7 @@ static Layout layout_of(const Caps& c) {
     L.qbase = add(qb * sizeof(TaskDesc));
     L.qfb = add((size_t)c.q_fb * sizeof(TaskDesc));
     L.qlvl = add((size_t)c.qn * sizeof(TaskDesc) * 2);
+    L.qmed = add((size_t)c.qm * sizeof(TaskDesc));
     L.ctr = add(CTR_N * 4 + 16);
     L.dsplit = add(MAXK * 8);
     L.dyn = add(sizeof(LevelDyn));
@@ -139,8 +144,8 @@ struct Workspace {
     Layout lay;
     u64 gen = 0;                 // bumps on every (re)allocation: cached graphs are rebuilt
     cudaStream_t cap_stream = nullptr;   // graph-building capture stream
-    cudaStream_t side[4];        // base-case size classes run as parallel graph branches
-    cudaEvent_t ev_fork, ev_join[4];
+    cudaStream_t side[5];        // base-case size classes and the single-CTA tier run as parallel graph branches
+    cudaEvent_t ev_fork, ev_join[5];
     cudaEvent_t ev_done;         // recorded after every call: the workspace is free again
     bool have_done = false;
     bool last_captured = false;
@@ -176,7 +181,7 @@ static void drop_graphs() {
 static int ensure_streams() {
     if (g_ws.streams_ready) return IPS4O_OK;
     CK(cudaStreamCreateWithFlags(&g_ws.cap_stream, cudaStreamNonBlocking));
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 5; ++c) {
         CK(cudaStreamCreateWithFlags(&g_ws.side[c], cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&g_ws.ev_join[c], cudaEventDisableTiming));
     }
@@ -195,7 +200,7 @@ static void release_all() {
     g_ws.kernels_type = -1;
     if (g_ws.streams_ready) {
         cudaStreamDestroy(g_ws.cap_stream);
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 5; ++c) {
             cudaStreamDestroy(g_ws.side[c]);
             cudaEventDestroy(g_ws.ev_join[c]);
         }
@@ -209,11 +214,29 @@ static void release_all() {
 
 static bool caps_cover(const Caps& have, const Caps& need) {
     if (have.esize != need.esize || have.tcap < need.tcap || have.scap < need.scap || have.q_fb < need.q_fb ||
-        have.qn < need.qn || have.spill < need.spill)
+        have.qn < need.qn || have.qm < need.qm || have.spill < need.spill)
         return false;
     for (int k = 0; k < 4; ++k)
         if (have.qb_cap[k] < need.qb_cap[k]) return false;
     return true;
+}
+
+// Tasks of (base capacity, medium_max] elements go to the single-CTA tier (k_cta.cuh);
+// IPS4O_MEDIUM_MAX (environment, read once) sets it, 0 = no tier.  The default is 0: on B200 one
+// CTA per subproblem sorts 3-10x slower per SM than the multi-CTA levels plus the multi-CTA-per-SM
+// base case (measured), so the tier is an opt-in mode (the strictly in-place driver
+// of PAPER.md:381-395).
+#ifndef IPS4O_MEDIUM_MAX
+#define IPS4O_MEDIUM_MAX 0ull
+#endif
+static u64 medium_max() {
+    static long long v = -1;
+    if (v < 0) {
+        const char* e = getenv("IPS4O_MEDIUM_MAX");
+        v = e ? atoll(e) : (long long)IPS4O_MEDIUM_MAX;
+        if (v < 0) v = 0;
+    }
+    return (u64)v;
 }
 
 static void fill_args() {
@@ -258,6 +281,9 @@ static void fill_args() {
     }
     A.q_fb = (TaskDesc*)(p + L.qfb);
     A.q_cap = c.q_fb;
+    A.q_med = (TaskDesc*)(p + L.qmed);
+    A.qm_cap = c.qm;
+    A.medium_max = medium_max();
     A.q_lvl0 = (TaskDesc*)(p + L.qlvl);
     A.q_lvl1 = A.q_lvl0 + c.qn;
     A.qn_cap = c.qn;
@@ -303,6 +329,7 @@ static int ensure_ws(u64 n) {
         for (int k = 0; k < 4; ++k) need.qb_cap[k] = std::max(need.qb_cap[k], h.qb_cap[k]);
         need.q_fb = std::max(need.q_fb, h.q_fb);
         need.qn = std::max(need.qn, h.qn);
+        need.qm = std::max(need.qm, h.qm);
         need.spill = std::max(need.spill, h.spill);
     }
     const Layout L = layout_of(need);
@@ -424,6 +451,8 @@ static int prepare_kernels(void) {
     if constexpr (!TR::KV) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_permute<TR>, K3_THREADS, 0));
     else occ3 = 1;
     CK(cudaFuncSetAttribute(k_permute_tma<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3TSmem<TR>::total));
+    if constexpr (!TR::WIDE)
+        CK(cudaFuncSetAttribute(k_cta_sort<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CtaCfg<TR>::smem));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3t, k_permute_tma<TR>, K3T_THREADS, K3TSmem<TR>::total));
     if (occ2 < 1 || occ3 < 1 || occ3t < 1) {
         snprintf(g_errbuf, sizeof g_errbuf, "occupancy query returned %d/%d/%d", occ2, occ3, occ3t);
@@ -530,14 +559,21 @@ static int enqueue_base(Enq& q) {
         STAMP(KK_BASE);
         return IPS4O_OK;
     } else {
-        cudaStream_t ss[4] = {st, st, st, st};
+        cudaStream_t ss[5] = {st, st, st, st, st};
         const bool conc = !q.prof;
         if (conc) {
             CK(cudaEventRecord(g_ws.ev_fork, st));
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 5; ++c) {
                 ss[c] = g_ws.side[c];
                 CK(cudaStreamWaitEvent(ss[c], g_ws.ev_fork, 0));
             }
+        }
+        // the single-CTA tier: medium tasks, each sorted completely by one CTA (k_cta.cuh)
+        if (A.medium_max) {
+            const cudaStream_t s4 = ss[4];
+            LAUNCH(KK_MEDIUM, (k_cta_sort<TR><<<g_ws.num_sms, CtaCfg<TR>::NT, CtaCfg<TR>::smem, s4>>>(
+                                  A, A.q_med, A.ctr + CTR_MED, A.qm_cap, A.ctr + CTR_MTK)));
+            if (q.prof) STAMP(KK_MEDIUM);
         }
         int rc = enqueue_cell<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>(q, ss[0], 0);
         if (rc) return rc;
@@ -554,7 +590,7 @@ static int enqueue_base(Enq& q) {
             STAMP(KK_BASE);
         }
         if (conc) {
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 5; ++c) {
                 CK(cudaEventRecord(g_ws.ev_join[c], ss[c]));
                 CK(cudaStreamWaitEvent(st, g_ws.ev_join[c], 0));
             }
@@ -680,7 +716,9 @@ static int sort_impl(void* data, u64 n, cudaStream_t st, void* vals = nullptr) {
     // previous call's work (the event is recorded at the end of every call)
     if (!capturing && g_ws.have_done && !g_ws.last_captured && g_ws.last_stream != st)
         CK(cudaStreamWaitEvent(st, g_ws.ev_done, 0));
-    const u32 small = n <= (u64)TR::CAP ? base_class<TR>(n) : (u32)NUM_BASE_CLASSES;
+    const u32 small = n <= (u64)TR::CAP                     ? base_class<TR>(n)
+                      : (!TR::WIDE && n <= g_ws.A.medium_max) ? (u32)NUM_BASE_CLASSES + 1
+                                                              : (u32)NUM_BASE_CLASSES;
     k_init<<<1, 32, 0, st>>>(g_ws.A, data, vals, n, 0x1234567ull, small);
     CK(cudaGetLastError());
     g_stats.host_syncs = 0;
@@ -886,6 +924,10 @@ static int fetch_stats() {
     g_stats.empty_block_moves = ds[DS_AMOVES];
     g_stats.base_fallback_tasks = ds[DS_FALLBACK];
     for (int c = 0; c < 4; ++c) g_stats.base_tasks_by_class[c] = ds[DS_BASE_C0 + c];
+    g_stats.medium_tasks = ds[DS_MED_TASKS];
+    g_stats.medium_partitions = ds[DS_MED_PARTS];
+    g_stats.medium_marks = ds[DS_MED_MARKS];
+    g_stats.medium_leaves = ds[DS_MED_LEAVES];
     // one k_init, then every iteration of the loop launches the body's kernels
     g_stats.kernel_launches = 1 + ds[DS_ITERS] * g_nodes_per_iter;
     return IPS4O_OK;

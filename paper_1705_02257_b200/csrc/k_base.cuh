@@ -474,338 +474,350 @@ __device__ __forceinline__ void sts_v(u32 saddr, const V& v) {
 // Leaves are taken from the class queue through an atomic ticket (the grid is the resident
 // CTAs: a CTA that finishes early takes the next leaf); the next leaf's descriptor is known
 // one leaf ahead and its elements are prefetched into L2 by a TMA bulk prefetch.
+// Shared scalars of one cell-sort leaf.
+template <int NW>
+struct CellSh {
+    u32 r[4];        // 32-bit key-range halves: hi min / max, lo min / max
+    u64 r64[2];      // exact 64-bit range (leaves whose high halves are close)
+    u32 flag, wsum[NW];
+};
+
+// The cell sort of one leaf td (<= NT*E elements) by the whole CTA (steps 1-5 above): X0 is the
+// leaf's shared-memory tile (TILE elements + 16 bytes), cnt the cell counters.  after_range() is
+// called by every thread between the barriers that follow the key-range reduction (the caller's
+// next-leaf bookkeeping).  Returns 0 when the leaf is sorted in place, 1 when its keys are too
+// clustered for the cells (it is left untouched for the merge sort).
+template <class TR, int NT, int E, class F>
+__device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem, typename TR::V* data,
+                                         typename TR::V* X0, u32* cnt, CellSh<NT / 32>& S, F&& after_range) {
+    typedef typename TR::V V;
+    typedef CellBase<TR, NT, E> CB;
+    typedef typename CellWork<TR>::T TW;
+    const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint4* myrun = reinterpret_cast<uint4*>(cnt + cpad<E>(tid * E));  // this thread's E counters
+    const u32 n = (u32)(td.hi - td.lo);
+    V* g = data + td.lo;
+    // the leaf in shared memory starts at the same offset modulo 16 bytes as in global
+    // memory, so that its aligned body leaves by one TMA bulk store
+    const u32 p = (sizeof(V) == 8 && !TR::KV) ? (u32)((reinterpret_cast<uintptr_t>(g) >> 3) & 1u) : 0u;
+    V* const X = X0 + p;
+    const u32 ncell = n > 1 ? n : 1u;  // one cell per element (n <= the tile)
+    if (tid == 0) {
+        S.r[0] = ~0u;
+        S.r[1] = 0u;
+        S.r[2] = ~0u;
+        S.r[3] = 0u;
+        S.r64[0] = ~0ull;
+        S.r64[1] = 0ull;
+        S.flag = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < E / 4; ++k) myrun[k] = make_uint4(0u, 0u, 0u, 0u);
+    // 1. load (element j*NT + tid) and the range of the keys' high 32-bit halves
+    //    (warp reductions in one REDUX instruction each)
+    //    (branch-free over the whole tile: the slots past n load a copy of element n-1,
+    //    which changes no range; they get cells of their own past the leaf's cells)
+    V v[E];
+    u32 hmin = ~0u, hmax = 0u;
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const u32 idx = min((u32)(j * NT) + tid, n - 1u);
+        v[j] = CellWork<TR>::in(mem.ld(td.lo + idx));
+        const u32 h = (u32)(TW::key(v[j]) >> 32);
+        hmin = min(hmin, h);
+        hmax = max(hmax, h);
+    }
+    hmin = __reduce_min_sync(0xffffffffu, hmin);
+    hmax = __reduce_max_sync(0xffffffffu, hmax);
+    __syncthreads();  // the range words and the counters are reset; the previous leaf is done
+    BASE_PROF_MARK(1);
+    if (lane == 0) {
+        atomicMin(&S.r[0], hmin);
+        atomicMax(&S.r[1], hmax);
+    }
+    __syncthreads();
+    BASE_PROF_MARK(2);
+    after_range();  // (the caller: next-leaf bookkeeping between the barriers)
+    // the key range: from the high halves when they are far apart (a conservative range
+    // at most (d+1)/(d-1) wider than the exact one for d = hmax - hmin >= 16); exact from
+    // the low halves when all high halves are equal; exact 64-bit otherwise
+    const u32 H0 = S.r[0], H1 = S.r[1];
+    u64 kmin, span;
+    if (H1 - H0 >= 16u) {
+        kmin = (u64)H0 << 32;
+        span = ((((u64)H1) << 32) | 0xFFFFFFFFull) - kmin;
+    } else if (H1 == H0) {
+        u32 lmin = ~0u, lmax = 0u;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const u32 l = (u32)TW::key(v[j]);
+            lmin = min(lmin, l);
+            lmax = max(lmax, l);
+        }
+        lmin = __reduce_min_sync(0xffffffffu, lmin);
+        lmax = __reduce_max_sync(0xffffffffu, lmax);
+        if (lane == 0) {
+            atomicMin(&S.r[2], lmin);
+            atomicMax(&S.r[3], lmax);
+        }
+        __syncthreads();
+        kmin = ((u64)H0 << 32) | S.r[2];
+        span = (u64)(S.r[3] - S.r[2]);
+    } else {
+        u64 mn = ~0ull, mx = 0ull;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const u64 k = TW::key(v[j]);
+            mn = k < mn ? k : mn;
+            mx = k > mx ? k : mx;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const u64 a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+        }
+        if (lane == 0) {
+            atomicMin(&S.r64[0], mn);
+            atomicMax(&S.r64[1], mx);
+        }
+        __syncthreads();
+        kmin = S.r64[0];
+        span = S.r64[1] - kmin;
+    }
+    if (span == 0) return 0;  // all keys equal: already sorted (no write)
+    // cell(key) = floor(x * ncell / (span32 + 1)) for x = (key - kmin) >> s, the top 32
+    // bits of the offset (s = 0 when the span fits 32 bits): one 32x32 multiply-high with
+    // a per-leaf multiplier, monotone, onto [0, ncell).  (mul = floor(ncell * 2^32 /
+    // (span32 + 1)) < 2^32 for span32 >= ncell; otherwise s = 0 and the cell is x itself,
+    // a single key value.)
+    const u32 bl = 64u - (u32)__clzll((long long)span);
+    const u32 sh = bl > 32u ? bl - 32u : 0u;
+    const u32 span32 = (u32)(span >> sh);
+    const u32 mul = span32 >= ncell ? (u32)(((u64)ncell << 32) / ((u64)span32 + 1ull)) : 0u;
+    // 2. cell and rank inside the cell (slots past n: cell = the slot index >= n)
+    const u32 s_cnt = (u32)__cvta_generic_to_shared(cnt);
+    u32 cr[E];  // cell | rank << 16
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const u32 idx = j * NT + tid;
+        const u32 x = (u32)((TW::key(v[j]) - kmin) >> sh);
+        u32 c = mul ? __umulhi(x, mul) : x;
+        c = idx < n ? c : idx;
+        cr[j] = c | (atoms_inc(s_cnt + 4u * cpad<E>(c)) << 16);
+    }
+    __syncthreads();
+    BASE_PROF_MARK(3);
+    // 3. exclusive scan of the counts (own run of E cells, 128-bit accesses)
+    u32 sum = 0;
+#pragma unroll
+    for (int k = 0; k < E / 4; ++k) {
+        const uint4 q = myrun[k];
+        sum += q.x + q.y + q.z + q.w;
+    }
+    u32 incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (u32)o) incl += y;
+    }
+    if (lane == 31) S.wsum[w] = incl;
+    __syncthreads();
+    BASE_PROF_MARK(4);
+    u32 base = incl - sum;
+    for (u32 ww = 0; ww < w; ++ww) base += S.wsum[ww];
+    u32 bigwork = 0;  // insertion work of this run's cells (~m^2 / 4 for large cells)
+    {
+        u32 run = base;
+#pragma unroll
+        for (int k = 0; k < E / 4; ++k) {
+            uint4 q = myrun[k];
+            u32 x;
+            x = q.x; q.x = run; run += x; if (x > 8) bigwork += x * x / 4;
+            x = q.y; q.y = run; run += x; if (x > 8) bigwork += x * x / 4;
+            x = q.z; q.z = run; run += x; if (x > 8) bigwork += x * x / 4;
+            x = q.w; q.w = run; run += x; if (x > 8) bigwork += x * x / 4;
+            myrun[k] = q;
+        }
+    }
+    if (bigwork && mul) atomicAdd(&S.flag, bigwork);
+    if (IPS4O_BASE_TMA_WB && tid == 0) bulk_wait_read0();  // the previous leaf has left X
+    __syncthreads();
+    BASE_PROF_MARK(5);
+    if (S.flag > CELL_FIX_BUDGET) return 1;  // clustered keys (heavy duplicates in few cells): the caller hands the leaf on
+    {
+        const u32 s_x = (u32)__cvta_generic_to_shared(X);
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const u32 pos = lds_u32(s_cnt + 4u * cpad<E>(cr[j] & 0xFFFFu)) + (cr[j] >> 16);
+            sts_v<V>(s_x + pos * (u32)sizeof(V), v[j]);
+        }
+    }
+    __syncthreads();
+    BASE_PROF_MARK(6);
+    // 4. order the cells of this thread's run that hold several elements (PAPER.md:403
+    //    finishes small subproblems by insertion sort): cells of 2-4 elements by a
+    //    4-element sorting network over the cell padded with the largest key (pads never
+    //    move: a comparator swaps only on strictly smaller keys), larger ones by insertion
+    //    sort.  Singleton cells need nothing; nothing at all when every cell is a single
+    //    key value.
+    if (mul) {
+        u32 bs[E + 1];
+#pragma unroll
+        for (int k = 0; k < E / 4; ++k) {
+            const uint4 q = myrun[k];
+            bs[4 * k] = q.x;
+            bs[4 * k + 1] = q.y;
+            bs[4 * k + 2] = q.z;
+            bs[4 * k + 3] = q.w;
+        }
+        bs[E] = tid + 1 < (u32)NT ? cnt[cpad<E>((tid + 1) * E)] : (u32)CB::TILE;
+        // cells of 2 (most multi-element cells), of 3-4 and larger ones in separate
+        // loops, so that a warp's lanes run the same code in each
+        u32 m2 = 0, m34 = 0, mbig = 0;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const u32 m = bs[k + 1] - bs[k];
+            m2 |= (m == 2u ? 1u : 0u) << k;
+            m34 |= (m - 3u <= 1u ? 1u : 0u) << k;
+            mbig |= (m > 4u ? 1u : 0u) << k;
+        }
+        const u32 enext = bs[E];
+        while (m2) {
+            const u32 k = (u32)__ffs(m2) - 1u;
+            m2 &= m2 - 1u;
+            const u32 b = cnt[cpad<E>(tid * E + k)];
+            const V x0 = X[b], x1 = X[b + 1];
+            if (TW::less(x1, x0)) {
+                X[b] = x1;
+                X[b + 1] = x0;
+            }
+        }
+        while (m34) {
+            const u32 k = (u32)__ffs(m34) - 1u;
+            m34 &= m34 - 1u;
+            const u32 b = cnt[cpad<E>(tid * E + k)];
+            const u32 e = k + 1 < (u32)E ? cnt[cpad<E>(tid * E + k + 1)] : enext;
+            const V pd = TW::pad();
+            V x0 = X[b], x1 = X[b + 1], x2 = X[b + 2];
+            V x3 = e - b > 3u ? X[b + 3] : pd;
+            auto cas = [](V& lo, V& hi) {
+                const bool sw = TW::less(hi, lo);
+                const V t = sw ? hi : lo;
+                hi = sw ? lo : hi;
+                lo = t;
+            };
+            cas(x0, x1);
+            cas(x2, x3);
+            cas(x0, x2);
+            cas(x1, x3);
+            cas(x1, x2);
+            X[b] = x0;
+            X[b + 1] = x1;
+            X[b + 2] = x2;
+            if (e - b > 3u) X[b + 3] = x3;
+        }
+        while (mbig) {
+            const u32 k = (u32)__ffs(mbig) - 1u;
+            mbig &= mbig - 1u;
+            const u32 b = cnt[cpad<E>(tid * E + k)];
+            const u32 e = k + 1 < (u32)E ? cnt[cpad<E>(tid * E + k + 1)] : enext;
+            for (u32 i = b + 1; i < e; ++i) {
+                const V x = X[i];
+                u32 q = i;
+                while (q > b && TW::less(x, X[q - 1])) {
+                    X[q] = X[q - 1];
+                    --q;
+                }
+                X[q] = x;
+            }
+        }
+    }
+    if constexpr (TR::KV) {
+        // 5. write back: key and value arrays by coalesced stores
+        __syncthreads();
+        for (u32 i = tid; i < n; i += NT) mem.st(td.lo + i, CellWork<TR>::out(X[i]));
+        return 0;
+    }
+    if constexpr (!std::is_same<TW, TR>::value) {
+        __syncthreads();
+        for (u32 i = tid; i < n; i += NT) X[i] = CellWork<TR>::out(X[i]);
+    }
+#if IPS4O_BASE_TMA_WB
+    fence_proxy_async_smem();
+    __syncthreads();
+    BASE_PROF_MARK(7);
+    // 5. write back: the 16-byte aligned body by one TMA bulk store (read before the next
+    //    leaf's scatter), the element before / after it by plain stores
+    {
+        const u32 i0 = p < n ? p : n;
+        const u32 i1 = sizeof(V) == 8 ? i0 + ((n - i0) & ~1u) : n;
+        if (tid == 0 && i1 > i0) {
+            bulk_s2g(g + i0, X + i0, (i1 - i0) * (u32)sizeof(V));
+            bulk_commit();
+        }
+        if (tid == 32 && i0 > 0) g[0] = X[0];
+        if (tid == 64 && i1 < n) g[n - 1] = X[n - 1];
+    }
+#else
+    __syncthreads();
+    BASE_PROF_MARK(7);
+    // 5. write back
+    for (u32 i = tid; i < n; i += NT) g[i] = X[i];
+#endif
+    return 0;
+}
+
 template <class TR, int NT, int E>
 __global__ void __launch_bounds__(NT, (CellMinB<TR, NT, E>::v))
     k_base_cell(const TaskDesc* tasks, const u32* d_ntasks, u32 qcap, u32* ticket, const LevelDyn* dyn,
                 TaskDesc* fb_queue, u32* fb_count, u32 fb_cap) {
     typedef typename TR::V V;
     typedef CellBase<TR, NT, E> CB;
-    typedef typename CellWork<TR>::T TW;
-    constexpr int NW = NT / 32;
     static_assert(E % 4 == 0, "cell runs are read as 128-bit vectors");
     extern __shared__ __align__(16) unsigned char smc[];
     V* const X0 = reinterpret_cast<V*>(smc);
     u32* cnt = reinterpret_cast<u32*>(smc + CB::x_bytes);
-    __shared__ u32 s_r[4];        // 32-bit key-range halves: hi min / max, lo min / max
-    __shared__ u64 s_r64[2];      // exact 64-bit range (leaves whose high halves are close)
-    __shared__ u32 s_flag, s_wsum[NW], s_next[2];
+    __shared__ CellSh<NT / 32> sh;
+    __shared__ u32 s_next[2];
     const u32 ntasks = min(*d_ntasks, qcap);  // (the count lives on the device: the grid is fixed)
     const Mem<TR> mem(dyn->data, dyn->vals);
     V* data = reinterpret_cast<V*>(dyn->data);  // (AoS types: the leaf's TMA write-back)
-    const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    uint4* myrun = reinterpret_cast<uint4*>(cnt + cpad<E>(tid * E));  // this thread's E counters
-    BASE_PROF_INIT();
+    const u32 tid = threadIdx.x;
     if (tid == 0) s_next[0] = atomicAdd(ticket, 1u);
     __syncthreads();
     u32 cur = s_next[0], par = 1;
     while (cur < ntasks) {
         const TaskDesc td = tasks[cur];
         if (tid == 0) s_next[par] = atomicAdd(ticket, 1u);  // the next leaf (read after the barriers below)
-        const u32 n = (u32)(td.hi - td.lo);
-        V* g = data + td.lo;
-        // the leaf in shared memory starts at the same offset modulo 16 bytes as in global
-        // memory, so that its aligned body leaves by one TMA bulk store
-        const u32 p = (sizeof(V) == 8 && !TR::KV) ? (u32)((reinterpret_cast<uintptr_t>(g) >> 3) & 1u) : 0u;
-        V* const X = X0 + p;
-        const u32 ncell = n > 1 ? n : 1u;  // one cell per element (n <= the tile)
-        if (tid == 0) {
-            s_r[0] = ~0u;
-            s_r[1] = 0u;
-            s_r[2] = ~0u;
-            s_r[3] = 0u;
-            s_r64[0] = ~0ull;
-            s_r64[1] = 0ull;
-            s_flag = 0;
-        }
-#pragma unroll
-        for (int k = 0; k < E / 4; ++k) myrun[k] = make_uint4(0u, 0u, 0u, 0u);
-        // 1. load (element j*NT + tid) and the range of the keys' high 32-bit halves
-        //    (warp reductions in one REDUX instruction each)
-        //    (branch-free over the whole tile: the slots past n load a copy of element n-1,
-        //    which changes no range; they get cells of their own past the leaf's cells)
-        V v[E];
-        u32 hmin = ~0u, hmax = 0u;
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-            const u32 idx = min((u32)(j * NT) + tid, n - 1u);
-            v[j] = CellWork<TR>::in(mem.ld(td.lo + idx));
-            const u32 h = (u32)(TW::key(v[j]) >> 32);
-            hmin = min(hmin, h);
-            hmax = max(hmax, h);
-        }
-        hmin = __reduce_min_sync(0xffffffffu, hmin);
-        hmax = __reduce_max_sync(0xffffffffu, hmax);
-        __syncthreads();  // the range words and the counters are reset; the previous leaf is done
-        BASE_PROF_MARK(1);
-        if (lane == 0) {
-            atomicMin(&s_r[0], hmin);
-            atomicMax(&s_r[1], hmax);
-        }
-        __syncthreads();
-        BASE_PROF_MARK(2);
-        const u32 nxt = s_next[par];
-        if (tid == 0 && nxt < ntasks) {
-            const TaskDesc tn = tasks[nxt];
-            if constexpr (TR::KV) {
-                for (int h = 0; h < 2; ++h) {
-                    const u64* arr = h ? mem.v : mem.k;
-                    const uintptr_t a0 = reinterpret_cast<uintptr_t>(arr + tn.lo) & ~(uintptr_t)15;
-                    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(arr + tn.hi) + 15) & ~(uintptr_t)15;
+        u32 nxt = ntasks;
+        const int r = cell_leaf<TR, NT, E>(td, mem, data, X0, cnt, sh, [&]() {
+            nxt = s_next[par];
+            if (tid == 0 && nxt < ntasks) {
+                // the next leaf's elements into L2 (TMA bulk prefetch)
+                const TaskDesc tn = tasks[nxt];
+                if constexpr (TR::KV) {
+                    for (int h = 0; h < 2; ++h) {
+                        const u64* arr = h ? mem.v : mem.k;
+                        const uintptr_t a0 = reinterpret_cast<uintptr_t>(arr + tn.lo) & ~(uintptr_t)15;
+                        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(arr + tn.hi) + 15) & ~(uintptr_t)15;
+                        if (a1 > a0) bulk_prefetch_l2(reinterpret_cast<const void*>(a0), (u32)(a1 - a0));
+                    }
+                } else {
+                    const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + tn.lo) & ~(uintptr_t)15;
+                    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(data + tn.hi) + 15) & ~(uintptr_t)15;
                     if (a1 > a0) bulk_prefetch_l2(reinterpret_cast<const void*>(a0), (u32)(a1 - a0));
                 }
-            } else {
-                const uintptr_t a0 = reinterpret_cast<uintptr_t>(data + tn.lo) & ~(uintptr_t)15;
-                const uintptr_t a1 = (reinterpret_cast<uintptr_t>(data + tn.hi) + 15) & ~(uintptr_t)15;
-                if (a1 > a0) bulk_prefetch_l2(reinterpret_cast<const void*>(a0), (u32)(a1 - a0));
             }
+        });
+        if (r == 1 && tid == 0) {
+            const u32 q = atomicAdd(fb_count, 1u);
+            if (q < fb_cap) fb_queue[q] = td;
         }
-        // the key range: from the high halves when they are far apart (a conservative range
-        // at most (d+1)/(d-1) wider than the exact one for d = hmax - hmin >= 16); exact from
-        // the low halves when all high halves are equal; exact 64-bit otherwise
-        const u32 H0 = s_r[0], H1 = s_r[1];
-        u64 kmin, span;
-        if (H1 - H0 >= 16u) {
-            kmin = (u64)H0 << 32;
-            span = ((((u64)H1) << 32) | 0xFFFFFFFFull) - kmin;
-        } else if (H1 == H0) {
-            u32 lmin = ~0u, lmax = 0u;
-#pragma unroll
-            for (int j = 0; j < E; ++j) {
-                const u32 l = (u32)TW::key(v[j]);
-                lmin = min(lmin, l);
-                lmax = max(lmax, l);
-            }
-            lmin = __reduce_min_sync(0xffffffffu, lmin);
-            lmax = __reduce_max_sync(0xffffffffu, lmax);
-            if (lane == 0) {
-                atomicMin(&s_r[2], lmin);
-                atomicMax(&s_r[3], lmax);
-            }
-            __syncthreads();
-            kmin = ((u64)H0 << 32) | s_r[2];
-            span = (u64)(s_r[3] - s_r[2]);
-        } else {
-            u64 mn = ~0ull, mx = 0ull;
-#pragma unroll
-            for (int j = 0; j < E; ++j) {
-                const u64 k = TW::key(v[j]);
-                mn = k < mn ? k : mn;
-                mx = k > mx ? k : mx;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const u64 a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
-                mn = a < mn ? a : mn;
-                mx = b > mx ? b : mx;
-            }
-            if (lane == 0) {
-                atomicMin(&s_r64[0], mn);
-                atomicMax(&s_r64[1], mx);
-            }
-            __syncthreads();
-            kmin = s_r64[0];
-            span = s_r64[1] - kmin;
-        }
-        if (span == 0) {  // all keys equal: already sorted (no write)
-            cur = nxt;
-            par ^= 1u;
-            continue;
-        }
-        // cell(key) = floor(x * ncell / (span32 + 1)) for x = (key - kmin) >> s, the top 32
-        // bits of the offset (s = 0 when the span fits 32 bits): one 32x32 multiply-high with
-        // a per-leaf multiplier, monotone, onto [0, ncell).  (mul = floor(ncell * 2^32 /
-        // (span32 + 1)) < 2^32 for span32 >= ncell; otherwise s = 0 and the cell is x itself,
-        // a single key value.)
-        const u32 bl = 64u - (u32)__clzll((long long)span);
-        const u32 sh = bl > 32u ? bl - 32u : 0u;
-        const u32 span32 = (u32)(span >> sh);
-        const u32 mul = span32 >= ncell ? (u32)(((u64)ncell << 32) / ((u64)span32 + 1ull)) : 0u;
-        // 2. cell and rank inside the cell (slots past n: cell = the slot index >= n)
-        const u32 s_cnt = (u32)__cvta_generic_to_shared(cnt);
-        u32 cr[E];  // cell | rank << 16
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-            const u32 idx = j * NT + tid;
-            const u32 x = (u32)((TW::key(v[j]) - kmin) >> sh);
-            u32 c = mul ? __umulhi(x, mul) : x;
-            c = idx < n ? c : idx;
-            cr[j] = c | (atoms_inc(s_cnt + 4u * cpad<E>(c)) << 16);
-        }
-        __syncthreads();
-        BASE_PROF_MARK(3);
-        // 3. exclusive scan of the counts (own run of E cells, 128-bit accesses)
-        u32 sum = 0;
-#pragma unroll
-        for (int k = 0; k < E / 4; ++k) {
-            const uint4 q = myrun[k];
-            sum += q.x + q.y + q.z + q.w;
-        }
-        u32 incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u32 y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= (u32)o) incl += y;
-        }
-        if (lane == 31) s_wsum[w] = incl;
-        __syncthreads();
-        BASE_PROF_MARK(4);
-        u32 base = incl - sum;
-        for (u32 ww = 0; ww < w; ++ww) base += s_wsum[ww];
-        u32 bigwork = 0;  // insertion work of this run's cells (~m^2 / 4 for large cells)
-        {
-            u32 run = base;
-#pragma unroll
-            for (int k = 0; k < E / 4; ++k) {
-                uint4 q = myrun[k];
-                u32 x;
-                x = q.x; q.x = run; run += x; if (x > 8) bigwork += x * x / 4;
-                x = q.y; q.y = run; run += x; if (x > 8) bigwork += x * x / 4;
-                x = q.z; q.z = run; run += x; if (x > 8) bigwork += x * x / 4;
-                x = q.w; q.w = run; run += x; if (x > 8) bigwork += x * x / 4;
-                myrun[k] = q;
-            }
-        }
-        if (bigwork && mul) atomicAdd(&s_flag, bigwork);
-        if (IPS4O_BASE_TMA_WB && tid == 0) bulk_wait_read0();  // the previous leaf has left X
-        __syncthreads();
-        BASE_PROF_MARK(5);
-        if (s_flag > CELL_FIX_BUDGET) {
-            // clustered keys (heavy duplicates in few cells): leave the leaf to the merge sort
-            if (tid == 0) {
-                const u32 q = atomicAdd(fb_count, 1u);
-                if (q < fb_cap) fb_queue[q] = td;
-            }
-            cur = nxt;
-            par ^= 1u;
-            continue;
-        }
-        {
-            const u32 s_x = (u32)__cvta_generic_to_shared(X);
-#pragma unroll
-            for (int j = 0; j < E; ++j) {
-                const u32 pos = lds_u32(s_cnt + 4u * cpad<E>(cr[j] & 0xFFFFu)) + (cr[j] >> 16);
-                sts_v<V>(s_x + pos * (u32)sizeof(V), v[j]);
-            }
-        }
-        __syncthreads();
-        BASE_PROF_MARK(6);
-        // 4. order the cells of this thread's run that hold several elements (PAPER.md:403
-        //    finishes small subproblems by insertion sort): cells of 2-4 elements by a
-        //    4-element sorting network over the cell padded with the largest key (pads never
-        //    move: a comparator swaps only on strictly smaller keys), larger ones by insertion
-        //    sort.  Singleton cells need nothing; nothing at all when every cell is a single
-        //    key value.
-        if (mul) {
-            u32 bs[E + 1];
-#pragma unroll
-            for (int k = 0; k < E / 4; ++k) {
-                const uint4 q = myrun[k];
-                bs[4 * k] = q.x;
-                bs[4 * k + 1] = q.y;
-                bs[4 * k + 2] = q.z;
-                bs[4 * k + 3] = q.w;
-            }
-            bs[E] = tid + 1 < (u32)NT ? cnt[cpad<E>((tid + 1) * E)] : (u32)CB::TILE;
-            // cells of 2 (most multi-element cells), of 3-4 and larger ones in separate
-            // loops, so that a warp's lanes run the same code in each
-            u32 m2 = 0, m34 = 0, mbig = 0;
-#pragma unroll
-            for (int k = 0; k < E; ++k) {
-                const u32 m = bs[k + 1] - bs[k];
-                m2 |= (m == 2u ? 1u : 0u) << k;
-                m34 |= (m - 3u <= 1u ? 1u : 0u) << k;
-                mbig |= (m > 4u ? 1u : 0u) << k;
-            }
-            const u32 enext = bs[E];
-            while (m2) {
-                const u32 k = (u32)__ffs(m2) - 1u;
-                m2 &= m2 - 1u;
-                const u32 b = cnt[cpad<E>(tid * E + k)];
-                const V x0 = X[b], x1 = X[b + 1];
-                if (TW::less(x1, x0)) {
-                    X[b] = x1;
-                    X[b + 1] = x0;
-                }
-            }
-            while (m34) {
-                const u32 k = (u32)__ffs(m34) - 1u;
-                m34 &= m34 - 1u;
-                const u32 b = cnt[cpad<E>(tid * E + k)];
-                const u32 e = k + 1 < (u32)E ? cnt[cpad<E>(tid * E + k + 1)] : enext;
-                const V pd = TW::pad();
-                V x0 = X[b], x1 = X[b + 1], x2 = X[b + 2];
-                V x3 = e - b > 3u ? X[b + 3] : pd;
-                auto cas = [](V& lo, V& hi) {
-                    const bool sw = TW::less(hi, lo);
-                    const V t = sw ? hi : lo;
-                    hi = sw ? lo : hi;
-                    lo = t;
-                };
-                cas(x0, x1);
-                cas(x2, x3);
-                cas(x0, x2);
-                cas(x1, x3);
-                cas(x1, x2);
-                X[b] = x0;
-                X[b + 1] = x1;
-                X[b + 2] = x2;
-                if (e - b > 3u) X[b + 3] = x3;
-            }
-            while (mbig) {
-                const u32 k = (u32)__ffs(mbig) - 1u;
-                mbig &= mbig - 1u;
-                const u32 b = cnt[cpad<E>(tid * E + k)];
-                const u32 e = k + 1 < (u32)E ? cnt[cpad<E>(tid * E + k + 1)] : enext;
-                for (u32 i = b + 1; i < e; ++i) {
-                    const V x = X[i];
-                    u32 q = i;
-                    while (q > b && TW::less(x, X[q - 1])) {
-                        X[q] = X[q - 1];
-                        --q;
-                    }
-                    X[q] = x;
-                }
-            }
-        }
-        if constexpr (TR::KV) {
-            // 5. write back: key and value arrays by coalesced stores
-            __syncthreads();
-            for (u32 i = tid; i < n; i += NT) mem.st(td.lo + i, CellWork<TR>::out(X[i]));
-            cur = nxt;
-            par ^= 1u;
-            continue;
-        }
-        if constexpr (!std::is_same<TW, TR>::value) {
-            __syncthreads();
-            for (u32 i = tid; i < n; i += NT) X[i] = CellWork<TR>::out(X[i]);
-        }
-#if IPS4O_BASE_TMA_WB
-        fence_proxy_async_smem();
-        __syncthreads();
-        BASE_PROF_MARK(7);
-        // 5. write back: the 16-byte aligned body by one TMA bulk store (read before the next
-        //    leaf's scatter), the element before / after it by plain stores
-        {
-            const u32 i0 = p < n ? p : n;
-            const u32 i1 = sizeof(V) == 8 ? i0 + ((n - i0) & ~1u) : n;
-            if (tid == 0 && i1 > i0) {
-                bulk_s2g(g + i0, X + i0, (i1 - i0) * (u32)sizeof(V));
-                bulk_commit();
-            }
-            if (tid == 32 && i0 > 0) g[0] = X[0];
-            if (tid == 64 && i1 < n) g[n - 1] = X[n - 1];
-        }
-#else
-        __syncthreads();
-        BASE_PROF_MARK(7);
-        // 5. write back
-        for (u32 i = tid; i < n; i += NT) g[i] = X[i];
-#endif
         cur = nxt;
         par ^= 1u;
     }
     if (IPS4O_BASE_TMA_WB && tid == 0) bulk_wait0();
-    BASE_PROF_FLUSH(NT >= 512 ? 1 : 0);
 }
 
 template <class TR, int THREADS, int ITEMS>

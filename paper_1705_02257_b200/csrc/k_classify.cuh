@@ -548,6 +548,84 @@ __device__ __forceinline__ void k2_drain(typename TR::V* buf, K2Defer<TR, E>& df
     __syncthreads();
 }
 
+// Local classification of one stripe by the whole CTA: the stripe's front
+// receives s_nflushed full blocks; per bucket fill / cnt / nbl count its buffered elements,
+// flushed blocks and total; the partially filled buffers stay in buf (deferred elements
+// joined).  The task's classifier is in shared memory (spl, lut, rtree); fill, cnt, nbl and
+// *s_nflushed are zero on entry.  s_mbar: two initialised mbarriers with their phase bits.
+template <class TR, int NT, int E>
+__device__ __forceinline__ void k2_stripe(const Mem<TR>& mem, const StripeDesc& sd, const TaskParam& tp,
+                                          typename TR::V* buf, u64* rtree, u64* spl, u32* fill, u32* cnt, u32* slotb,
+                                          u32* nfl, u32* nbl, typename TR::V* stage, unsigned short* lut,
+                                          u32* s_nflushed_p, u64* s_mbar, u32& phase) {
+    constexpr int B = TR::B;
+    constexpr u32 TILE = NT * E;
+    const u32 tid = threadIdx.x;
+    u32& s_nflushed = *s_nflushed_p;
+    const u64 mb = sd.begin > tp.g ? sd.begin : tp.g;  // stripe main region start (block aligned)
+    const u64 me = sd.end;
+    K2Defer<TR, E> df;
+    df.mask = 0;
+    bool agg = false;  // skewed tiles: aggregate the atomics of uniform warps
+    const u32 cap = me > mb ? (u32)((me - mb) / B) : 0u;
+    if (mb < me) {
+        // full tiles: staged in shared memory by TMA bulk loads two tiles ahead (a tile
+        // is contiguous: one cp.async.bulk each, completion on the stage's mbarrier);
+        // then the (single) partial tail tile by direct 128-bit loads
+        const u64 nft = (me - mb) / TILE;
+        uint4 cur[E / TR::VEC];
+        constexpr u32 ALL = (E >= 32) ? 0xFFFFFFFFu : ((1u << E) - 1u);
+        if (tid == 0) {
+            for (u64 k = 0; k < (u64)K2_STAGES && k < nft; ++k)
+                k2_stage_load<TR, NT, E>(stage + k * TILE, mem, mb + k * TILE, &s_mbar[k]);
+        }
+        for (u64 ti = 0; ti < nft; ++ti) {
+            const u32 st = K2_STAGES == 2 ? (u32)(ti & 1) : 0u;
+            mbar_wait(&s_mbar[st], (phase >> st) & 1u);
+            phase ^= 1u << st;
+            k2_stage_read<TR, NT, E>(stage + st * TILE, cur);
+            // two stages: the tile's first barrier follows every thread's reads of the
+            // stage, and the refill for tile ti+2 is issued after it, inside k2_tile; one
+            // stage: an extra barrier here, then the load of tile ti+1
+            u64 refill = ~0ull;
+            if (K2_STAGES == 2) {
+                refill = ti + 2 < nft ? mb + (ti + 2) * TILE : ~0ull;
+            } else {
+                __syncthreads();
+                if (tid == 0 && ti + 1 < nft) {
+                    fence_proxy_async_smem();
+                    k2_stage_load<TR, NT, E>(stage, mem, mb + (ti + 1) * TILE, &s_mbar[0]);
+                }
+            }
+            if (tp.logk == 8 && !agg)
+                k2_tile<TR, NT, E, 8, false>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                                             slotb, nfl, s_nflushed_p, tp.logk, tp.kprime, tp.eq,
+                                             refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);
+            else
+                k2_tile<TR, NT, E, 0, true>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                                            slotb, nfl, s_nflushed_p, tp.logk, tp.kprime, tp.eq,
+                                            refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);
+        }
+        const u64 tb = mb + nft * TILE;
+        if (tb < me) {
+            const u32 vt = k2_load<TR, NT, E>(mem, tb, (u32)(me - tb), cur);
+            k2_tile<TR, NT, E, 0, true>(mem, cur, vt, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                                  slotb, nfl, s_nflushed_p, tp.logk, tp.kprime, tp.eq,
+                                  ~0ull, nullptr, nullptr, df, agg, lut, tp.lut_lo, tp.lut_sh);
+        }
+    }
+    if (sd.first && tp.lo < tp.g) {
+        // head elements [lo, g) of the task, processed last so that every write stays
+        // behind the read frontier (their block grid starts at g)
+        const u64 hend = tp.g < tp.hi ? tp.g : tp.hi;
+        uint4 hv[E / TR::VEC];
+        const u32 hval = k2_load<TR, NT, E>(mem, tp.lo, (u32)(hend - tp.lo), hv);
+        k2_tile<TR, NT, E, 0, true>(mem, hv, hval, true, mb, cap, buf, nbl, rtree, spl, fill, cnt, slotb, nfl,
+                       s_nflushed_p, tp.logk, tp.kprime, tp.eq, ~0ull, nullptr, nullptr, df, agg, lut, tp.lut_lo, tp.lut_sh);
+    }
+    k2_drain<TR, E>(buf, df);
+}
+
 template <class TR, int NT, int E, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A0) {
     const LevelArgs A = with_dyn(A0);
@@ -605,68 +683,8 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A0) {
         }
         if (tid == 0) s_nflushed = 0;
         __syncthreads();
-        const u64 mb = sd.begin > tp.g ? sd.begin : tp.g;  // stripe main region start (block aligned)
-        const u64 me = sd.end;
-        K2Defer<TR, E> df;
-        df.mask = 0;
-        bool agg = false;  // skewed tiles: aggregate the atomics of uniform warps
-        const u32 cap = me > mb ? (u32)((me - mb) / B) : 0u;
-        if (mb < me) {
-            // full tiles: staged in shared memory by TMA bulk loads two tiles ahead (a tile
-            // is contiguous: one cp.async.bulk each, completion on the stage's mbarrier);
-            // then the (single) partial tail tile by direct 128-bit loads
-            const u64 nft = (me - mb) / TILE;
-            uint4 cur[E / TR::VEC];
-            constexpr u32 ALL = (E >= 32) ? 0xFFFFFFFFu : ((1u << E) - 1u);
-            if (tid == 0) {
-                for (u64 k = 0; k < (u64)K2_STAGES && k < nft; ++k)
-                    k2_stage_load<TR, NT, E>(stage + k * TILE, mem, mb + k * TILE, &s_mbar[k]);
-            }
-            for (u64 ti = 0; ti < nft; ++ti) {
-                const u32 st = K2_STAGES == 2 ? (u32)(ti & 1) : 0u;
-                mbar_wait(&s_mbar[st], (phase >> st) & 1u);
-                phase ^= 1u << st;
-                k2_stage_read<TR, NT, E>(stage + st * TILE, cur);
-                // two stages: the tile's first barrier follows every thread's reads of the
-                // stage, and the refill for tile ti+2 is issued after it, inside k2_tile; one
-                // stage: an extra barrier here, then the load of tile ti+1
-                u64 refill = ~0ull;
-                if (K2_STAGES == 2) {
-                    refill = ti + 2 < nft ? mb + (ti + 2) * TILE : ~0ull;
-                } else {
-                    __syncthreads();
-                    if (tid == 0 && ti + 1 < nft) {
-                        fence_proxy_async_smem();
-                        k2_stage_load<TR, NT, E>(stage, mem, mb + (ti + 1) * TILE, &s_mbar[0]);
-                    }
-                }
-                if (tp.logk == 8 && !agg)
-                    k2_tile<TR, NT, E, 8, false>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
-                                                 slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
-                                                 refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);
-                else
-                    k2_tile<TR, NT, E, 0, true>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
-                                                slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
-                                                refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);
-            }
-            const u64 tb = mb + nft * TILE;
-            if (tb < me) {
-                const u32 vt = k2_load<TR, NT, E>(mem, tb, (u32)(me - tb), cur);
-                k2_tile<TR, NT, E, 0, true>(mem, cur, vt, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
-                                      slotb, nfl, &s_nflushed, tp.logk, tp.kprime, tp.eq,
-                                      ~0ull, nullptr, nullptr, df, agg, lut, tp.lut_lo, tp.lut_sh);
-            }
-        }
-        if (sd.first && tp.lo < tp.g) {
-            // head elements [lo, g) of the task, processed last so that every write stays
-            // behind the read frontier (their block grid starts at g)
-            const u64 hend = tp.g < tp.hi ? tp.g : tp.hi;
-            uint4 hv[E / TR::VEC];
-            const u32 hval = k2_load<TR, NT, E>(mem, tp.lo, (u32)(hend - tp.lo), hv);
-            k2_tile<TR, NT, E, 0, true>(mem, hv, hval, true, mb, cap, buf, nbl, rtree, spl, fill, cnt, slotb, nfl,
-                           &s_nflushed, tp.logk, tp.kprime, tp.eq, ~0ull, nullptr, nullptr, df, agg, lut, tp.lut_lo, tp.lut_sh);
-        }
-        k2_drain<TR, E>(buf, df);
+        k2_stripe<TR, NT, E>(mem, sd, tp, buf, rtree, spl, fill, cnt, slotb, nfl, nbl, stage, lut, &s_nflushed, s_mbar,
+                             phase);
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area
         u32 f = tid < (u32)MAXK ? fill[tid] : 0u;
         u32 incl = f;

@@ -32,7 +32,9 @@ __device__ __forceinline__ typename TR::V ovf_get(const void* ovf_block, u32 i) 
 }
 
 // Emission decision for bucket b of task tp (PAPER.md:342 for equality buckets): returns
-// 0..3 = base-case class, 4 = next-level task, 5 = nothing; *td = the task.
+// 0..3 = base-case class, 4 = next-level task, 5 = nothing, 6 = the single-CTA tier (medium
+// tasks: "assign remaining problems ... which sort them sequentially");
+// *td = the task.
 template <class TR>
 __device__ __forceinline__ u32 emit_kind(const LevelArgs& A, const TaskParam& tp, u32 b, u64 e0, u64 e1,
                                          TaskDesc* td) {
@@ -56,6 +58,9 @@ __device__ __forceinline__ u32 emit_kind(const LevelArgs& A, const TaskParam& tp
         return base_class<TR>(sz);
     }
     *td = TaskDesc{e0, e1, part, 0u};
+    if constexpr (!TR::WIDE) {
+        if (sz <= A.medium_max) return 6u;
+    }
     return 4u;
 }
 
@@ -255,15 +260,16 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup(LevelArgs A0) {
             }
         }
         __syncwarp();
-        // the group's tasks: lane q (< 5) reserves the slots of queue q with one atomic
-        if (A.emit && lane < 5u) {
+        // the group's tasks: lane q (queue q: 0-3 base classes, 4 next level, 6 medium)
+        // reserves the queue's slots with one atomic
+        if (A.emit && lane < 7u && lane != 5u) {
             u32 cntq = 0;
 #pragma unroll
             for (u32 gi = 0; gi < K4_GROUP; ++gi) cntq += s_kind[gi] == lane ? 1u : 0u;
             if (cntq) {
-                u32* ctr = lane < 4u ? &A.ctr[CTR_BASE0 + lane] : &A.ctr[CTR_NEXT];
-                TaskDesc* q = lane < 4u ? A.q_base + A.qb_off[lane] : A.q_next;
-                const u32 cap = lane < 4u ? A.qb_cap[lane] : A.qn_cap;
+                u32* ctr = lane < 4u ? &A.ctr[CTR_BASE0 + lane] : lane == 4u ? &A.ctr[CTR_NEXT] : &A.ctr[CTR_MED];
+                TaskDesc* q = lane < 4u ? A.q_base + A.qb_off[lane] : lane == 4u ? A.q_next : A.q_med;
+                const u32 cap = lane < 4u ? A.qb_cap[lane] : lane == 4u ? A.qn_cap : A.qm_cap;
                 u32 i = atomicAdd(ctr, cntq);
                 for (u32 gi = 0; gi < K4_GROUP; ++gi) {
                     if (s_kind[gi] != lane) continue;
@@ -417,6 +423,10 @@ __global__ void __launch_bounds__(K4_THREADS) k_cleanup_cta(LevelArgs A0) {
         } else if (kd == 4u) {
             const u32 i = atomicAdd(&A.ctr[CTR_NEXT], 1u);
             if (i < A.qn_cap) A.q_next[i] = td;
+            else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
+        } else if (kd == 6u) {
+            const u32 i = atomicAdd(&A.ctr[CTR_MED], 1u);
+            if (i < A.qm_cap) A.q_med[i] = td;
             else atomicOr(&A.ctr[CTR_ERROR], (u32)ERR_QUEUE);
         }
     }

@@ -42,7 +42,8 @@ __device__ void build_lut_block(const u64* s_dist, u32 nd, u32 kp, unsigned shor
         const u32 bl = 64u - (u32)__clzll((long long)span);
         sh = bl > LUT_LOG ? bl - LUT_LOG : 0u;  // span >> sh < LUT_N
     }
-    const u32 tid = threadIdx.x, nt = blockDim.x, per = LUT_N / nt, lane = tid & 31, w = tid >> 5;
+    // thread t owns cells [t*per, (t+1)*per) (any block size: the last owners may own none)
+    const u32 tid = threadIdx.x, nt = blockDim.x, per = (LUT_N + nt - 1) / nt, lane = tid & 31, w = tid >> 5;
     for (u32 c = tid; c < LUT_N; c += nt) scr[c] = 0u;
     __syncthreads();
     for (u32 i = 1 + tid; i < kp; i += nt) {
@@ -53,7 +54,7 @@ __device__ void build_lut_block(const u64* s_dist, u32 nd, u32 kp, unsigned shor
     }
     __syncthreads();
     u32 sum = 0;
-    for (u32 k = 0; k < per; ++k) {
+    for (u32 k = 0; k < per && tid * per + k < LUT_N; ++k) {
         const u32 x = scr[tid * per + k];
         sum += (x & 0xFFFFu) + (x >> 16);
     }
@@ -67,7 +68,7 @@ __device__ void build_lut_block(const u64* s_dist, u32 nd, u32 kp, unsigned shor
     __syncthreads();
     u32 run = incl - sum;
     for (u32 ww = 0; ww < w; ++ww) run += s_ws[ww];
-    for (u32 k = 0; k < per; ++k) {
+    for (u32 k = 0; k < per && tid * per + k < LUT_N; ++k) {
         const u32 c = tid * per + k, x = scr[c];
         const u32 eqc = x >> 16, gtc = x & 0xFFFFu;
         g_lut[c] = (unsigned short)((run + eqc) | gtc << 8);

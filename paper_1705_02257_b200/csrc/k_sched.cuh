@@ -63,7 +63,13 @@ __global__ void k_init(LevelArgs A0, void* data, void* vals, u64 n, u64 seed, u3
     Q->ca = 0;
     Q->seed = seed;
     Q->ntot = n;
-    if (small_class >= NUM_BASE_CLASSES) {
+    if (small_class == NUM_BASE_CLASSES + 1) {
+        // a medium problem: one CTA sorts it (the single-CTA tier, k_cta.cuh)
+        Q->na = 0;
+        Q->level = 0;
+        A0.q_med[0] = TaskDesc{0, n, 0u, 0u};
+        A0.ctr[CTR_MED] = 1;
+    } else if (small_class >= NUM_BASE_CLASSES) {
         A0.q_lvl0[0] = TaskDesc{0, n, 0u, 0u};
         Q->na = 1;
         Q->level = 1;
@@ -332,6 +338,7 @@ __global__ void k_epi(LevelArgs A0, cudaGraphConditionalHandle h, u32 use_handle
     }
     st[DS_BASE_TASKS] += nb;
     st[DS_FALLBACK] += ctr[CTR_FB];
+    st[DS_MED_TASKS] += ctr[CTR_MED];
     st[DS_BLOCK_MOVES] += ctr[CTR_BMOVES];
     st[DS_AMOVES] += ctr[CTR_AMOVES];
     st[DS_BASE_ELEMS] += *A0.base_elems;

@@ -505,3 +505,35 @@ def test_type_switching_and_reuse():
 
 
 # (v) full BASELINE sizes: tests/test_full_parity.py (element-wise oracle parity)
+
+
+# ------------------------------------------------------------ the single-CTA tier
+
+def _tier_run(medium_max, specs):
+    import json as _json
+    import os as _os
+    import subprocess as _sp
+    import sys as _sys
+    env = dict(_os.environ, IPS4O_MEDIUM_MAX=str(medium_max))
+    here = _os.path.dirname(_os.path.abspath(__file__))
+    out = _sp.run([_sys.executable, _os.path.join(here, "tier_check.py"), *specs], env=env, capture_output=True,
+                  text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return _json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def test_single_cta_tier_vs_oracle():
+    """Every task of <= 2^30 elements sorted by one CTA with the strictly in-place driver
+    (k_cta.cuh): all distributions and the 8/16-byte types, sizes from one
+    partition to several levels inside the CTA (recursion through searchNextLargest with
+    bucket-maximum marking on skewed inputs)."""
+    specs = [f"{d}:{n}:{s}" for d, n, s in [
+        ("uniform", 20_000, 1), ("uniform", 70_001, 2), ("uniform", 1 << 20, 3), ("uniform", (1 << 22) + 7, 1),
+        ("f64_exponential", 300_007, 2), ("rootdup", 1 << 21, 1), ("twodup", 1 << 21, 2), ("eightdup", 1 << 21, 3),
+        ("almostsorted", 1 << 20, 1), ("reversesorted", 1 << 20, 1), ("zeros", 1 << 20, 1), ("ones", 100_000, 1),
+        ("sorted", 1 << 20, 2), ("pair16", 500_001, 1), ("pair_f64", 300_001, 2)]]
+    res = _tier_run(1 << 30, specs)
+    for r in res:
+        assert r["ok"] and r["err"] == 0, r
+    assert all(r["medium_tasks"] >= 1 for r in res if not r["spec"].startswith(("zeros", "ones")))
+    assert sum(r["medium_marks"] for r in res) > 0     # the marking path ran (recursion inside a CTA)
