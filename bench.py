@@ -53,6 +53,8 @@ CONFIGS = {
     "C5": ("rec100", 24, "C5: 2^24 100-byte records (10-byte key)"),
     "F3_pair_f64": ("pair_f64", 27, "f3: 2^27 the paper's Pair (f64 key uniform [0,1) + f64 payload)"),
     "F3_quartet": ("quartet_f64", 26, "f3: 2^26 the paper's Quartet (three f64 keys, lexicographic, + payload)"),
+    "C4_kv": ("pair16", 27, "C4 as structure of arrays: 2^27 u64 keys uniform [0,2^32) + u64 values = index, "
+                            "ips4o_sort_kv (in place)"),
 }
 DTYPE = {W.ELEM_U64: "u64", W.ELEM_F64: "f64", W.ELEM_PAIR: "u64x2", W.ELEM_REC100: "u8x100",
          W.ELEM_PAIR_F64: "f64x2", W.ELEM_QUARTET_F64: "f64x4"}
@@ -301,14 +303,23 @@ def run_ours(args):
     et, a, desc = make_input(args.config, args.n)
     n = a.shape[0]
     esize = W.ELEM_SIZE[et]
-    pristine = host_to_device(a, et)
+    kv = args.config.endswith("_kv")
+    if kv:
+        # structure of arrays: row 0 the keys, row 1 the values (each row contiguous)
+        import numpy as _np
+        pristine = torch.from_numpy(_np.ascontiguousarray(a.T).view(_np.int64)).cuda().view(torch.uint64)
+    else:
+        pristine = host_to_device(a, et)
     ver = OracleVerify(a, et) if (rank == 0 and not args.no_verify) else None
     work = pristine.clone()
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
 
     def one_sort():
-        ips4o.ips4o_sort(work.data_ptr(), n, et, sptr)
+        if kv:
+            ips4o.ips4o_sort_kv(work[0].data_ptr(), work[1].data_ptr(), n, W.ELEM_U64, sptr)
+        else:
+            ips4o.ips4o_sort(work.data_ptr(), n, et, sptr)
 
     for _ in range(max(args.warmup, 0)):
         work.copy_(pristine)
@@ -352,11 +363,11 @@ def run_ours(args):
     if ws > 1:
         mean_ms = replica_ms(step_ms, "cuda")
     # verify the last output against the oracle (never report an unverified run)
-    ok = ver.check(work) if ver else None
+    ok = ver.check(work.t().contiguous() if kv else work) if ver else None
 
     # end-to-end: host (pinned) buffer -> device -> sort -> host, through the C ABI
     e2e = None
-    if rank == 0 and args.e2e_steps > 0:
+    if rank == 0 and args.e2e_steps > 0 and not kv:
         h = torch.empty(tuple(work.shape), dtype=work.dtype, pin_memory=True)
         hsrc = pristine.cpu().pin_memory()
         e2e_t = []

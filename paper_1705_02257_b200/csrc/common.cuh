@@ -151,8 +151,8 @@ struct TQuad {
     static constexpr int S = 32, B = BLOCK_BYTES / 32, VEC = 0, CAP = 4096, TYPE = 5, PARTS = 3, RW = 8;
     static constexpr bool WIDE = true, F64KEY = true, KV = false;
     static constexpr u32 LEAF = 2048;
-    static constexpr u32 C0MAX = 4096, C1MAX = 4096, C2MAX = 4096;  // one class: the merge-sort base case
-    __device__ __forceinline__ static u64 key(const V& v, u32 part) { return TF64::key(v.w[part]); }
+    static constexpr u32 C0MAX = 2048, C1MAX = 4096, C2MAX = 4096;  // base-case classes (cells on k0)
+    __device__ __forceinline__ static u64 key(const V& v, u32 part = 0) { return TF64::key(v.w[part]); }
     __device__ __forceinline__ static u64 key_w(const u32* w, u32 part) {
         return TF64::key(((u64)w[2 * part + 1] << 32) | w[2 * part]);
     }

@@ -428,6 +428,8 @@ static int prepare_kernels(void) {
             CK(cudaFuncSetAttribute(k_base_rec<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase<4>::smem));
             g_ws.cell_grid[0] = g_ws.cell_grid[1] = 4u * nsm;
         } else {
+            CK((cell_setup<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>(&g_ws.cell_grid[0], nsm)));
+            CK((cell_setup<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>(&g_ws.cell_grid[1], nsm)));
             typedef MergeCfg<TR> M;
             CK(cudaFuncSetAttribute(k_base_merge<TR, M::TH, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)M::BC::smem));
@@ -552,10 +554,17 @@ static int enqueue_base(Enq& q) {
         STAMP(KK_BASE);
         return IPS4O_OK;
     } else if constexpr (TR::WIDE) {
-        // quartets: one class, sorted by the merge sort (lexicographic order of three keys)
+        // quartets: two cell classes (cells on k0, cells ordered by the lexicographic key), then
+        // the merge sort for the leaves they hand back (equal or clustered k0)
+        int rc = enqueue_cell<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>(q, st, 0);
+        if (rc) return rc;
+        STAMP(KK_BASE);
+        rc = enqueue_cell<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>(q, st, 1);
+        if (rc) return rc;
+        STAMP(KK_BASE);
         typedef MergeCfg<TR> M;
         LAUNCH(KK_BASE, (k_base_merge<TR, M::TH, 16><<<g_ws.cell_grid[4], M::TH, M::BC::smem, st>>>(
-                             A.q_base + A.qb_off[0], 0u, A.ctr + CTR_BASE0 + 0, A.dyn, A.qb_cap[0])));
+                             A.q_fb, 0u, A.ctr + CTR_FB, A.dyn, A.q_cap)));
         STAMP(KK_BASE);
         return IPS4O_OK;
     } else {

@@ -441,13 +441,20 @@ template <> struct CellWork<TKV> {  // key-value pairs: sorted as {key, value} p
     __device__ __forceinline__ static ulonglong2 out(ulonglong2 v) { return v; }
 };
 template <> struct CellWork<TKVF64> : CellWork<TPairF64> {};
+// quartets: cells on the image of k0, the cells' elements ordered by the full lexicographic key
+template <> struct CellWork<TQuad> {
+    typedef TQuad T;
+    __device__ __forceinline__ static Quad in(const Quad& v) { return v; }
+    __device__ __forceinline__ static Quad out(const Quad& v) { return v; }
+};
 
 template <class TR, int NT, int E>
 struct CellMinB {
     static constexpr int v = sizeof(typename TR::V) == 8
                                  ? (E >= 16 ? (NT <= 128 ? 6 : NT <= 256 ? 3 : NT <= 384 ? 2 : 1)
                                             : (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 512 ? 2 : 1))
-                                 : (NT <= 256 ? 3 : 1);
+                             : sizeof(typename TR::V) == 16 ? (NT <= 256 ? 3 : NT <= 512 ? 2 : 1)
+                                                            : (NT <= 256 ? 2 : 1);
 };
 __device__ __forceinline__ u32 atoms_inc(u32 saddr) {
     u32 r;
@@ -466,9 +473,13 @@ __device__ __forceinline__ void sts_v(u32 saddr, const V& v) {
         memcpy(&x, &v, 8);
         asm volatile("st.shared.u64 [%0], %1;" ::"r"(saddr), "l"(x));
     } else {
-        ulonglong2 x;
-        memcpy(&x, &v, 16);
-        asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(saddr), "l"(x.x), "l"(x.y));
+        static_assert(sizeof(V) % 16 == 0, "16-byte multiples");
+#pragma unroll
+        for (u32 o = 0; o < sizeof(V); o += 16) {
+            ulonglong2 x;
+            memcpy(&x, reinterpret_cast<const char*>(&v) + o, 16);
+            asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(saddr + o), "l"(x.x), "l"(x.y));
+        }
     }
 }
 // Leaves are taken from the class queue through an atomic ticket (the grid is the resident
@@ -501,7 +512,6 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
     // memory, so that its aligned body leaves by one TMA bulk store
     const u32 p = (sizeof(V) == 8 && !TR::KV) ? (u32)((reinterpret_cast<uintptr_t>(g) >> 3) & 1u) : 0u;
     V* const X = X0 + p;
-    const u32 ncell = n > 1 ? n : 1u;  // one cell per element (n <= the tile)
     if (tid == 0) {
         S.r[0] = ~0u;
         S.r[1] = 0u;
@@ -516,7 +526,7 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
     // 1. load (element j*NT + tid) and the range of the keys' high 32-bit halves
     //    (warp reductions in one REDUX instruction each)
     //    (branch-free over the whole tile: the slots past n load a copy of element n-1,
-    //    which changes no range; they get cells of their own past the leaf's cells)
+    //    which changes no range; they take no part in the steps below)
     V v[E];
     u32 hmin = ~0u, hmax = 0u;
 #pragma unroll
@@ -585,7 +595,9 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
         kmin = S.r64[0];
         span = S.r64[1] - kmin;
     }
-    if (span == 0) return 0;  // all keys equal: already sorted (no write)
+    // all keys equal: already sorted (no write) -- for keys of several parts (quartets) only
+    // the first part is equal: the merge sort orders the rest
+    if (span == 0) return TR::PARTS > 1 ? 1 : 0;
     // cell(key) = floor(x * ncell / (span32 + 1)) for x = (key - kmin) >> s, the top 32
     // bits of the offset (s = 0 when the span fits 32 bits): one 32x32 multiply-high with
     // a per-leaf multiplier, monotone, onto [0, ncell).  (mul = floor(ncell * 2^32 /
@@ -594,17 +606,20 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
     const u32 bl = 64u - (u32)__clzll((long long)span);
     const u32 sh = bl > 32u ? bl - 32u : 0u;
     const u32 span32 = (u32)(span >> sh);
+    // cells: one per key value when the span fits the tile (nothing to order inside a cell),
+    // else one per element (at most one element per cell on average)
+    const u32 ncell = span < (u64)CB::TILE ? max(n, (u32)span + 1u) : n;
     const u32 mul = span32 >= ncell ? (u32)(((u64)ncell << 32) / ((u64)span32 + 1ull)) : 0u;
-    // 2. cell and rank inside the cell (slots past n: cell = the slot index >= n)
+    // 2. cell and rank inside the cell
     const u32 s_cnt = (u32)__cvta_generic_to_shared(cnt);
     u32 cr[E];  // cell | rank << 16
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-        const u32 idx = j * NT + tid;
-        const u32 x = (u32)((TW::key(v[j]) - kmin) >> sh);
-        u32 c = mul ? __umulhi(x, mul) : x;
-        c = idx < n ? c : idx;
-        cr[j] = c | (atoms_inc(s_cnt + 4u * cpad<E>(c)) << 16);
+        if (j * NT + tid < n) {
+            const u32 x = (u32)((TW::key(v[j]) - kmin) >> sh);
+            const u32 c = mul ? __umulhi(x, mul) : x;
+            cr[j] = c | (atoms_inc(s_cnt + 4u * cpad<E>(c)) << 16);
+        }
     }
     __syncthreads();
     BASE_PROF_MARK(3);
@@ -640,7 +655,7 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
             myrun[k] = q;
         }
     }
-    if (bigwork && mul) atomicAdd(&S.flag, bigwork);
+    if (bigwork && (mul || TR::PARTS > 1)) atomicAdd(&S.flag, bigwork);
     if (IPS4O_BASE_TMA_WB && tid == 0) bulk_wait_read0();  // the previous leaf has left X
     __syncthreads();
     BASE_PROF_MARK(5);
@@ -649,8 +664,10 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
         const u32 s_x = (u32)__cvta_generic_to_shared(X);
 #pragma unroll
         for (int j = 0; j < E; ++j) {
-            const u32 pos = lds_u32(s_cnt + 4u * cpad<E>(cr[j] & 0xFFFFu)) + (cr[j] >> 16);
-            sts_v<V>(s_x + pos * (u32)sizeof(V), v[j]);
+            if (j * NT + tid < n) {
+                const u32 pos = lds_u32(s_cnt + 4u * cpad<E>(cr[j] & 0xFFFFu)) + (cr[j] >> 16);
+                sts_v<V>(s_x + pos * (u32)sizeof(V), v[j]);
+            }
         }
     }
     __syncthreads();
@@ -661,7 +678,7 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
     //    move: a comparator swaps only on strictly smaller keys), larger ones by insertion
     //    sort.  Singleton cells need nothing; nothing at all when every cell is a single
     //    key value.
-    if (mul) {
+    if (mul || TR::PARTS > 1) {  // (cells of one key part value may differ in the later parts)
         u32 bs[E + 1];
 #pragma unroll
         for (int k = 0; k < E / 4; ++k) {
@@ -671,7 +688,7 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
             bs[4 * k + 2] = q.z;
             bs[4 * k + 3] = q.w;
         }
-        bs[E] = tid + 1 < (u32)NT ? cnt[cpad<E>((tid + 1) * E)] : (u32)CB::TILE;
+        bs[E] = tid + 1 < (u32)NT ? cnt[cpad<E>((tid + 1) * E)] : n;
         // cells of 2 (most multi-element cells), of 3-4 and larger ones in separate
         // loops, so that a warp's lanes run the same code in each
         u32 m2 = 0, m34 = 0, mbig = 0;
