@@ -30,6 +30,10 @@ constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
 #define IPS4O_K2_STAGES (IPS4O_K2_LUT ? 2 : 1)
 #endif
 constexpr int K2_STAGES = IPS4O_K2_STAGES;   // tiles staged ahead in K2 (TMA)
+#ifndef IPS4O_K2_MAIN_STAGES  // the multi-CTA K2 kernel's stages (the single-CTA tier keeps K2_STAGES)
+#define IPS4O_K2_MAIN_STAGES K2_STAGES
+#endif
+constexpr int K2_MAIN_STAGES = IPS4O_K2_MAIN_STAGES;
 // replicated splitter tree in K2: 16 copies (conflict-free lookups) when shared memory
 // allows, else 8 (lanes l, l+8 of a half-warp share a copy)
 constexpr int TREE_COPIES = K2_STAGES == 1 ? 16 : 8;
@@ -338,6 +342,8 @@ struct LevelArgs {
     TaskDesc* q_med;  // [qm_cap] medium tasks of the batch (single-CTA tier, k_cta.cuh)
     u32 qm_cap;
     u64 medium_max;   // tasks of base_cap < n <= medium_max go to the single-CTA tier (0: none)
+    u64 wave_elems;   // levels >= 2: at most this many elements per batch (L2-sized waves; 0: off)
+    u64 wave_stripe;  // minimum stripe length of a wave batch (elements)
     TaskDesc* q_lvl0; // [qn_cap] level queue A
     TaskDesc* q_lvl1; // [qn_cap] level queue B
     u32 qb_off[4], qb_cap[4];

@@ -239,6 +239,30 @@ static u64 medium_max() {
     return (u64)v;
 }
 
+// Levels >= 2 run in L2-sized waves: a batch holds at most IPS4O_WAVE elements (environment, read
+// once; 0 = off), so that a wave's blocks, written by K2 and K3, are still in L2 when K3 and the
+// base case read them (§4.7: the last level sorted while the buckets are in
+// cache).  IPS4O_WAVE_STRIPE: minimum stripe length inside a wave.
+#ifndef IPS4O_WAVE
+#define IPS4O_WAVE 0ll
+#endif
+#ifndef IPS4O_WAVE_STRIPE
+#define IPS4O_WAVE_STRIPE 16384ll
+#endif
+static u64 env_u64(const char* name, long long dflt) {
+    const char* e = getenv(name);
+    long long v = e ? atoll(e) : dflt;
+    return v < 0 ? 0ull : (u64)v;
+}
+static u64 wave_elems() {
+    static u64 v = env_u64("IPS4O_WAVE", IPS4O_WAVE);
+    return v;
+}
+static u64 wave_stripe() {
+    static u64 v = env_u64("IPS4O_WAVE_STRIPE", IPS4O_WAVE_STRIPE);
+    return v;
+}
+
 static void fill_args() {
     char* p = g_ws.dev;
     const Layout& L = g_ws.lay;
@@ -284,6 +308,8 @@ static void fill_args() {
     A.q_med = (TaskDesc*)(p + L.qmed);
     A.qm_cap = c.qm;
     A.medium_max = medium_max();
+    A.wave_elems = wave_elems();
+    A.wave_stripe = std::max<u64>(wave_stripe(), 1024);
     A.q_lvl0 = (TaskDesc*)(p + L.qlvl);
     A.q_lvl1 = A.q_lvl0 + c.qn;
     A.qn_cap = c.qn;
@@ -398,8 +424,16 @@ static cudaError_t cell_setup(u32* grid, int nsm) {
 // K2 configuration: (threads, elements per thread); 256 buffers of 512 B = 128 KB of shared
 // memory: one CTA per SM (640 threads: 20 warps hide more of the barrier and shared-memory
 // latency than 16, at 96 registers per thread; two 40 KB stages still fit next to the buffers)
-template <class TR> struct K2Cfg { static constexpr int NT = 640, E = 16 / TR::S * 4, MINB = 1; };
-constexpr int K2REC_THREADS = 256;
+#ifndef IPS4O_K2_NT  // K2 threads per CTA (one CTA per SM)
+#define IPS4O_K2_NT 640
+#endif
+#ifndef IPS4O_K2_EMUL  // K2 elements per thread = 16-byte vectors per thread x elements per vector
+#define IPS4O_K2_EMUL 4
+#endif
+#ifndef IPS4O_K2_MINB  // K2 CTAs per SM the launch bounds aim at
+#define IPS4O_K2_MINB 1
+#endif
+template <class TR> struct K2Cfg { static constexpr int NT = IPS4O_K2_NT, E = 16 / TR::S * IPS4O_K2_EMUL, MINB = IPS4O_K2_MINB; };
 constexpr int K4_GRID_PER_SM = 8;
 
 // IPS4O_K3=regs selects the register-buffer permutation (tuning experiments)
@@ -419,10 +453,10 @@ static int prepare_kernels(void) {
     int occ2 = 0, occ3 = 0, occ3t = 0;
     CK(cudaFuncSetAttribute(k_sample<TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K1_SMEM));
     if constexpr (TR::WIDE) {
-        CK(cudaFuncSetAttribute(k_classify_rec<TR, K2REC_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)K2RecSmem<TR, K2REC_THREADS>::total));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_classify_rec<TR, K2REC_THREADS>, K2REC_THREADS,
-                                                         K2RecSmem<TR, K2REC_THREADS>::total));
+        CK(cudaFuncSetAttribute(k_classify_rec<TR, K2RecRpt<TR>::NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)K2RecSmem<TR, K2RecRpt<TR>::NT>::total));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_classify_rec<TR, K2RecRpt<TR>::NT>, K2RecRpt<TR>::NT,
+                                                         K2RecSmem<TR, K2RecRpt<TR>::NT>::total));
         if constexpr (TR::S == 100) {
             CK(cudaFuncSetAttribute(k_base_rec<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase<2>::smem));
             CK(cudaFuncSetAttribute(k_base_rec<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RecBase<4>::smem));
@@ -438,9 +472,9 @@ static int prepare_kernels(void) {
     } else {
         typedef K2Cfg<TR> C;
         CK(cudaFuncSetAttribute(k_classify<TR, C::NT, C::E, C::MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)K2Smem<TR, C::NT, C::E>::total));
+                                (int)K2Smem<TR, C::NT, C::E, K2_MAIN_STAGES>::total));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_classify<TR, C::NT, C::E, C::MINB>, C::NT,
-                                                         K2Smem<TR, C::NT, C::E>::total));
+                                                         K2Smem<TR, C::NT, C::E, K2_MAIN_STAGES>::total));
         CK((cell_setup<TR, CellCfg<TR>::NT0, CellCfg<TR>::E0>(&g_ws.cell_grid[0], nsm)));
         CK((cell_setup<TR, CellCfg<TR>::NT1, CellCfg<TR>::E1>(&g_ws.cell_grid[1], nsm)));
         CK((cell_setup<TR, CellCfg<TR>::NT2, CellCfg<TR>::E2>(&g_ws.cell_grid[2], nsm)));
@@ -500,11 +534,11 @@ static int enqueue_level(Enq& q) {
     LAUNCH(KK_SAMPLE, (k_sample<TR><<<T, K1_THREADS, K1_SMEM, st>>>(A)));
     STAMP(KK_SAMPLE);
     if constexpr (TR::WIDE) {
-        LAUNCH(KK_CLASSIFY, (k_classify_rec<TR, K2REC_THREADS><<<g_ws.k2_blocks, K2REC_THREADS,
-                                                                 K2RecSmem<TR, K2REC_THREADS>::total, st>>>(A)));
+        LAUNCH(KK_CLASSIFY, (k_classify_rec<TR, K2RecRpt<TR>::NT><<<g_ws.k2_blocks, K2RecRpt<TR>::NT,
+                                                                 K2RecSmem<TR, K2RecRpt<TR>::NT>::total, st>>>(A)));
     } else {
         typedef K2Cfg<TR> C;
-        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E, C::MINB><<<g_ws.k2_blocks, C::NT, K2Smem<TR, C::NT, C::E>::total, st>>>(A)));
+        LAUNCH(KK_CLASSIFY, (k_classify<TR, C::NT, C::E, C::MINB><<<g_ws.k2_blocks, C::NT, K2Smem<TR, C::NT, C::E, K2_MAIN_STAGES>::total, st>>>(A)));
     }
     STAMP(KK_CLASSIFY);
     LAUNCH(KK_PREPARE, (k_prepare<TR><<<T, MAXK, 0, st>>>(A)));

@@ -19,7 +19,10 @@
 
 namespace ips4o {
 
-template <class TR, int NT, int E>
+#ifndef IPS4O_K2_PRED_SPL  // the bucket-hint classifier loads a splitter only for cells that hold one (measured: no gain)
+#define IPS4O_K2_PRED_SPL 0
+#endif
+template <class TR, int NT, int E, int ST = K2_STAGES>
 struct K2Smem {
     typedef typename TR::V V;
     static constexpr int B = TR::B;
@@ -29,7 +32,7 @@ struct K2Smem {
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
     static constexpr size_t arr_bytes = 5 * MAXK * 4;
     static constexpr size_t rtree_bytes = IPS4O_K2_LUT ? 0 : (size_t)MAXK * TREE_COPIES * 8;  // tree copies
-    static constexpr size_t stage_bytes = (size_t)K2_STAGES * NT * E * TR::S;  // staged tiles
+    static constexpr size_t stage_bytes = (size_t)ST * NT * E * TR::S;  // staged tiles
     static constexpr size_t lut_bytes = IPS4O_K2_LUT ? (size_t)LUT_STRIDE * 2 : 0;  // bucket hints
     static constexpr size_t total =
         buf_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes + stage_bytes + lut_bytes;
@@ -327,13 +330,23 @@ __device__ __forceinline__ void k2_bucket_keys_lut(const u64 (&key)[E], u32 vali
     u32 cnt[E], en[E], more = 0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        // (branch-free: every key loads its cell's first splitter, used only if d > 0)
         const u64 y = (key[e] - lut_lo) >> lut_sh;
         u32 c = (y >> LUT_LOG) != 0ull ? LUT_N - 1u : (u32)y;
         c = key[e] < lut_lo ? LUT_N : c;
         en[e] = lut[c];
         const u32 A = en[e] & 0xFFu, d = en[e] >> 8;
+#if IPS4O_K2_PRED_SPL
+        // only keys whose cell holds a splitter (d > 0; ~6 % of the cells at k = 256) load
+        // its first splitter: a predicated load (branch-free), so the other lanes add no
+        // shared-memory wavefronts
+        u64 s1 = ~0ull;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u64 %0, [%1];\n\t}"
+                     : "+l"(s1)
+                     : "r"((u32)__cvta_generic_to_shared(spl + min(A + 1u, (u32)MAXK - 1u))), "r"(d));
+#else
+        // (branch-free: every key loads its cell's first splitter, used only if d > 0)
         const u64 s1 = spl[min(A + 1u, (u32)MAXK - 1u)];
+#endif
         const u32 ge = (u32)(key[e] >= s1) & (u32)(d != 0u);
         cnt[e] = A + ge;
         more |= (ge & (u32)(d > 1u)) << e;
@@ -553,7 +566,7 @@ __device__ __forceinline__ void k2_drain(typename TR::V* buf, K2Defer<TR, E>& df
 // flushed blocks and total; the partially filled buffers stay in buf (deferred elements
 // joined).  The task's classifier is in shared memory (spl, lut, rtree); fill, cnt, nbl and
 // *s_nflushed are zero on entry.  s_mbar: two initialised mbarriers with their phase bits.
-template <class TR, int NT, int E>
+template <class TR, int NT, int E, int ST = K2_STAGES>
 __device__ __forceinline__ void k2_stripe(const Mem<TR>& mem, const StripeDesc& sd, const TaskParam& tp,
                                           typename TR::V* buf, u64* rtree, u64* spl, u32* fill, u32* cnt, u32* slotb,
                                           u32* nfl, u32* nbl, typename TR::V* stage, unsigned short* lut,
@@ -576,11 +589,11 @@ __device__ __forceinline__ void k2_stripe(const Mem<TR>& mem, const StripeDesc& 
         uint4 cur[E / TR::VEC];
         constexpr u32 ALL = (E >= 32) ? 0xFFFFFFFFu : ((1u << E) - 1u);
         if (tid == 0) {
-            for (u64 k = 0; k < (u64)K2_STAGES && k < nft; ++k)
+            for (u64 k = 0; k < (u64)ST && k < nft; ++k)
                 k2_stage_load<TR, NT, E>(stage + k * TILE, mem, mb + k * TILE, &s_mbar[k]);
         }
         for (u64 ti = 0; ti < nft; ++ti) {
-            const u32 st = K2_STAGES == 2 ? (u32)(ti & 1) : 0u;
+            const u32 st = ST == 2 ? (u32)(ti & 1) : 0u;
             mbar_wait(&s_mbar[st], (phase >> st) & 1u);
             phase ^= 1u << st;
             k2_stage_read<TR, NT, E>(stage + st * TILE, cur);
@@ -588,7 +601,7 @@ __device__ __forceinline__ void k2_stripe(const Mem<TR>& mem, const StripeDesc& 
             // stage, and the refill for tile ti+2 is issued after it, inside k2_tile; one
             // stage: an extra barrier here, then the load of tile ti+1
             u64 refill = ~0ull;
-            if (K2_STAGES == 2) {
+            if (ST == 2) {
                 refill = ti + 2 < nft ? mb + (ti + 2) * TILE : ~0ull;
             } else {
                 __syncthreads();
@@ -630,7 +643,7 @@ template <class TR, int NT, int E, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A0) {
     const LevelArgs A = with_dyn(A0);
     typedef typename TR::V V;
-    typedef K2Smem<TR, NT, E> SM;
+    typedef K2Smem<TR, NT, E, K2_MAIN_STAGES> SM;
     constexpr int B = TR::B;
     constexpr u32 TILE = NT * E;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -683,7 +696,7 @@ __global__ void __launch_bounds__(NT, MINB) k_classify(LevelArgs A0) {
         }
         if (tid == 0) s_nflushed = 0;
         __syncthreads();
-        k2_stripe<TR, NT, E>(mem, sd, tp, buf, rtree, spl, fill, cnt, slotb, nfl, nbl, stage, lut, &s_nflushed, s_mbar,
+        k2_stripe<TR, NT, E, K2_MAIN_STAGES>(mem, sd, tp, buf, rtree, spl, fill, cnt, slotb, nfl, nbl, stage, lut, &s_nflushed, s_mbar,
                              phase);
         // ---- publish counts; spill partial buffers (compacted) to the auxiliary area
         u32 f = tid < (u32)MAXK ? fill[tid] : 0u;

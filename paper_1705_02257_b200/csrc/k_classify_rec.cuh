@@ -12,13 +12,27 @@
 
 namespace ips4o {
 
-constexpr int K2REC_RPT = 2;  // records per thread and tile
+// threads and elements per thread and tile: records 256 x 2 (a 51 KB tile), quartets
+// IPS4O_K2Q_NT x (1024 / IPS4O_K2Q_NT) (32 KB)
+#ifndef IPS4O_K2Q_NT
+#define IPS4O_K2Q_NT 256
+#endif
+template <class TR>
+struct K2RecRpt {
+    static constexpr int NT = TR::S >= 64 ? 256 : IPS4O_K2Q_NT;
+    static constexpr int v = TR::S >= 64 ? 2 : 1024 / IPS4O_K2Q_NT;
+};
+#ifndef IPS4O_K2REC_STAGES  // tiles staged ahead by TMA (2: the next tile loads while this one is placed)
+#define IPS4O_K2REC_STAGES 2
+#endif
+constexpr int K2REC_STAGES = IPS4O_K2REC_STAGES;
 
 template <class TR, int NT>
 struct K2RecSmem {
     static constexpr int NW = NT / 32;
     static constexpr size_t buf_bytes = (size_t)MAXK * TR::B * TR::S;
-    static constexpr size_t stage_bytes = (size_t)NT * K2REC_RPT * TR::S + 16;
+    static constexpr size_t stage1 = ((size_t)NT * K2RecRpt<TR>::v * TR::S + 16 + 15) / 16 * 16;  // one stage
+    static constexpr size_t stage_bytes = stage1 * K2REC_STAGES;
     static constexpr size_t wcnt_bytes = 0;
     static constexpr size_t tree_bytes = 2 * MAXK * 8;
     static constexpr size_t arr_bytes = 5 * MAXK * 4;
@@ -28,10 +42,17 @@ struct K2RecSmem {
         buf_bytes + stage_bytes + wcnt_bytes + tree_bytes + arr_bytes + rtree_bytes + lut_bytes;
 };
 
+// one element's words (quartets: 16-byte vectors -- their stage, buffer and block-grid
+// addresses are 16-byte aligned; records: 4-byte words)
 template <int RW>
 __device__ __forceinline__ void copy_rec(u32* dst, const u32* src) {
+    if constexpr (RW % 4 == 0) {
 #pragma unroll
-    for (int i = 0; i < RW; ++i) dst[i] = src[i];
+        for (int i = 0; i < RW / 4; ++i) reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    } else {
+#pragma unroll
+        for (int i = 0; i < RW; ++i) dst[i] = src[i];
+    }
 }
 
 template <class TR, int NT>
@@ -43,7 +64,7 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A0) {
     constexpr u32 RW = TR::RW;     // words per element
     extern __shared__ __align__(128) unsigned char smem[];
     u32* buf = reinterpret_cast<u32*>(smem);                                   // [256][B][25]
-    u32* stage = reinterpret_cast<u32*>(smem + SM::buf_bytes);                 // [NT][25]
+    u32* stage = reinterpret_cast<u32*>(smem + SM::buf_bytes);                 // [stages][NT*RPT][RW]
     u64* tree = reinterpret_cast<u64*>(smem + SM::buf_bytes + SM::stage_bytes + SM::wcnt_bytes);
     u64* spl = tree + MAXK;
     u32* fill = reinterpret_cast<u32*>(spl + MAXK);
@@ -51,13 +72,14 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A0) {
     u32* slotb = cnt + MAXK;
     u32* nfl = slotb + MAXK;
     u32* nbl = nfl + MAXK;
-    constexpr int RPT = K2REC_RPT;
+    constexpr int RPT = K2RecRpt<TR>::v;
     constexpr int RS = RPT;  // record slots per thread
+    constexpr u32 STW = (u32)(SM::stage1 / 4);  // words per stage
     __shared__ u32 s_head[3 * RW], s_hb[3];
-    __shared__ __align__(8) u64 s_mbar;
-    u32 sphase = 0;
+    __shared__ __align__(8) u64 s_mbar[K2REC_STAGES];
+    u32 sphase = 0;  // bit s: parity of stage s's next completion
     if (threadIdx.x == 0) {
-        mbar_init(&s_mbar, 1);
+        for (int i = 0; i < K2REC_STAGES; ++i) mbar_init(&s_mbar[i], 1);
         mbar_fence_init();
     }
     constexpr u32 RT = NT * RPT;  // records per tile
@@ -104,38 +126,56 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A0) {
         const u32 nhead = sd.first ? (u32)(tp.g - tp.lo) : 0u;
         if (tid < nhead * RW) s_head[tid] = gw[tp.lo * RW + tid];
         if (tid < 3) s_hb[tid] = INV_BUCKET;
-        for (u64 tb = mb; tb < me; tb += (u64)RT) {
-            const u32 len = (u32)((me - tb) < RT ? (me - tb) : RT);
-            constexpr bool with_head = false;
-            // stage the tile: the 16-byte aligned body of its bytes by one TMA bulk copy
-            // (mbarrier completion), the < 16 bytes before / after it by plain loads; record
-            // r of the tile then starts at stage word dw + 25 r
-            const uintptr_t p0 = (uintptr_t)(gw + tb * RW), p1 = p0 + (uintptr_t)len * (u32)TR::S;
-            const uintptr_t a0 = (p0 + 15) & ~(uintptr_t)15, a1 = p1 & ~(uintptr_t)15;
-            const uintptr_t w0 = p0 & ~(uintptr_t)15;  // stage byte 0
+        // stage tile ti into stage st: the 16-byte aligned body of its bytes by one TMA bulk
+        // copy (mbarrier completion), the < 16 bytes before / after it by plain loads; record
+        // r of the tile then starts at stage word dw + RW r.  The plain stores are ordered
+        // before the tile's processing by the barriers in between.
+        const u64 ntiles = mb < me ? (me - mb + RT - 1) / RT : 0ull;
+        auto tile_geom = [&](u64 ti, uintptr_t& p0, uintptr_t& p1, uintptr_t& a0, uintptr_t& a1, uintptr_t& w0, u32& len) {
+            const u64 tb = mb + ti * RT;
+            len = (u32)((me - tb) < RT ? (me - tb) : RT);
+            p0 = (uintptr_t)(gw + tb * RW);
+            p1 = p0 + (uintptr_t)len * (u32)TR::S;
+            a0 = (p0 + 15) & ~(uintptr_t)15;
+            a1 = p1 & ~(uintptr_t)15;
+            w0 = p0 & ~(uintptr_t)15;  // stage byte 0
+        };
+        auto stage_tile = [&](u64 ti, u32 st) {
+            uintptr_t p0, p1, a0, a1, w0;
+            u32 len;
+            tile_geom(ti, p0, p1, a0, a1, w0, len);
+            u32* sg = stage + st * STW;
             const u32 dw = (u32)((p0 - w0) / 4);
             if (tid == 0) {
-                if (a1 > a0) bulk_g2s(reinterpret_cast<char*>(stage) + (a0 - w0), reinterpret_cast<const void*>(a0),
-                                      (u32)(a1 - a0), &s_mbar);
-                else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((u32)__cvta_generic_to_shared(&s_mbar)) : "memory");
+                fence_proxy_async_smem();  // earlier generic accesses of the stage before the TMA write
+                if (a1 > a0) bulk_g2s(reinterpret_cast<char*>(sg) + (a0 - w0), reinterpret_cast<const void*>(a0),
+                                      (u32)(a1 - a0), &s_mbar[st]);
+                else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((u32)__cvta_generic_to_shared(&s_mbar[st])) : "memory");
             }
-            {
-                // head words [p0, min(a0, p1)) and tail words [max(a1, a0), p1)
-                const u32 nh = (u32)(((a0 < p1 ? a0 : p1) - p0) / 4);
-                const uintptr_t t0 = a1 > a0 ? a1 : (a0 < p1 ? a0 : p1);
-                const u32 nt = (u32)((p1 - t0) / 4);
-                if (tid < nh) stage[dw + tid] = reinterpret_cast<const u32*>(p0)[tid];
-                if (tid >= 32 && tid - 32 < nt) stage[(t0 - w0) / 4 + (tid - 32)] = reinterpret_cast<const u32*>(t0)[tid - 32];
-            }
-            mbar_wait(&s_mbar, sphase);
-            sphase ^= 1u;
+            // head words [p0, min(a0, p1)) and tail words [max(a1, a0), p1)
+            const u32 nh = (u32)(((a0 < p1 ? a0 : p1) - p0) / 4);
+            const uintptr_t t0 = a1 > a0 ? a1 : (a0 < p1 ? a0 : p1);
+            const u32 nt = (u32)((p1 - t0) / 4);
+            if (tid < nh) sg[dw + tid] = reinterpret_cast<const u32*>(p0)[tid];
+            if (tid >= 32 && tid - 32 < nt) sg[(t0 - w0) / 4 + (tid - 32)] = reinterpret_cast<const u32*>(t0)[tid - 32];
+        };
+        for (u64 ti = 0; ti < (u64)K2REC_STAGES && ti < ntiles; ++ti) stage_tile(ti, (u32)ti);
+        for (u64 ti = 0; ti < ntiles; ++ti) {
+            const u32 st = K2REC_STAGES == 2 ? (u32)(ti & 1) : 0u;
+            uintptr_t p0, p1, a0, a1, w0;
+            u32 len;
+            tile_geom(ti, p0, p1, a0, a1, w0, len);
+            const u32 dw = (u32)((p0 - w0) / 4);
+            const u32* sg = stage + st * STW;
+            constexpr bool with_head = false;
+            mbar_wait(&s_mbar[st], (sphase >> st) & 1u);
+            sphase ^= 1u << st;
             __syncthreads();
             // classify this thread's records (branchless descent) and rank
             // them in their buckets' buffer streams by shared-memory atomics (any order
             // inside a bucket)
-            // slot RS-1 of threads tid < nhead holds a head record in the first tile
             auto rec_ptr = [&](int r) -> const u32* {
-                return r < RPT ? stage + dw + (tid + r * NT) * RW : s_head + tid * RW;
+                return r < RPT ? sg + dw + (tid + r * NT) * RW : s_head + tid * RW;
             };
             u64 key[RS];
             u32 valid = 0;
@@ -200,8 +240,8 @@ __global__ void __launch_bounds__(NT, 1) k_classify_rec(LevelArgs A0) {
 #pragma unroll
             for (int r = 0; r < RS; ++r)
                 if (defer & (1u << r)) copy_rec<RW>(buf + (bk[r] * B + pos[r]) * RW, rec_ptr(r));
-            __syncthreads();
-            if (tid == 0) fence_proxy_async_smem();  // generic reads of the stage before the next TMA write
+            __syncthreads();  // every read of this stage is done: it takes the tile K2REC_STAGES ahead
+            if (ti + K2REC_STAGES < ntiles) stage_tile(ti + K2REC_STAGES, st);
         }
         // head records: classified now, spilled with the bucket's partial buffer
         if (tid < nhead) {

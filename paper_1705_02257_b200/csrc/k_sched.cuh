@@ -206,13 +206,28 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_plan(LevelArgs A0, u32 num_sms
         if (tid == 0) Q->ntot = sz;
     }
     __syncthreads();
-    // stripe length of the level: ~3 stripes per SM over the level's elements, >= 2^16
-    const u64 ntot = Q->ntot;
+    // candidate tasks of this batch
+    u32 cand = min(A0.tcap, na - ca);
     const u64 target = max(1ull, (u64)min(A0.scap, (u32)IPS4O_STRIPES_PER_SM * num_sms));
-    u64 L = max((ntot + target - 1) / target, MIN_STRIPE);
+    u64 L;
+    if (A0.wave_elems && Q->level >= 2) {
+        // an L2-sized wave: the first tasks whose sizes sum to <= wave_elems (>= 1 task);
+        // stripes ~3 per SM over the wave's elements
+        const u64 m = tid < cand ? qa[ca + tid].hi - qa[ca + tid].lo : 0ull;
+        const u32 mk = (u32)min((m + 1023) >> 10, 0xFFFFFFull);
+        const u32 pk = plan_scan(mk, s_w);
+        const u32 wk = (u32)min(A0.wave_elems >> 10, 0xFFFFFFFFull);
+        const u32 fit = __syncthreads_count(tid < cand && pk <= wk);
+        cand = cand ? max(fit, 1u) : 0u;
+        const u64 wsum = plan_sum64(tid < cand ? m : 0ull, s_w64);
+        L = max((wsum + target - 1) / target, A0.wave_stripe);
+    } else {
+        // stripe length of the level: ~3 stripes per SM over the level's elements, >= 2^16
+        const u64 ntot = Q->ntot;
+        L = max((ntot + target - 1) / target, MIN_STRIPE);
+    }
     L = (L + B - 1) / B * B;
-    // candidate tasks of this batch, their stripe counts
-    const u32 cand = min(A0.tcap, na - ca);
+    // the candidates' stripe counts
     const uintptr_t base = reinterpret_cast<uintptr_t>(D->data);
     u32 ns = 0;
     TaskDesc td = TaskDesc{0, 0, 0u, 0u};

@@ -10,7 +10,7 @@ fi
 for v in default $VARIANTS; do
   if [ "$v" = default ]; then lib=paper_1705_02257_b200/libips4o.so; else lib=paper_1705_02257_b200/libips4o_$v.so; fi
   for c in ${CFG:-H}; do
-    IPS4O_LIB=$PWD/$lib timeout 300 python bench.py --config $c --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline --e2e-steps 0 > /tmp/v.json 2>/tmp/v.err
+    IPS4O_LIB=$PWD/$lib timeout 300 python bench.py --config $c --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline --e2e-steps 0 ${NOVERIFY:+--no-verify} > /tmp/v.json 2>/tmp/v.err
     python - "$v" "$c" >> gpurun_out/variants.log <<'PY'
 import json, sys
 try:
