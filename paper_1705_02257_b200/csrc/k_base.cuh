@@ -374,7 +374,10 @@ __global__ void __launch_bounds__(KREC_THREADS) k_base_rec(const TaskDesc* tasks
 // whose cells would need too much insertion work (keys clustered far below the resolution
 // of the cells, e.g. heavy duplicates) is handed to the merge-sort kernel (fallback queue)
 // untouched.
-#ifndef IPS4O_BASE_TMA_WB  // write sorted leaves back by TMA bulk stores (1) or plain stores (0)
+#ifndef IPS4O_BASE_WARP_WB  // each warp writes back its threads' cells as soon as it has ordered them
+#define IPS4O_BASE_WARP_WB 1
+#endif
+#ifndef IPS4O_BASE_TMA_WB  // whole-leaf write-back by TMA bulk stores (1) or plain stores (0)
 #define IPS4O_BASE_TMA_WB 1
 #endif
 // Phase profile of the cell base case (tuning builds only): thread 0 of each CTA adds the
@@ -660,6 +663,11 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
     __syncthreads();
     BASE_PROF_MARK(5);
     if (S.flag > CELL_FIX_BUDGET) return 1;  // clustered keys (heavy duplicates in few cells): the caller hands the leaf on
+    // the end of this thread's run of cells (the next thread's first base), read while every
+    // counter is still this leaf's: with per-warp write-back a thread may start the next leaf
+    // (and reset its counters) while this one still orders its cells
+    const u32 run_end = tid + 1 < (u32)NT ? cnt[cpad<E>((tid + 1) * E)] : n;
+    const u32 run_beg = cnt[cpad<E>(tid * E)];
     {
         const u32 s_x = (u32)__cvta_generic_to_shared(X);
 #pragma unroll
@@ -688,7 +696,7 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
             bs[4 * k + 2] = q.z;
             bs[4 * k + 3] = q.w;
         }
-        bs[E] = tid + 1 < (u32)NT ? cnt[cpad<E>((tid + 1) * E)] : n;
+        bs[E] = run_end;
         // cells of 2 (most multi-element cells), of 3-4 and larger ones in separate
         // loops, so that a warp's lanes run the same code in each
         u32 m2 = 0, m34 = 0, mbig = 0;
@@ -750,6 +758,20 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
             }
         }
     }
+#if IPS4O_BASE_WARP_WB
+    // 5. write back of a leaf whose cells were ordered: warp by warp -- the cells of a warp's
+    //    32 runs are the contiguous range [first base of lane 0, end of lane 31) of the tile,
+    //    so each warp stores its range (coalesced) as soon as its own lanes are done, with no
+    //    CTA barrier waiting for the slowest warp's cells; the next leaf's barriers order
+    //    these reads of X before X is overwritten.  (Leaves with one key value per cell have
+    //    nothing to order: the whole-leaf TMA store below.)
+    if (mul || TR::PARTS > 1) {
+        __syncwarp();
+        const u32 wbeg = __shfl_sync(0xffffffffu, run_beg, 0), wend = __shfl_sync(0xffffffffu, run_end, 31);
+        for (u32 i = wbeg + lane; i < wend; i += 32) mem.st(td.lo + i, CellWork<TR>::out(X[i]));
+        return 0;
+    }
+#endif
     if constexpr (TR::KV) {
         // 5. write back: key and value arrays by coalesced stores
         __syncthreads();

@@ -493,6 +493,7 @@ __global__ void __launch_bounds__(CtaCfg<TR>::NT, 1)
                 int r = 0;
                 if (j - i > 1) r = cell_leaf<TR, NT, C::CE>(td, mem, data, stage, reinterpret_cast<u32*>(smem), S.cell, []() {});
                 if (IPS4O_BASE_TMA_WB && tid == 0) bulk_wait0();
+                fence_proxy_async_global();  // (plain write-back stores before later TMA reads)
                 __syncthreads();
                 if (r == 0) {
                     ++nleaves;
