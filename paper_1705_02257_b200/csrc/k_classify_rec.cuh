@@ -17,10 +17,13 @@ namespace ips4o {
 #ifndef IPS4O_K2Q_NT
 #define IPS4O_K2Q_NT 256
 #endif
+#ifndef IPS4O_K2R_NT  // records: threads per K2 CTA (tile 512 records)
+#define IPS4O_K2R_NT 512
+#endif
 template <class TR>
 struct K2RecRpt {
-    static constexpr int NT = TR::S >= 64 ? 256 : IPS4O_K2Q_NT;
-    static constexpr int v = TR::S >= 64 ? 2 : 1024 / IPS4O_K2Q_NT;
+    static constexpr int NT = TR::S >= 64 ? IPS4O_K2R_NT : IPS4O_K2Q_NT;
+    static constexpr int v = TR::S >= 64 ? 512 / IPS4O_K2R_NT : 1024 / IPS4O_K2Q_NT;
 };
 #ifndef IPS4O_K2REC_STAGES  // tiles staged ahead by TMA (2: the next tile loads while this one is placed)
 #define IPS4O_K2REC_STAGES 2
