@@ -324,7 +324,7 @@ __device__ __forceinline__ void k2_bucket_keys(const u64 (&key)[E], u32 valid, c
 // holds at most one splitter, so one comparison settles the key; cells with several
 // splitters finish with a binary search over them (all lanes of a warp wait for it only when
 // one of them needs it).  Equality buckets as in k2_bucket_keys.
-template <int E>
+template <int E, bool FULL = false>
 __device__ __forceinline__ void k2_bucket_keys_lut(const u64 (&key)[E], u32 valid, const unsigned short* lut,
                                                    const u64* spl, u64 lut_lo, u32 lut_sh, u32 eq, u32 (&bk)[E]) {
     u32 cnt[E], en[E], more = 0;
@@ -378,7 +378,7 @@ __device__ __forceinline__ void k2_bucket_keys_lut(const u64 (&key)[E], u32 vali
             const bool isq = i >= 1u && spl[ii] >= key[e];
             i = 2 * i - (isq ? 1u : 0u);
         }
-        bk[e] = ((valid >> e) & 1u) ? i : INV_BUCKET;
+        bk[e] = (FULL || ((valid >> e) & 1u)) ? i : INV_BUCKET;
     }
 }
 
@@ -393,7 +393,7 @@ struct K2Defer {
     u32 mask;
 };
 
-template <class TR, int NT, int E, int LOGK, bool AGG>
+template <class TR, int NT, int E, int LOGK, bool AGG, bool FULL = false>
 __device__ __forceinline__ void k2_tile(const Mem<TR>& mem, const uint4 (&raw)[E / TR::VEC],
                                         u32 valid, bool final_tile, u64 mb, u32 cap,
                                         typename TR::V* buf, u32* nbl,
@@ -417,7 +417,7 @@ __device__ __forceinline__ void k2_tile(const Mem<TR>& mem, const uint4 (&raw)[E
 #pragma unroll
         for (int e = 0; e < E; ++e) key[e] = TR::key(v[e], 0);
 #if IPS4O_K2_LUT
-        k2_bucket_keys_lut<E>(key, valid, lut, spl, lut_lo, lut_sh, eq, bk);
+        k2_bucket_keys_lut<E, FULL>(key, valid, lut, spl, lut_lo, lut_sh, eq, bk);
 #else
         k2_bucket_keys<E, LOGK>(key, valid, tree, spl, logk, kprime, eq, bk);
 #endif
@@ -431,16 +431,16 @@ __device__ __forceinline__ void k2_tile(const Mem<TR>& mem, const uint4 (&raw)[E
         bool done = false;
         if (AGG) {
             const u32 b0 = __shfl_sync(0xffffffffu, bk[j], 0);
-            if (__all_sync(0xffffffffu, bk[j] == b0) && b0 != INV_BUCKET) {
+            if (__all_sync(0xffffffffu, bk[j] == b0) && (FULL || b0 != INV_BUCKET)) {
                 u32 base = 0;
                 if (lane == 0) base = atomicAdd(&cnt[b0], 32u);
                 pos[j] = __shfl_sync(0xffffffffu, base, 0) + lane;
                 done = true;
             }
         }
-        if (!done && bk[j] != INV_BUCKET) pos[j] = atomicAdd(&cnt[bk[j]], 1u);
+        if (!done && (FULL || bk[j] != INV_BUCKET)) pos[j] = atomicAdd(&cnt[bk[j]], 1u);
         // bucket (< 2^16) and position (< B + tile < 2^16) in one register until placement
-        if (bk[j] != INV_BUCKET) bk[j] |= pos[j] << 16;
+        if (FULL || bk[j] != INV_BUCKET) bk[j] |= pos[j] << 16;
     }
     __syncthreads();
     if (refill != ~0ull && tid == 0) {
@@ -491,7 +491,7 @@ __device__ __forceinline__ void k2_tile(const Mem<TR>& mem, const uint4 (&raw)[E
     u32 defer = 0;
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-        if (bk[j] == INV_BUCKET) continue;
+        if (!FULL && bk[j] == INV_BUCKET) continue;
         const u32 b = bk[j] & 0xFFFFu;
         const u32 p = bk[j] >> 16;
         const u32 q = p / B, off = p % B;
@@ -611,11 +611,11 @@ __device__ __forceinline__ void k2_stripe(const Mem<TR>& mem, const StripeDesc& 
                 }
             }
             if (tp.logk == 8 && !agg)
-                k2_tile<TR, NT, E, 8, false>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                k2_tile<TR, NT, E, 8, false, true>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                              slotb, nfl, s_nflushed_p, tp.logk, tp.kprime, tp.eq,
                                              refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);
             else
-                k2_tile<TR, NT, E, 0, true>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                k2_tile<TR, NT, E, 0, true, true>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                             slotb, nfl, s_nflushed_p, tp.logk, tp.kprime, tp.eq,
                                             refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);
         }
