@@ -324,15 +324,23 @@ __device__ __forceinline__ void k2_bucket_keys(const u64 (&key)[E], u32 valid, c
 // holds at most one splitter, so one comparison settles the key; cells with several
 // splitters finish with a binary search over them (all lanes of a warp wait for it only when
 // one of them needs it).  Equality buckets as in k2_bucket_keys.
-template <int E, bool FULL = false>
+template <int E, bool FULL = false, bool HI32 = false>
 __device__ __forceinline__ void k2_bucket_keys_lut(const u64 (&key)[E], u32 valid, const unsigned short* lut,
                                                    const u64* spl, u64 lut_lo, u32 lut_sh, u32 eq, u32 (&bk)[E]) {
     u32 cnt[E], en[E], more = 0;
+    // HI32 (lut_sh >= 32; lut_lo is a multiple of 2^lut_sh): the cell from the keys' high words
+    const u32 lo_hi = (u32)(lut_lo >> 32) >> (lut_sh - 32u);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-        const u64 y = (key[e] - lut_lo) >> lut_sh;
-        u32 c = (y >> LUT_LOG) != 0ull ? LUT_N - 1u : (u32)y;
-        c = key[e] < lut_lo ? LUT_N : c;
+        u32 c;
+        if constexpr (HI32) {
+            const u32 kh = (u32)(key[e] >> 32) >> (lut_sh - 32u);
+            c = kh < lo_hi ? LUT_N : min(kh - lo_hi, LUT_N - 1u);
+        } else {
+            const u64 y = (key[e] - lut_lo) >> lut_sh;
+            c = (y >> LUT_LOG) != 0ull ? LUT_N - 1u : (u32)y;
+            c = key[e] < lut_lo ? LUT_N : c;
+        }
         en[e] = lut[c];
         const u32 A = en[e] & 0xFFu, d = en[e] >> 8;
 #if IPS4O_K2_PRED_SPL
@@ -393,7 +401,7 @@ struct K2Defer {
     u32 mask;
 };
 
-template <class TR, int NT, int E, int LOGK, bool AGG, bool FULL = false>
+template <class TR, int NT, int E, int LOGK, bool AGG, bool FULL = false, bool HI32 = false>
 __device__ __forceinline__ void k2_tile(const Mem<TR>& mem, const uint4 (&raw)[E / TR::VEC],
                                         u32 valid, bool final_tile, u64 mb, u32 cap,
                                         typename TR::V* buf, u32* nbl,
@@ -417,7 +425,7 @@ __device__ __forceinline__ void k2_tile(const Mem<TR>& mem, const uint4 (&raw)[E
 #pragma unroll
         for (int e = 0; e < E; ++e) key[e] = TR::key(v[e], 0);
 #if IPS4O_K2_LUT
-        k2_bucket_keys_lut<E, FULL>(key, valid, lut, spl, lut_lo, lut_sh, eq, bk);
+        k2_bucket_keys_lut<E, FULL, HI32>(key, valid, lut, spl, lut_lo, lut_sh, eq, bk);
 #else
         k2_bucket_keys<E, LOGK>(key, valid, tree, spl, logk, kprime, eq, bk);
 #endif
@@ -610,7 +618,11 @@ __device__ __forceinline__ void k2_stripe(const Mem<TR>& mem, const StripeDesc& 
                     k2_stage_load<TR, NT, E>(stage, mem, mb + (ti + 1) * TILE, &s_mbar[0]);
                 }
             }
-            if (tp.logk == 8 && !agg)
+            if (tp.logk == 8 && !agg && tp.lut_sh >= 32u)
+                k2_tile<TR, NT, E, 8, false, true, true>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
+                                                         slotb, nfl, s_nflushed_p, tp.logk, tp.kprime, tp.eq,
+                                                         refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);
+            else if (tp.logk == 8 && !agg)
                 k2_tile<TR, NT, E, 8, false, true>(mem, cur, ALL, false, mb, cap, buf, nbl, rtree, spl, fill, cnt,
                                              slotb, nfl, s_nflushed_p, tp.logk, tp.kprime, tp.eq,
                                              refill, stage + st * TILE, &s_mbar[st], df, agg, lut, tp.lut_lo, tp.lut_sh);

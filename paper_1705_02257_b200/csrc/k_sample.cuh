@@ -36,11 +36,19 @@ __device__ void build_lut_block(const u64* s_dist, u32 nd, u32 kp, unsigned shor
                                 u32* scr) {
     __shared__ u32 s_ws[32];
     auto S = [&](u32 i) { return s_dist[(i <= nd ? i : nd) - 1]; };
-    const u64 lo = S(1), span = S(kp - 1) - lo;
+    const u64 s1 = S(1), span = S(kp - 1) - s1;
     u32 sh = 0;
     if (span) {
         const u32 bl = 64u - (u32)__clzll((long long)span);
         sh = bl > LUT_LOG ? bl - LUT_LOG : 0u;  // span >> sh < LUT_N
+    }
+    // the cells start at lo = s_1 rounded down to a multiple of 2^sh, so that K2 can take a
+    // key's cell as (key >> sh) - (lo >> sh) (one 32-bit subtraction when sh >= 32); if the
+    // rounding pushes the last splitter past the table, the cells double
+    u64 lo = sh ? s1 & ~((1ull << sh) - 1ull) : s1;
+    if (((S(kp - 1) - lo) >> sh) >= LUT_N) {
+        ++sh;
+        lo = s1 & ~((1ull << sh) - 1ull);
     }
     // thread t owns cells [t*per, (t+1)*per) (any block size: the last owners may own none)
     const u32 tid = threadIdx.x, nt = blockDim.x, per = (LUT_N + nt - 1) / nt, lane = tid & 31, w = tid >> 5;
