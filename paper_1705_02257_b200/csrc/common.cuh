@@ -17,6 +17,9 @@ constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
 #ifndef IPS4O_CELL_C1MAX  // largest leaf of base-case class 1 (8-byte types)
 #define IPS4O_CELL_C1MAX 4096
 #endif
+#ifndef IPS4O_CAP8  // base-case capacity of the 8-byte key types (larger buckets are distributed again)
+#define IPS4O_CAP8 16384
+#endif
 #ifndef IPS4O_CELL_C2MAX  // largest leaf of base-case class 2 (8/16-byte types)
 #define IPS4O_CELL_C2MAX 6144
 #endif
@@ -66,7 +69,7 @@ constexpr int BLOCK_BYTES = IPS4O_BLOCK_BYTES;  // block b*s in bytes for the 8/
 // F64KEY = key parts are IEEE doubles compared through the order-preserving image.
 struct TU64 {
     typedef u64 V;
-    static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 0, PARTS = 1;
+    static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = IPS4O_CAP8, TYPE = 0, PARTS = 1;
     static constexpr bool WIDE = false, F64KEY = false, KV = false;
     static constexpr u32 LEAF = 4096;  // target base-case size of the adaptive k
     static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX, C2MAX = IPS4O_CELL_C2MAX;  // largest leaves of base-case classes 0-2
@@ -79,7 +82,7 @@ struct TU64 {
 // non-negatives -> unsigned order equals '<' (PAPER.md:452 uses 64-bit floats).
 struct TF64 {
     typedef u64 V;
-    static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = 16384, TYPE = 1, PARTS = 1;
+    static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = IPS4O_CAP8, TYPE = 1, PARTS = 1;
     static constexpr bool WIDE = false, F64KEY = true, KV = false;
     static constexpr u32 LEAF = 4096;
     static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX, C2MAX = IPS4O_CELL_C2MAX;

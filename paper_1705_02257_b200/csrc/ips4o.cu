@@ -873,7 +873,9 @@ __global__ void k_debug_classify_lut(const void* vin, u64 n, const u64* spl_g, c
         const u64 i = i0 + threadIdx.x;
         u64 key[1] = {i < n ? TR::key(in[i], 0) : 0ull};
         u32 bk[1];
-        k2_bucket_keys_lut<1>(key, i < n ? 1u : 0u, lut, spl, lut_lo, lut_sh, eq, bk);
+        // (K2's two variants: the cell from the keys' high words when cells are >= 2^32 wide)
+        if (lut_sh >= 32u) k2_bucket_keys_lut<1, false, true>(key, i < n ? 1u : 0u, lut, spl, lut_lo, lut_sh, eq, bk);
+        else k2_bucket_keys_lut<1>(key, i < n ? 1u : 0u, lut, spl, lut_lo, lut_sh, eq, bk);
         if (i < n) out[i] = bk[0];
     }
 }

@@ -173,6 +173,12 @@ def _adversarial_cases(rng, et):
     cases.append(np.array([12345], dtype=np.uint64))
     cases.append(np.array([7, 8], dtype=np.uint64))
     cases.append(np.array([top - 2, top - 1, top], dtype=np.uint64))
+    # the table origin s_1 rounded down to the cell width pushes the last splitter past
+    # the last cell (the cells double: K1's re-rounding), with cells >= 2^32 wide (K2's
+    # high-word path) and < 2^32 wide
+    for w in (52, 30):
+        s1 = (1 << (w - 12)) * 3 // 2 + 12345
+        cases.append(np.array([s1, s1 + (1 << (w - 1)), s1 + (1 << w) - 1], dtype=np.uint64))
     out = []
     for spl in cases:
         near = np.concatenate([spl, spl - np.uint64(1), spl + np.uint64(1), np.array([0, 1, top, top - 1], np.uint64)])

@@ -16,7 +16,7 @@ import json, sys
 try:
     d = json.loads(open('/tmp/v.json').read().strip().splitlines()[-1])
     k = {a: round(b, 3) for a, b in d['kernels_ms_per_step'].items()}
-    print(sys.argv[1], sys.argv[2], round(d['ms_per_step'], 3), 'ms', round(d['value'], 2), d['unit'], 'ok' if d.get('verified') else 'BAD', k)
+    print(sys.argv[1], sys.argv[2], round(d['ms_per_step'], 3), 'ms', round(d['value'], 2), d['unit'], 'ok' if d.get('verified') else 'BAD', k, 'lv', d['sort_stats']['levels'], 'b', d['sort_stats']['batches'], d['sort_stats']['base_tasks_by_class'], 'fb', d['sort_stats']['base_fallback_tasks'])
 except Exception as e:
     print(sys.argv[1], sys.argv[2], 'FAILED', e, open('/tmp/v.err').read()[-300:].replace('\n', ' | '))
 PY
