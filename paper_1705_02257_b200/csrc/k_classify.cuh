@@ -378,16 +378,17 @@ __device__ __forceinline__ void k2_bucket_keys_lut(const u64 (&key)[E], u32 vali
             }
         }
     }
+    if (eq) {  // (one uniform branch for all E keys)
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-        u32 i = cnt[e];
-        if (eq) {
+        for (int e = 0; e < E; ++e) {
+            const u32 i = cnt[e];
             const u32 ii = i ? i : 1u;
             const bool isq = i >= 1u && spl[ii] >= key[e];
-            i = 2 * i - (isq ? 1u : 0u);
+            cnt[e] = 2 * i - (isq ? 1u : 0u);
         }
-        bk[e] = (FULL || ((valid >> e) & 1u)) ? i : INV_BUCKET;
     }
+#pragma unroll
+    for (int e = 0; e < E; ++e) bk[e] = (FULL || ((valid >> e) & 1u)) ? cnt[e] : INV_BUCKET;
 }
 
 // Elements of a tile that start a bucket's next buffer block while the buffer's completed
