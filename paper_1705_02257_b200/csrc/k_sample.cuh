@@ -14,7 +14,10 @@ namespace ips4o {
 
 // A K1 CTA has 1024 threads: 4 (ordinary tasks) or 8 (big tasks) sample keys per thread
 // (register network + merge passes).
-constexpr int K1_THREADS = 1024;
+#ifndef IPS4O_K1_THREADS
+#define IPS4O_K1_THREADS 1024
+#endif
+constexpr int K1_THREADS = IPS4O_K1_THREADS;
 constexpr int K1_SAMPLE = 4096;        // sample capacity for ordinary tasks
 constexpr int K1_SAMPLE_BIG = 8192;    // for tasks of >= 2^22 elements (dynamic smem, 64 KB)
 constexpr size_t K1_SMEM = (size_t)(K1_SAMPLE_BIG + K1_SAMPLE_BIG / 16) * 8 + 16;
