@@ -15,7 +15,10 @@ VARIANTS = {"cellE8": ["-DIPS4O_CELL_E=8"], "k3relaxed": ["-DIPS4O_K3_RELAXED=1"
             "k1big19": ["-DIPS4O_K1_BIG_LOG=19"], "k2pred": ["-DIPS4O_K2_PRED_SPL=1"],
             "q512": ["-DIPS4O_K2Q_NT=512"], "k2s1": ["-DIPS4O_K2_MAIN_STAGES=1"],
             "bctawb": ["-DIPS4O_BASE_WARP_WB=0"], "r256": ["-DIPS4O_K2R_NT=256"],
-            "k3w2": ["-DIPS4O_K3T_WARPS=2"]}
+            "k3w2": ["-DIPS4O_K3T_WARPS=2"],
+            "leaf8k": ["-DIPS4O_LEAF8=8192"],
+            "leaf8k512": ["-DIPS4O_LEAF8=8192", "-DIPS4O_CELL_C2MAX=8192"],
+            "leaf8k768": ["-DIPS4O_LEAF8=8192", "-DIPS4O_CELL_C2MAX=12288"]}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

@@ -20,6 +20,9 @@ constexpr int CTL_STRIDE = 2;        // u64 words per bucket control pair (16 B)
 #ifndef IPS4O_CAP8  // base-case capacity of the 8-byte key types (larger buckets are distributed again)
 #define IPS4O_CAP8 16384
 #endif
+#ifndef IPS4O_LEAF8  // target leaf size of the adaptive k for u64 / f64 keys
+#define IPS4O_LEAF8 4096
+#endif
 #ifndef IPS4O_CELL_C2MAX  // largest leaf of base-case class 2 (8/16-byte types)
 #define IPS4O_CELL_C2MAX 6144
 #endif
@@ -71,7 +74,7 @@ struct TU64 {
     typedef u64 V;
     static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = IPS4O_CAP8, TYPE = 0, PARTS = 1;
     static constexpr bool WIDE = false, F64KEY = false, KV = false;
-    static constexpr u32 LEAF = 4096;  // target base-case size of the adaptive k
+    static constexpr u32 LEAF = IPS4O_LEAF8;  // target base-case size of the adaptive k
     static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX, C2MAX = IPS4O_CELL_C2MAX;  // largest leaves of base-case classes 0-2
     __device__ __forceinline__ static u64 key(V v, u32 = 0) { return v; }
     __device__ __forceinline__ static bool less(V a, V b) { return a < b; }
@@ -84,7 +87,7 @@ struct TF64 {
     typedef u64 V;
     static constexpr int S = 8, B = BLOCK_BYTES / 8, VEC = 2, CAP = IPS4O_CAP8, TYPE = 1, PARTS = 1;
     static constexpr bool WIDE = false, F64KEY = true, KV = false;
-    static constexpr u32 LEAF = 4096;
+    static constexpr u32 LEAF = IPS4O_LEAF8;
     static constexpr u32 C0MAX = 2048, C1MAX = IPS4O_CELL_C1MAX, C2MAX = IPS4O_CELL_C2MAX;
     __host__ __device__ __forceinline__ static u64 key(V v, u32 = 0) {
         return (v >> 63) ? ~v : (v | 0x8000000000000000ull);
