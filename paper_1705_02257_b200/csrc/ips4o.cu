@@ -399,11 +399,14 @@ static int ensure_ws(u64 n) {
 #ifndef IPS4O_CELL_E  // elements per thread of the 8-byte types' base-case classes 0-2
 #define IPS4O_CELL_E 16
 #endif
+#ifndef IPS4O_CELL_NT3  // threads of the 8-byte types' largest class (0: the base-case capacity / 16); leaves above its tile: merge sort
+#define IPS4O_CELL_NT3 0
+#endif
 template <class TR> struct CellCfg {
     static constexpr int E0 = TR::S == 8 ? IPS4O_CELL_E : 8, NT0 = (int)TR::C0MAX / E0;
     static constexpr int E1 = TR::S == 8 ? IPS4O_CELL_E : 8, NT1 = (int)TR::C1MAX / E1;
     static constexpr int E2 = TR::S == 8 ? IPS4O_CELL_E : 8, NT2 = (int)TR::C2MAX / E2;
-    static constexpr int E3 = TR::S == 8 ? 16 : 8, NT3 = (int)TR::CAP / E3;
+    static constexpr int E3 = TR::S == 8 ? 16 : 8, NT3 = (TR::S == 8 && IPS4O_CELL_NT3) ? IPS4O_CELL_NT3 : (int)TR::CAP / E3;
 };
 template <class TR>
 struct MergeCfg {
@@ -482,6 +485,9 @@ static int prepare_kernels(void) {
         typedef MergeCfg<TR> M;
         CK(cudaFuncSetAttribute(k_base_merge<TR, M::TH, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)M::BC::smem));
+        if constexpr (FbCell2<TR, M::TH, 16>::on)
+            CK(cudaFuncSetAttribute(k_base_fb<TR, M::TH, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)FbCell2<TR, M::TH, 16>::smem));
         g_ws.cell_grid[4] = 2u * nsm;
     }
     if constexpr (!TR::KV) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, k_permute<TR>, K3_THREADS, 0));
@@ -639,8 +645,13 @@ static int enqueue_base(Enq& q) {
             }
         }
         typedef MergeCfg<TR> M;
-        LAUNCH(KK_BASE, (k_base_merge<TR, M::TH, 16><<<g_ws.cell_grid[4], M::TH, M::BC::smem, st>>>(
-                             A.q_fb, 0u, A.ctr + CTR_FB, A.dyn, A.q_cap)));
+        if constexpr (FbCell2<TR, M::TH, 16>::on) {
+            LAUNCH(KK_BASE, (k_base_fb<TR, M::TH, 16><<<g_ws.cell_grid[4], M::TH, FbCell2<TR, M::TH, 16>::smem, st>>>(
+                                 A.q_fb, 0u, A.ctr + CTR_FB, A.dyn, A.q_cap)));
+        } else {
+            LAUNCH(KK_BASE, (k_base_merge<TR, M::TH, 16><<<g_ws.cell_grid[4], M::TH, M::BC::smem, st>>>(
+                                 A.q_fb, 0u, A.ctr + CTR_FB, A.dyn, A.q_cap)));
+        }
         STAMP(KK_BASE);
         return IPS4O_OK;
     }

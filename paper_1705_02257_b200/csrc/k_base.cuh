@@ -414,6 +414,9 @@ struct CellBase {
 };
 template <int E>
 __device__ __forceinline__ u32 cpad(u32 c) { return c + 4u * (c / E); }
+#ifndef IPS4O_CELL_TILE_CELLS  // cells of a leaf with a wide key span: one per tile slot (1) or one per element (0)
+#define IPS4O_CELL_TILE_CELLS 1
+#endif
 #ifndef IPS4O_CELL_FIX_BUDGET
 #define IPS4O_CELL_FIX_BUDGET 16384
 #endif
@@ -451,10 +454,13 @@ template <> struct CellWork<TQuad> {
     __device__ __forceinline__ static Quad out(const Quad& v) { return v; }
 };
 
+#ifndef IPS4O_CELL_MINB1  // resident CTAs per SM the 256-thread class of 8-byte keys is compiled for
+#define IPS4O_CELL_MINB1 3
+#endif
 template <class TR, int NT, int E>
 struct CellMinB {
     static constexpr int v = sizeof(typename TR::V) == 8
-                                 ? (E >= 16 ? (NT <= 128 ? 6 : NT <= 256 ? 3 : NT <= 384 ? 2 : 1)
+                                 ? (E >= 16 ? (NT <= 128 ? 6 : NT <= 256 ? IPS4O_CELL_MINB1 : NT <= 384 ? 2 : 1)
                                             : (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 512 ? 2 : 1))
                              : sizeof(typename TR::V) == 16 ? (NT <= 256 ? 3 : NT <= 512 ? 2 : 1)
                                                             : (NT <= 256 ? 2 : 1);
@@ -464,6 +470,39 @@ __device__ __forceinline__ u32 atoms_inc(u32 saddr) {
     asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(saddr));
     return r;
 }
+// predicated forms (the slots of a tile past the leaf's n elements): straight-line code, so that
+// the tile's E atomics / loads are in flight together instead of one per basic block
+__device__ __forceinline__ u32 atoms_inc_if(u32 saddr, bool p) {
+    u32 r = 0;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q atom.shared.add.u32 %0, [%1], 1;\n\t}"
+                 : "+r"(r)
+                 : "r"(saddr), "r"((u32)p));
+    return r;
+}
+template <class V>
+__device__ __forceinline__ void sts_v_if(u32 saddr, const V& v, bool p) {
+    if constexpr (sizeof(V) == 8) {
+        u64 x;
+        memcpy(&x, &v, 8);
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u64 [%0], %1;\n\t}" ::"r"(saddr), "l"(x),
+                     "r"((u32)p));
+    } else {
+        static_assert(sizeof(V) % 16 == 0, "16-byte multiples");
+#pragma unroll
+        for (u32 o = 0; o < sizeof(V); o += 16) {
+            ulonglong2 x;
+            memcpy(&x, reinterpret_cast<const char*>(&v) + o, 16);
+            asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q st.shared.v2.u64 [%0], {%1, %2};\n\t}" ::"r"(saddr + o),
+                         "l"(x.x), "l"(x.y), "r"((u32)p));
+        }
+    }
+}
+#ifndef IPS4O_BASE_M2X2  // cells of two elements ordered two per loop iteration
+#define IPS4O_BASE_M2X2 0
+#endif
+#ifndef IPS4O_BASE_PRED  // rank and scatter as predicated straight-line code (1; measured no faster: H base 1.86 = 1.86 ms, C4 1.45 -> 1.50) or one branch per slot (0)
+#define IPS4O_BASE_PRED 0
+#endif
 __device__ __forceinline__ u32 lds_u32(u32 saddr) {
     u32 r;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(saddr));
@@ -501,12 +540,27 @@ struct CellSh {
 // called by every thread between the barriers that follow the key-range reduction (the caller's
 // next-leaf bookkeeping).  Returns 0 when the leaf is sorted in place, 1 when its keys are too
 // clustered for the cells (it is left untouched for the merge sort).
-template <class TR, int NT, int E, class F>
-__device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem, typename TR::V* data,
-                                         typename TR::V* X0, u32* cnt, CellSh<NT / 32>& S, F&& after_range) {
+// The leaf's elements into registers (element j*NT + tid; the slots past n load a copy of
+// element n-1, which changes no range and takes no part in the steps after the range): plain
+// loads with no use of the values, so that they stay in flight behind whatever the caller does
+// next (k_base_cell issues the next leaf's loads while this leaf's cells are ordered).
+template <class TR, int NT, int E>
+__device__ __forceinline__ void cell_load(const TaskDesc& td, const Mem<TR>& mem, typename TR::V (&v)[E]) {
+    const u32 n = (u32)(td.hi - td.lo);
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = mem.ld(td.lo + min((u32)(j * NT) + threadIdx.x, n - 1u));
+}
+
+// v: the leaf's elements as cell_load left them.  after_scatter() is called once v has been
+// consumed (the scatter), unless the leaf returns early (all keys equal, or 1): it may refill v.
+template <class TR, int NT, int E, class F, class G>
+__device__ __forceinline__ int cell_leaf_pre(const TaskDesc& td, const Mem<TR>& mem, typename TR::V* data,
+                                             typename TR::V* X0, u32* cnt, CellSh<NT / 32>& S,
+                                             typename TR::V (&v)[E], F&& after_range, G&& after_scatter) {
     typedef typename TR::V V;
     typedef CellBase<TR, NT, E> CB;
     typedef typename CellWork<TR>::T TW;
+    constexpr bool PRED = IPS4O_BASE_PRED && NT < 1024;  // (1024 threads: 64 registers, the straight-line form spills)
     const u32 tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     uint4* myrun = reinterpret_cast<uint4*>(cnt + cpad<E>(tid * E));  // this thread's E counters
     const u32 n = (u32)(td.hi - td.lo);
@@ -530,12 +584,10 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
     //    (warp reductions in one REDUX instruction each)
     //    (branch-free over the whole tile: the slots past n load a copy of element n-1,
     //    which changes no range; they take no part in the steps below)
-    V v[E];
     u32 hmin = ~0u, hmax = 0u;
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-        const u32 idx = min((u32)(j * NT) + tid, n - 1u);
-        v[j] = CellWork<TR>::in(mem.ld(td.lo + idx));
+        v[j] = CellWork<TR>::in(v[j]);
         const u32 h = (u32)(TW::key(v[j]) >> 32);
         hmin = min(hmin, h);
         hmax = max(hmax, h);
@@ -611,14 +663,25 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
     const u32 span32 = (u32)(span >> sh);
     // cells: one per key value when the span fits the tile (nothing to order inside a cell),
     // else one per element (at most one element per cell on average)
+#if IPS4O_CELL_TILE_CELLS
+    // (every counter of the tile is a cell: the counter scan covers the whole tile anyway, more
+    // cells than elements mean fewer elements per cell, and every thread owns cells to order)
+    const u32 ncell = span < (u64)CB::TILE ? max(n, (u32)span + 1u) : CB::TILE;
+#else
     const u32 ncell = span < (u64)CB::TILE ? max(n, (u32)span + 1u) : n;
+#endif
     const u32 mul = span32 >= ncell ? (u32)(((u64)ncell << 32) / ((u64)span32 + 1ull)) : 0u;
     // 2. cell and rank inside the cell
     const u32 s_cnt = (u32)__cvta_generic_to_shared(cnt);
     u32 cr[E];  // cell | rank << 16
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-        if (j * NT + tid < n) {
+        if constexpr (PRED) {
+            // (a slot past n holds a copy of element n-1: its cell is a valid one, only the count is skipped)
+            const u32 x = (u32)((TW::key(v[j]) - kmin) >> sh);
+            const u32 c = mul ? __umulhi(x, mul) : x;
+            cr[j] = c | (atoms_inc_if(s_cnt + 4u * cpad<E>(c), (u32)(j * NT) + tid < n) << 16);
+        } else if (j * NT + tid < n) {
             const u32 x = (u32)((TW::key(v[j]) - kmin) >> sh);
             const u32 c = mul ? __umulhi(x, mul) : x;
             cr[j] = c | (atoms_inc(s_cnt + 4u * cpad<E>(c)) << 16);
@@ -672,12 +735,16 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
         const u32 s_x = (u32)__cvta_generic_to_shared(X);
 #pragma unroll
         for (int j = 0; j < E; ++j) {
-            if (j * NT + tid < n) {
+            if constexpr (PRED) {
+                const u32 pos = lds_u32(s_cnt + 4u * cpad<E>(cr[j] & 0xFFFFu)) + (cr[j] >> 16);
+                sts_v_if<V>(s_x + pos * (u32)sizeof(V), v[j], (u32)(j * NT) + tid < n);
+            } else if (j * NT + tid < n) {
                 const u32 pos = lds_u32(s_cnt + 4u * cpad<E>(cr[j] & 0xFFFFu)) + (cr[j] >> 16);
                 sts_v<V>(s_x + pos * (u32)sizeof(V), v[j]);
             }
         }
     }
+    after_scatter();
     __syncthreads();
     BASE_PROF_MARK(6);
     // 4. order the cells of this thread's run that hold several elements (PAPER.md:403
@@ -708,6 +775,25 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
             mbig |= (m > 4u ? 1u : 0u) << k;
         }
         const u32 enext = bs[E];
+#if IPS4O_BASE_M2X2
+        // (two cells per iteration: their dependent shared-memory loads overlap)
+        while (m2) {
+            const u32 k = (u32)__ffs(m2) - 1u;
+            m2 &= m2 - 1u;
+            const u32 k2 = m2 ? (u32)__ffs(m2) - 1u : k;
+            m2 &= m2 - 1u;
+            const u32 b = cnt[cpad<E>(tid * E + k)], b2 = cnt[cpad<E>(tid * E + k2)];
+            const V x0 = X[b], x1 = X[b + 1], y0 = X[b2], y1 = X[b2 + 1];
+            if (TW::less(x1, x0)) {
+                X[b] = x1;
+                X[b + 1] = x0;
+            }
+            if (k2 != k && TW::less(y1, y0)) {
+                X[b2] = y1;
+                X[b2 + 1] = y0;
+            }
+        }
+#else
         while (m2) {
             const u32 k = (u32)__ffs(m2) - 1u;
             m2 &= m2 - 1u;
@@ -718,6 +804,7 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
                 X[b + 1] = x0;
             }
         }
+#endif
         while (m34) {
             const u32 k = (u32)__ffs(m34) - 1u;
             m34 &= m34 - 1u;
@@ -807,6 +894,18 @@ __device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem,
     return 0;
 }
 
+// One leaf, loaded here.
+template <class TR, int NT, int E, class F>
+__device__ __forceinline__ int cell_leaf(const TaskDesc& td, const Mem<TR>& mem, typename TR::V* data,
+                                         typename TR::V* X0, u32* cnt, CellSh<NT / 32>& S, F&& after_range) {
+    typename TR::V v[E];
+    cell_load<TR, NT, E>(td, mem, v);
+    return cell_leaf_pre<TR, NT, E>(td, mem, data, X0, cnt, S, v, after_range, []() {});
+}
+
+#ifndef IPS4O_BASE_PIPE  // the next leaf's loads issued behind this leaf's scatter (measured slower: H base 1.86 -> 1.88 ms; off)
+#define IPS4O_BASE_PIPE 0
+#endif
 template <class TR, int NT, int E>
 __global__ void __launch_bounds__(NT, (CellMinB<TR, NT, E>::v))
     k_base_cell(const TaskDesc* tasks, const u32* d_ntasks, u32 qcap, u32* ticket, const LevelDyn* dyn,
@@ -825,16 +924,40 @@ __global__ void __launch_bounds__(NT, (CellMinB<TR, NT, E>::v))
     const u32 tid = threadIdx.x;
     if (tid == 0) s_next[0] = atomicAdd(ticket, 1u);
     __syncthreads();
+    constexpr bool PIPE = IPS4O_BASE_PIPE && NT < 1024;  // (1024 threads: 64 registers, no room for a second leaf)
     u32 cur = s_next[0], par = 1;
+    V v[E];
+    TaskDesc td = cur < ntasks ? tasks[cur] : TaskDesc{0, 1, 0u, 0u};
+    if (PIPE && cur < ntasks) cell_load<TR, NT, E>(td, mem, v);
     while (cur < ntasks) {
-        const TaskDesc td = tasks[cur];
         if (tid == 0) s_next[par] = atomicAdd(ticket, 1u);  // the next leaf (read after the barriers below)
         u32 nxt = ntasks;
-        const int r = cell_leaf<TR, NT, E>(td, mem, data, X0, cnt, sh, [&]() {
+        TaskDesc tn = td;
+        if ((u64)(td.hi - td.lo) > (u64)CB::TILE) {
+            // (a class whose tile is smaller than the base-case capacity: the rare larger leaves
+            // go to the merge sort)
+            __syncthreads();
             nxt = s_next[par];
+            if (tid == 0) {
+                const u32 q = atomicAdd(fb_count, 1u);
+                if (q < fb_cap) fb_queue[q] = td;
+            }
+            __syncthreads();
+            cur = nxt;
+            par ^= 1u;
+            if (cur < ntasks) {
+                td = tasks[cur];
+                if (PIPE) cell_load<TR, NT, E>(td, mem, v);
+            }
+            continue;
+        }
+        if (!PIPE) cell_load<TR, NT, E>(td, mem, v);
+        bool pre = false;
+        const int r = cell_leaf_pre<TR, NT, E>(td, mem, data, X0, cnt, sh, v, [&]() {
+            nxt = s_next[par];
+            if (nxt < ntasks) tn = tasks[nxt];
             if (tid == 0 && nxt < ntasks) {
                 // the next leaf's elements into L2 (TMA bulk prefetch)
-                const TaskDesc tn = tasks[nxt];
                 if constexpr (TR::KV) {
                     for (int h = 0; h < 2; ++h) {
                         const u64* arr = h ? mem.v : mem.k;
@@ -848,12 +971,18 @@ __global__ void __launch_bounds__(NT, (CellMinB<TR, NT, E>::v))
                     if (a1 > a0) bulk_prefetch_l2(reinterpret_cast<const void*>(a0), (u32)(a1 - a0));
                 }
             }
+        }, [&]() {
+            // v has been scattered: the next leaf's loads fly while this leaf's cells are ordered
+            pre = true;
+            if (PIPE && nxt < ntasks) cell_load<TR, NT, E>(tn, mem, v);
         });
         if (r == 1 && tid == 0) {
             const u32 q = atomicAdd(fb_count, 1u);
             if (q < fb_cap) fb_queue[q] = td;
         }
+        if (PIPE && !pre && nxt < ntasks) cell_load<TR, NT, E>(tn, mem, v);
         cur = nxt;
+        td = tn;
         par ^= 1u;
     }
     if (IPS4O_BASE_TMA_WB && tid == 0) bulk_wait0();
@@ -864,6 +993,53 @@ struct BaseClass {
     static constexpr u32 TILE = THREADS * ITEMS;
     static constexpr size_t smem = (size_t)padidx(TILE) * sizeof(typename TR::V) + 16;
 };
+
+// The fallback queue of the 8-byte key types: leaves the cell kernels of the smaller classes
+// handed back get a second chance in the largest tile (a leaf of few distinct values whose key
+// span exceeds its own class's tile but not this one has one key value per cell here: nothing
+// to order), and only leaves that are clustered at this resolution too are merge-sorted.
+#ifndef IPS4O_FB_CELL2
+#define IPS4O_FB_CELL2 1
+#endif
+template <class TR, int THREADS, int ITEMS>
+struct FbCell2 {
+    static constexpr bool on = IPS4O_FB_CELL2 && sizeof(typename TR::V) == 8 && !TR::KV && TR::PARTS == 1;
+    static constexpr size_t cell_smem = CellBase<TR, THREADS, ITEMS>::smem;
+    static constexpr size_t merge_smem = (size_t)padidx(THREADS * ITEMS) * sizeof(typename TR::V) + 16;
+    static constexpr size_t smem = on ? (cell_smem > merge_smem ? cell_smem : merge_smem) : merge_smem;
+};
+template <class TR, int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS) k_base_fb(const TaskDesc* tasks, u32 start, const u32* d_ntasks,
+                                                      const LevelDyn* dyn, u32 cap) {
+    const u32 ntasks = min(*d_ntasks, cap);  // tasks [start, ntasks) (the count lives on the device)
+    typedef typename TR::V V;
+    typedef CellBase<TR, THREADS, ITEMS> CB;
+    extern __shared__ __align__(16) unsigned char smem5[];
+    V* s = reinterpret_cast<V*>(smem5);
+    u32* cnt = reinterpret_cast<u32*>(smem5 + CB::x_bytes);
+    __shared__ CellSh<THREADS / 32> sh;
+    const Mem<TR> mem(dyn->data, dyn->vals);
+    V* data = reinterpret_cast<V*>(dyn->data);
+    const u32 tid = threadIdx.x;
+    for (u32 ti = start + blockIdx.x; ti < ntasks; ti += gridDim.x) {
+        const TaskDesc td = tasks[ti];
+        const u32 n = (u32)(td.hi - td.lo);
+        if (n < 2) continue;
+        if (cell_leaf<TR, THREADS, ITEMS>(td, mem, data, s, cnt, sh, []() {}) == 0) continue;
+        // clustered at this resolution too: merge sort (the tile is free once every warp has left
+        // the previous leaf and its TMA store has read the tile)
+        if (IPS4O_BASE_TMA_WB && tid == 0) bulk_wait_read0();
+        __syncthreads();
+        const u32 n16 = (n + ITEMS - 1) / ITEMS * ITEMS;
+        for (u32 i = tid; i < n16; i += THREADS) s[padidx(i)] = i < n ? mem.ld(td.lo + i) : TR::pad();
+        __syncthreads();
+        block_sort_smem<TR, THREADS, ITEMS>(s, n);
+        for (u32 i = tid; i < n; i += THREADS) mem.st(td.lo + i, s[padidx(i)]);
+        __syncthreads();
+    }
+    if (IPS4O_BASE_TMA_WB && tid == 0) bulk_wait0();
+}
+
 
 template <class TR>
 __global__ void k_debug_classify(const void* vin, u64 n, const u64* tree_g, const u64* spl_g,
