@@ -585,6 +585,15 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A0) {
 //   SWAPPING  the displaced block is arriving: if it already belongs to the destination it
 //             stays (skip), else ours is written over it and the displaced one is carried on.
 // Used for the 8/16-byte types (block grid 16-byte aligned); records use k_permute.
+#ifndef IPS4O_K3_PF  // L2 prefetch of the blocks later claims / takes of a bucket will load (0: off; n: n x the default distance)
+#define IPS4O_K3_PF 1
+#endif
+#ifndef IPS4O_K3_PF_DEN
+#define IPS4O_K3_PF_DEN 1
+#endif
+#ifndef IPS4O_K3_PF_MIN
+#define IPS4O_K3_PF_MIN 1
+#endif
 #ifndef IPS4O_K3T_WARPS
 #define IPS4O_K3T_WARPS 4
 #endif
@@ -628,6 +637,15 @@ struct K3Blk {
             bulk_g2s_tx(sbuf + H, vb + (u64)x * H, H, mbar);
         } else {
             bulk_g2s(sbuf, kb + (u64)x * BB, BB, mbar);
+        }
+    }
+    __device__ __forceinline__ static void prefetch(const char* kb, const char* vb, u32 x) {
+        if constexpr (TR::KV) {
+            constexpr u32 H = TR::B * 8;
+            bulk_prefetch_l2(kb + (u64)x * H, H);
+            bulk_prefetch_l2(vb + (u64)x * H, H);
+        } else {
+            bulk_prefetch_l2(kb + (u64)x * BB, BB);
         }
     }
     __device__ __forceinline__ static void store(char* kb, char* vb, u32 x, const char* sbuf) {
@@ -731,6 +749,13 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
             return classify_key(TR::key(v, tp.part), s_tree, s_spl, tp.logk, tp.kprime, tp.eq);
         };
 
+#if IPS4O_K3_PF
+        // L2 prefetch distance: the block a later claim / take of the same bucket will load, about
+        // half the chains working on the bucket ahead (a bucket's unprocessed blocks [w, r] are
+        // consumed in order from both ends)
+        const int pfd = (int)max((u32)IPS4O_K3_PF_MIN, (u32)(gridDim.x * (K3T_WARPS * K3T_CHAINS)) / max(1u, T * tp.K * 2u) *
+                                                            (u32)IPS4O_K3_PF / (u32)IPS4O_K3_PF_DEN);
+#endif
         u32 st = chain ? CH_FREE : CH_DEAD;
         u32 pb = (u32)(((u64)blockIdx.x * (K3T_WARPS * K3T_CHAINS) + cid) * 97u % tp.K);
         u32 xb = 0;       // buffer holding our block (the other one receives loads)
@@ -762,6 +787,9 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
                         bulk_wait_read0();  // our earlier stores have read this buffer
                         fence_proxy_async_smem();
                         K3Blk<TR>::load(mybuf + xb * BB, tbase, vbase, (u32)orr, mymbar);
+#if IPS4O_K3_PF
+                        if (orr - pfd >= ow) K3Blk<TR>::prefetch(tbase, vbase, (u32)(orr - pfd));
+#endif
                         st = CH_TAKING;
                     }
                     progressed = true;
@@ -779,6 +807,9 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
                     bulk_wait_read0();
                     fence_proxy_async_smem();
                     K3Blk<TR>::load(mybuf + (xb ^ 1) * BB, tbase, vbase, (u32)ow, mymbar);
+#if IPS4O_K3_PF
+                    if (ow + pfd <= orr) K3Blk<TR>::prefetch(tbase, vbase, (u32)(ow + pfd));
+#endif
                     st = CH_SWAPPING;
                 } else {
                     st = CH_WAITW;  // empty block: written once the bucket has no readers
