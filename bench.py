@@ -80,7 +80,7 @@ def levels_for(n: int, esize: int) -> int:
 # ------------------------------------------------------------------ clocks sampler
 
 class ClockSampler:
-    """SM clocks and throttle reasons sampled DURING the timed region: NVML every 5 ms (at
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML every 4 ms (at
     least ~20 samples in a 0.1 s region), else nvidia-smi every 200 ms."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -92,20 +92,30 @@ class ClockSampler:
         self.proc = None
         self.out = []
         self.nv = None
+        self.mx = 0
         self.stop = threading.Event()
         self.thr = None
 
-    def __enter__(self):
+    def prepare(self):
+        """NVML initialised ahead of the timed region (nvmlInit can take longer than the region)."""
+        if self.nv is not None:
+            return
         try:
             import pynvml as nv
             nv.nvmlInit()
             h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
             self.nv = (nv, h)
+        except Exception:
+            self.nv = None
+
+    def __enter__(self):
+        self.prepare()
+        if self.nv is not None:
             self.thr = threading.Thread(target=self._nvml, daemon=True)
             self.thr.start()
             return self
-        except Exception:
-            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -121,7 +131,7 @@ class ClockSampler:
         nv, h = self.nv
         bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = self.mx
         while not self.stop.is_set():
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
@@ -130,7 +140,7 @@ class ClockSampler:
                 self.out.append(",".join([str(sm), str(mx)] + act))
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.004)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -162,9 +172,20 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+            # no sample landed inside the region (NVML missing or failing): one nvidia-smi query now,
+            # right behind the region, marked as such
+            try:
+                line = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                      timeout=20).stdout.strip().splitlines()[0]
+                parts = [p.strip() for p in line.split(",")]
+                rs = [nm for nm, v in zip(self.NAMES, parts[2:6]) if v.lower().startswith("active")]
+                return {"sm_mhz": float(parts[0]), "sm_max_mhz": float(parts[1]), "reasons": sorted(rs),
+                        "samples": 1, "source": "nvidia-smi, one query right after the timed region"}
+            except Exception:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm), "source": "nvml 5 ms" if self.nv else "nvidia-smi 200 ms"}
+                "samples": len(sm), "source": "nvml 4 ms" if self.nv else "nvidia-smi 200 ms"}
 
 
 # ------------------------------------------------------------------ helpers
@@ -331,12 +352,14 @@ def run_ours(args):
     # region right after this one, same workload and launches)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
+    clk = ClockSampler(local)
+    clk.prepare()
     launches = 0
     stats = None
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with clk:
         for i in range(args.steps):
             work.copy_(pristine)
             evs[i][0].record(stream)

@@ -588,6 +588,9 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A0) {
 #ifndef IPS4O_K3_PF  // L2 prefetch of the blocks later claims / takes of a bucket will load (0: off; n: n x the default distance)
 #define IPS4O_K3_PF 1
 #endif
+#ifndef IPS4O_K3_DEFER  // the atomics' return values consumed after the round's arrived blocks have been served
+#define IPS4O_K3_DEFER 0
+#endif
 #ifndef IPS4O_K3_PF_DEN
 #define IPS4O_K3_PF_DEN 1
 #endif
@@ -761,6 +764,95 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
         u32 xb = 0;       // buffer holding our block (the other one receives loads)
         u32 dest = 0, slot = 0;
         while (__any_sync(0xffffffffu, st != CH_DEAD)) {
+#if IPS4O_K3_DEFER
+            // The same steps with the atomics' results consumed late: takes and claims are issued,
+            // then the chains whose blocks have arrived are served, and only then the warp waits
+            // for the atomics' return values (a chain is in one state per round, so every chain's
+            // own sequence of operations is unchanged).
+            bool progressed = false;
+            u32 pend = 0;  // 1: take issued, 2: claim issued (result in old)
+            u64 old = 0;
+            if (st == CH_FREE) {
+                const u32 b = next_open_bucket(done, pb, tp.K);
+                if (b == 0xFFFFFFFFu) {
+                    st = CH_DEAD;
+                } else {
+                    pb = b;
+                    K3_TL_EVENT(1);
+                    atomicAdd(ctl_readers(A.wr, t, pb), 1u);  // (S18: announced before the take's release)
+                    old = atom_add_release_u64(ctl_wr(A.wr, t, pb), ~0ull);
+                    pend = 1;
+                    progressed = true;
+                }
+            } else if (st == CH_HELD) {
+                K3_TL_EVENT(0);
+                old = atom_add_acquire_u64(ctl_wr(A.wr, t, dest), 1ull << 32);
+                pend = 2;
+                progressed = true;
+            }
+            // ---- arrived blocks
+            if ((st == CH_TAKING || st == CH_SWAPPING) && mbar_test(mymbar, phase)) {
+                phase ^= 1u;
+                if (st == CH_TAKING) {
+                    red_add_release_u32(ctl_readers(A.wr, t, pb), ~0u);  // the block has been read (release)
+                    dest = classify_buf(mybuf + xb * BB);
+                    st = CH_HELD;
+                } else {
+                    const u32 od = classify_buf(mybuf + (xb ^ 1) * BB);
+                    if (od != dest) {
+                        K3Blk<TR>::store(tbase, vbase, slot, mybuf + xb * BB);
+                        bulk_commit();
+                        ++nmoves;
+                        xb ^= 1u;
+                        dest = od;
+                    }  // else: already in place, skip it and keep ours
+                    st = CH_HELD;
+                }
+                progressed = true;
+            }
+            // ---- the atomics' results
+            if (pend == 1) {
+                const int ow = (int)(u32)(old >> 32), orr = (int)((u32)old - RBIAS);
+                if (orr < ow) {
+                    atomicSub(ctl_readers(A.wr, t, pb), 1u);
+                    atomicOr(&done[pb >> 5], 1u << (pb & 31));
+                } else {
+                    bulk_wait_read0();  // our earlier stores have read this buffer
+                    fence_proxy_async_smem();
+                    K3Blk<TR>::load(mybuf + xb * BB, tbase, vbase, (u32)orr, mymbar);
+#if IPS4O_K3_PF
+                    if (orr - pfd >= ow) K3Blk<TR>::prefetch(tbase, vbase, (u32)(orr - pfd));
+#endif
+                    st = CH_TAKING;
+                }
+            } else if (pend == 2) {
+                const int ow = (int)(u32)(old >> 32), orr = (int)((u32)old - RBIAS);
+                slot = (u32)ow;
+                if (ow <= orr) {
+                    bulk_wait_read0();
+                    fence_proxy_async_smem();
+                    K3Blk<TR>::load(mybuf + (xb ^ 1) * BB, tbase, vbase, (u32)ow, mymbar);
+#if IPS4O_K3_PF
+                    if (ow + pfd <= orr) K3Blk<TR>::prefetch(tbase, vbase, (u32)(ow + pfd));
+#endif
+                    st = CH_SWAPPING;
+                } else {
+                    st = CH_WAITW;  // empty block: written once the bucket has no readers
+                }
+            }
+            if (st == CH_WAITW && ld_acquire_u32(ctl_readers(A.wr, t, dest)) == 0u) {
+                if (tp.g + (u64)(slot + 1) * TR::B > tp.hi) {
+                    bulk_s2g(reinterpret_cast<char*>(A.ovf) + (u64)t * BB, mybuf + xb * BB, BB);
+                    A.ovf_owner[t] = (int)dest;
+                } else {
+                    K3Blk<TR>::store(tbase, vbase, slot, mybuf + xb * BB);
+                }
+                bulk_commit();
+                ++nmoves;
+                st = CH_FREE;
+                progressed = true;
+            }
+#else
             bool progressed = false;
             // ---- atomics: takes (FREE) and claims (HELD), one round trip for all chains
             if (st == CH_FREE) {
@@ -851,6 +943,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
                 }
                 progressed = true;
             }
+#endif
             if (!__any_sync(0xffffffffu, progressed)) __nanosleep(IPS4O_K3_IDLE_NS);
         }
         __syncthreads();

@@ -310,6 +310,30 @@ def test_sort_duplicates_vs_oracle(et, kind):
         check_equal_to_oracle(et, a, _sort_gpu(a, et), oracle.sort(a))
 
 
+@pytest.mark.parametrize("et", [W.ELEM_U64, W.ELEM_F64])
+@pytest.mark.parametrize("span", [3000, 6000, 15000, 40000, 1 << 40])
+def test_fallback_leaves_vs_oracle(et, span):
+    """Leaves the cell kernels hand back: one heavy key value plus scattered others.  span < the
+    class tile: one key value per cell; class tile <= span < 16384: the fallback's second chance in
+    the largest cell tile; beyond: the merge sort.  Single leaves (n <= the base-case capacity)
+    and a two-level sort whose buckets are such leaves."""
+    rng = np.random.default_rng(span % 9973)
+    for n in (1500, 3000, 5000, 12000, 300_000):
+        nleaf = max(1, n // 3000)
+        parts = []
+        for q in range(nleaf):
+            m = n // nleaf
+            base = np.uint64(q) * np.uint64(min(span, 1 << 41) * 2)
+            heavy = base + np.uint64(rng.integers(0, span))
+            others = base + rng.integers(0, span, size=m - 2 * m // 3).astype(np.uint64)
+            parts.append(np.concatenate([np.full(2 * m // 3, heavy, np.uint64), others]))
+        k = np.concatenate(parts)
+        rng.shuffle(k)
+        a = k if et == W.ELEM_U64 else (k.astype(np.float64) - 1.0e6)
+        got = _sort_gpu(a, et)
+        check_equal_to_oracle(et, a, got, oracle.sort(a))
+
+
 @pytest.mark.parametrize("dist", ["rootdup", "twodup", "eightdup", "almostsorted", "reversesorted",
                                   "sorted", "zeros", "ones", "uniform", "f64_uniform", "f64_exponential",
                                   "pair16", "rec100", "pair_f64", "quartet_f64", "quartet_f64_dup"])
