@@ -591,6 +591,9 @@ __global__ void __launch_bounds__(K3_THREADS, K3_MINB) k_permute(LevelArgs A0) {
 #ifndef IPS4O_K3_DEFER  // the atomics' return values consumed after the round's arrived blocks have been served
 #define IPS4O_K3_DEFER 0
 #endif
+#ifndef IPS4O_K3_SKIPSCAN  // a chain takes from its last bucket again without scanning the done bits first
+#define IPS4O_K3_SKIPSCAN 0
+#endif
 #ifndef IPS4O_K3_PF_DEN
 #define IPS4O_K3_PF_DEN 1
 #endif
@@ -763,6 +766,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
         u32 pb = (u32)(((u64)blockIdx.x * (K3T_WARPS * K3T_CHAINS) + cid) * 97u % tp.K);
         u32 xb = 0;       // buffer holding our block (the other one receives loads)
         u32 dest = 0, slot = 0;
+        bool pb_ok = false;  // the last take from pb succeeded
         while (__any_sync(0xffffffffu, st != CH_DEAD)) {
 #if IPS4O_K3_DEFER
             // The same steps with the atomics' results consumed late: takes and claims are issued,
@@ -856,7 +860,12 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
             bool progressed = false;
             // ---- atomics: takes (FREE) and claims (HELD), one round trip for all chains
             if (st == CH_FREE) {
+#if IPS4O_K3_SKIPSCAN
+                // (the bucket the last take succeeded in is tried again without reading the done bits)
+                const u32 b = pb_ok ? pb : next_open_bucket(done, pb, tp.K);
+#else
                 const u32 b = next_open_bucket(done, pb, tp.K);
+#endif
                 if (b == 0xFFFFFFFFu) {
                     st = CH_DEAD;
                 } else {
@@ -872,6 +881,7 @@ __global__ void __launch_bounds__(K3T_THREADS) k_permute_tma(LevelArgs A0) {
                     const u64 old = atom_add_release_u64(ctl_wr(A.wr, t, pb), ~0ull);
 #endif
                     const int ow = (int)(u32)(old >> 32), orr = (int)((u32)old - RBIAS);
+                    pb_ok = orr >= ow;
                     if (orr < ow) {
                         atomicSub(ctl_readers(A.wr, t, pb), 1u);
                         atomicOr(&done[pb >> 5], 1u << (pb & 31));
