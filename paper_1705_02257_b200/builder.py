@@ -17,7 +17,8 @@ VARIANTS = {"cellE8": ["-DIPS4O_CELL_E=8"], "k3relaxed": ["-DIPS4O_K3_RELAXED=1"
             "bctawb": ["-DIPS4O_BASE_WARP_WB=0"], "r256": ["-DIPS4O_K2R_NT=256"],
             "k3w2": ["-DIPS4O_K3T_WARPS=2"],
                         "c3t512": ["-DIPS4O_CELL_NT3=512"], "cellminb4": ["-DIPS4O_CELL_MINB1=4"],
-            "nocelltile": ["-DIPS4O_CELL_TILE_CELLS=0"], "nofb2": ["-DIPS4O_FB_CELL2=0"], "pipe": ["-DIPS4O_BASE_PIPE=1"], "pred": ["-DIPS4O_BASE_PRED=1"], "m2x2": ["-DIPS4O_BASE_M2X2=1"], "k3nopf": ["-DIPS4O_K3_PF=0"], "k3defer": ["-DIPS4O_K3_DEFER=1"], "k3skip": ["-DIPS4O_K3_SKIPSCAN=1"], "k3pf2": ["-DIPS4O_K3_PF=2"],
+            "nocelltile": ["-DIPS4O_CELL_TILE_CELLS=0"], "nofb2": ["-DIPS4O_FB_CELL2=0"], "pipe": ["-DIPS4O_BASE_PIPE=1"], "pred": ["-DIPS4O_BASE_PRED=1"], "m2x2": ["-DIPS4O_BASE_M2X2=1"], "k3nopf": ["-DIPS4O_K3_PF=0"], "k3defer": ["-DIPS4O_K3_DEFER=1"], "k3skip": ["-DIPS4O_K3_SKIPSCAN=1"],
+            "c2_7168": ["-DIPS4O_CELL_C2MAX=7168"], "c2_8192": ["-DIPS4O_CELL_C2MAX=8192"], "k3pf2": ["-DIPS4O_K3_PF=2"],
             "k3pfh": ["-DIPS4O_K3_PF=1", "-DIPS4O_K3_PF_DEN=2"], "k3pfl2": ["-DIPS4O_K3_PF=1", "-DIPS4O_K3_PF_DEN=1000"],
             "k3pfm2": ["-DIPS4O_K3_PF=1", "-DIPS4O_K3_PF_MIN=2"],
             "leaf8k": ["-DIPS4O_LEAF8=8192"],

@@ -460,7 +460,7 @@ template <> struct CellWork<TQuad> {
 template <class TR, int NT, int E>
 struct CellMinB {
     static constexpr int v = sizeof(typename TR::V) == 8
-                                 ? (E >= 16 ? (NT <= 128 ? 6 : NT <= 256 ? IPS4O_CELL_MINB1 : NT <= 384 ? 2 : 1)
+                                 ? (E >= 16 ? (NT <= 128 ? 6 : NT <= 256 ? IPS4O_CELL_MINB1 : NT <= 512 ? 2 : 1)
                                             : (NT <= 128 ? 8 : NT <= 256 ? 4 : NT <= 512 ? 2 : 1))
                              : sizeof(typename TR::V) == 16 ? (NT <= 256 ? 3 : NT <= 512 ? 2 : 1)
                                                             : (NT <= 256 ? 2 : 1);
